@@ -1,0 +1,129 @@
+/*
+ * include/ht.h -- C ABI of the B200-native HouseHT library (libht_b200.so).
+ *
+ * Householder-based Hessenberg-triangular (HT) reduction of a real FP64 pencil
+ * A - lambda*B with B upper triangular (Bujanovic, Karlsson, Kressner,
+ * arXiv 1710.08538; PAPER.md).  The problem statement this ABI follows
+ * (sec. 1): find orthogonal Q, Z such that
+ *     H = Q^T A Z   is upper Hessenberg   and   T = Q^T B Z   is upper triangular,
+ * with B "already reduced to triangular form" and Q, Z "initialized to
+ * identity"; signature [H, T, Q, Z] = HouseHT(A, B) (Algorithm 1,
+ * P:1219).  The method is Algorithm 1: panels of nb columns
+ * reduced by left Householder reflectors and opposite (right) reflectors from
+ * a solve with B (sec. 3.2), accumulated in compact WY form and absorbed into
+ * A, B, Q, Z by staircase transformations (sec. 3.3).
+ *
+ * Conventions (all entry points):
+ *   - FP64 (IEEE binary64), column-major storage.
+ *   - On success A is overwritten by H (exact zeros below the first
+ *     sub-diagonal) and B by T (exact zeros below the diagonal).
+ *   - If wantq != 0, Q is OVERWRITTEN with the accumulated orthogonal factor
+ *     (initialised internally to I; Q e1 = e1).  If wantq == 0, Q may be NULL
+ *     and is never referenced.  Likewise Z / wantz.
+ *   - nb <= 0 selects the default 128; otherwise nb is clamped to
+ *     [1, min(256, max(1, n-2))].  nb changes speed, not the result beyond
+ *     rounding (the HT form is unique up to signs for nonsingular B).
+ *   - n = 0: nothing is touched, HT_OK.  n in {1, 2}: H = A, T = B, Q = Z = I.
+ *   - Iterative-refinement failures are NOT errors: they trigger a premature
+ *     absorption and are reported in ht_report.
+ *
+ * Error behaviour: arguments are validated before any write -- on a negative
+ * return code every buffer is untouched.  Positive codes are runtime errors
+ * after which buffer contents are unspecified (except HT_ENONFINITE and
+ * HT_EARG_B, detected before any write).
+ *
+ * Ownership: the caller owns A, B, Q, Z (host memory for ht_reduce, device
+ * memory for ht_reduce_ex).  The library owns its device workspace (cached per
+ * device, reused across calls) and keeps no caller pointer after returning.
+ * Calls on the same device are serialised by an internal mutex.
+ *
+ * No CPU fallback exists: without a CUDA device every entry point returns
+ * HT_ECUDA.
+ */
+#ifndef HT_B200_H
+#define HT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HT_API __attribute__((visibility("default")))
+#else
+#define HT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HT_OK = 0,
+    HT_EARG_N = -1,     /* n < 0 or too large                                  */
+    HT_EARG_A = -2,     /* A == NULL (n > 0) or lda < n                         */
+    HT_EARG_B = -3,     /* B == NULL, ldb < n, or B not upper triangular        */
+    HT_EARG_Q = -4,     /* wantq and (Q == NULL or ldq < n)                     */
+    HT_EARG_Z = -5,     /* wantz and (Z == NULL or ldz < n)                     */
+    HT_EARG_OPT = -8,   /* invalid ht_options                                   */
+    HT_ENONFINITE = 1,  /* A or B holds Inf/NaN (detected before any write)     */
+    HT_ECUDA = 2,       /* CUDA runtime error / no device                       */
+    HT_ENOMEM = 3,      /* device allocation failed                             */
+    HT_ENUMERIC = 4     /* internal numerical guard tripped (non-finite result) */
+};
+
+/* Options for ht_reduce_ex (zero-initialise, then set what you need). */
+typedef struct {
+    int64_t nb;            /* panel width; <= 0 -> 128                                   */
+    int max_ir;            /* max IR corrections per column; <= 0 -> 10          */
+    double tol_factor;     /* IR tolerance factor c in c*u*||B||_F; <= 0 -> 2    */
+    uint64_t seed;         /* seed of the desingularisation draws rho            */
+    void *stream;          /* cudaStream_t to run on (NULL: library stream)              */
+    const int64_t *force_ir_fail; /* host array of 0-based columns whose solve is forced
+                                     to fail IR (test hook for premature absorption)   */
+    int64_t n_force_ir_fail;
+} ht_options;
+
+/* Statistics of one reduction (the paper's Table 3/4 columns). */
+typedef struct {
+    double seconds;            /* wall time of the reduction (device events)           */
+    double flops;              /* executed FP64 flops, instrumented      */
+    double flops_level3;       /* part of `flops` executed by the DMMA GEMM            */
+    int64_t panels;            /* panel reductions run                                  */
+    int64_t absorptions;       /* absorptions (= panels)                                */
+    int64_t premature_absorptions; /* absorptions triggered by an IR failure            */
+    int64_t ir_steps_total;    /* IR correction solves                                  */
+    int64_t ir_extra_columns;  /* columns that needed >= 1 IR correction               */
+    int64_t ir_failed_columns; /* columns whose IR failed (premature absorption)        */
+    int64_t desingularizations;/* zero pivots replaced by 2u*rho*||B||_F                */
+    int64_t solve_rescales;    /* triangular solves that needed power-of-two rescaling  */
+    double t_panel, t_absorb;  /* seconds in panel kernels / absorption                 */
+} ht_report;
+
+/*
+ * North-star entry point (host memory).  A, B, Q, Z are n x n, column-major
+ * with leading dimension n.  Synchronous: copies to the device, reduces,
+ * copies back.  Returns HT_OK or an error code above.
+ */
+HT_API int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb);
+
+/*
+ * Device-memory entry point.  dA, dB, dQ, dZ are device pointers with leading
+ * dimensions ldda.. >= n.  Runs on opt->stream (or the library stream) and
+ * returns after the reduction completed on the device.  opt and rep may be
+ * NULL.  rep (if given) is filled on return.
+ */
+HT_API int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq,
+                 double *dZ, int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep);
+
+/* Human-readable text for a return code (static storage). */
+HT_API const char *ht_strerror(int code);
+
+/* Library version: major*10000 + minor*100 + patch. */
+HT_API int ht_version(void);
+
+/* Release the cached device workspace of the current device. Returns HT_OK. */
+HT_API int ht_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HT_B200_H */

@@ -1,0 +1,150 @@
+"""B200-native Householder Hessenberg-triangular reduction (arXiv 1710.08538, "HouseHT").
+
+Thin ctypes binding over the C ABI in include/ht.h (libht_b200.so, built for
+sm_100a by paper_1710_08538_b200/build.py).  Argument marshalling only: every
+step of the reduction runs in the library's CUDA kernels.  There is no CPU
+fallback -- if the library or a CUDA device is missing, calls raise.
+
+Names follow the ABI:
+    ht_reduce(A, B, nb=..., wantq=True, wantz=True)          host numpy arrays
+    ht_reduce_ex(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz,   raw device pointers
+                 wantq, wantz, options=None)
+plus reduce_device(A, B, Q, Z, ...) for torch CUDA tensors holding column-major
+matrices (a column-major n x n matrix M is the row-major tensor M^T).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
+
+HT_OK = 0
+ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
+          -8: "HT_EARG_OPT", 1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC"}
+EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release_workspace")
+
+
+class HTOptions(ctypes.Structure):
+    _fields_ = [("nb", ctypes.c_int64), ("max_ir", ctypes.c_int), ("tol_factor", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
+                ("force_ir_fail", ctypes.POINTER(ctypes.c_int64)), ("n_force_ir_fail", ctypes.c_int64)]
+
+
+class HTReport(ctypes.Structure):
+    _fields_ = [("seconds", ctypes.c_double), ("flops", ctypes.c_double), ("flops_level3", ctypes.c_double),
+                ("panels", ctypes.c_int64), ("absorptions", ctypes.c_int64),
+                ("premature_absorptions", ctypes.c_int64), ("ir_steps_total", ctypes.c_int64),
+                ("ir_extra_columns", ctypes.c_int64), ("ir_failed_columns", ctypes.c_int64),
+                ("desingularizations", ctypes.c_int64), ("solve_rescales", ctypes.c_int64),
+                ("t_panel", ctypes.c_double), ("t_absorb", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class HTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library():
+    """Load libht_b200.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_1710_08538_b200/build.py (or __graft_entry__.build())")
+        lib = ctypes.CDLL(LIB_PATH)
+        i64, P = ctypes.c_int64, ctypes.c_void_p
+        lib.ht_reduce.restype = ctypes.c_int
+        lib.ht_reduce.argtypes = [i64, P, P, P, P, ctypes.c_int, ctypes.c_int, i64]
+        lib.ht_reduce_ex.restype = ctypes.c_int
+        lib.ht_reduce_ex.argtypes = [i64, P, i64, P, i64, P, i64, P, i64, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(HTOptions), ctypes.POINTER(HTReport)]
+        lib.ht_strerror.restype = ctypes.c_char_p
+        lib.ht_strerror.argtypes = [ctypes.c_int]
+        lib.ht_version.restype = ctypes.c_int
+        lib.ht_version.argtypes = []
+        lib.ht_release_workspace.restype = ctypes.c_int
+        lib.ht_release_workspace.argtypes = []
+        _lib = lib
+    return _lib
+
+
+def ht_strerror(code: int) -> str:
+    return load_library().ht_strerror(code).decode()
+
+
+def ht_version() -> int:
+    return load_library().ht_version()
+
+
+def ht_release_workspace() -> int:
+    return load_library().ht_release_workspace()
+
+
+def _check(rc: int):
+    if rc != HT_OK:
+        raise HTError(rc, ht_strerror(rc))
+
+
+def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True):
+    """Host entry point: returns (H, T, Q, Z) as Fortran-ordered float64 arrays."""
+    lib = load_library()
+    H = np.array(A, dtype=np.float64, order="F", copy=True)
+    T = np.array(B, dtype=np.float64, order="F", copy=True)
+    n = H.shape[0]
+    if H.shape != (n, n) or T.shape != (n, n):
+        raise ValueError("A and B must be square and of equal size")
+    Q = np.zeros((n, n), order="F") if wantq else None
+    Z = np.zeros((n, n), order="F") if wantz else None
+    ptr = lambda a: a.ctypes.data if a is not None else None
+    _check(lib.ht_reduce(n, ptr(H), ptr(T), ptr(Q), ptr(Z), int(wantq), int(wantz), int(nb)))
+    return H, T, Q, Z
+
+
+def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=()):
+    opt = HTOptions()
+    opt.nb = int(nb)
+    opt.max_ir = int(max_ir)
+    opt.tol_factor = float(tol_factor)
+    opt.seed = int(seed)
+    opt.stream = stream
+    if force_ir_fail:
+        arr = (ctypes.c_int64 * len(force_ir_fail))(*[int(c) for c in force_ir_fail])
+        opt._keep = arr
+        opt.force_ir_fail = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+        opt.n_force_ir_fail = len(force_ir_fail)
+    return opt
+
+
+def ht_reduce_ex(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq=True, wantz=True, options=None):
+    """Device entry point on raw pointers (ints). Returns the ht_report as a dict."""
+    lib = load_library()
+    rep = HTReport()
+    opt = options if options is not None else make_options()
+    _check(lib.ht_reduce_ex(int(n), dA, int(ldda), dB, int(lddb), dQ, int(lddq), dZ, int(lddz),
+                            int(wantq), int(wantz), ctypes.byref(opt), ctypes.byref(rep)))
+    return rep.as_dict()
+
+
+def reduce_device(A, B, Q=None, Z=None, nb=0, stream=None, **kw):
+    """In-place reduction of torch CUDA tensors holding column-major matrices
+    (tensor t with t[j, i] = M[i, j], i.e. t = M^T row-major). Returns the report."""
+    n = A.shape[0]
+    for t in (A, B, Q, Z):
+        if t is not None:
+            assert t.is_cuda and t.is_contiguous() and t.shape == (n, n)
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    opt = make_options(nb=nb, stream=stream, **kw)
+    p = lambda t: t.data_ptr() if t is not None else None
+    return ht_reduce_ex(n, p(A), n, p(B), n, p(Q), n, p(Z), n, Q is not None, Z is not None, opt)

@@ -1,0 +1,694 @@
+// ht_driver.cu -- host driver of HouseHT (Algorithm 1) and the C ABI.
+//
+// The driver is the runtime around the kernels: it owns the device workspace,
+// launches the persistent panel kernel (sec. 3.2), and sequences the
+// absorption (sec. 3.3) as staircase window factorizations (ht_factor.cu) and
+// FP64 tensor-core GEMMs (ht_gemm.cu).  All arithmetic on the data runs in
+// those kernels; the host only computes indices and pointers.
+//
+// Readings of the paper:
+//   R-Z9  after an IR failure the next panel restarts AT the failed column (text P:497).
+//   R-Z10 reflectors pending at the end of the loop are absorbed.
+//   R-Z11 when m = n-j <= 2k the absorption is done explicitly (two-sided compact
+//         WY + one dense QR of the trailing m x m block of B).
+//   Remark 4: first right window has kt rows, k < kt <= 2k, k | (m-kt);
+//         restore chunks are aligned to the window boundaries.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/ht.h"
+#include "ht_common.cuh"
+#include "ht_internal.h"
+
+namespace {
+
+#define TRY(x)                     \
+    do {                           \
+        int _rc = (x);             \
+        if (_rc) return _rc;       \
+    } while (0)
+
+struct Work {
+    int dev = -1;
+    int64_t ncap = 0, nbcap = 0;
+    int gmax = 0;
+    cudaStream_t own_stream = nullptr;
+    double *U = nullptr, *V = nullptr, *Y = nullptr, *S = nullptr, *T = nullptr;
+    double *vec = nullptr, *part = nullptr;
+    unsigned *flags = nullptr;
+    int *bexp = nullptr;
+    unsigned epoch = 0;
+    int64_t *d_out = nullptr, *h_out = nullptr;
+    double *d_scal = nullptr, *h_scal = nullptr;
+    int *d_iflags = nullptr, *h_iflags = nullptr;
+    double *VW = nullptr, *UW = nullptr;
+    double *Vhat = nullptr, *tau = nullptr, *Gm = nullptr, *Tm = nullptr, *Wt = nullptr, *Qw = nullptr;
+    double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
+    int64_t *d_force = nullptr;
+    FactorDesc *d_fd = nullptr, *h_fd = nullptr;
+    LarftDesc *d_ld = nullptr, *h_ld = nullptr;
+    int64_t ndesc = 0, fd_cur = 0, ld_cur = 0;
+};
+
+std::mutex g_mu;
+Work g_work[16];
+
+void work_free(Work &w)
+{
+    double **dp[] = {&w.U, &w.V, &w.Y, &w.S, &w.T, &w.vec, &w.part, &w.VW, &w.UW, &w.Vhat, &w.tau,
+                     &w.Gm, &w.Tm, &w.Wt, &w.Qw, &w.tmp, &w.W1, &w.W2, &w.UR, &w.fscr, &w.d_scal};
+    for (auto p : dp)
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    if (w.flags) cudaFree(w.flags);
+    if (w.bexp) cudaFree(w.bexp);
+    if (w.d_out) cudaFree(w.d_out);
+    if (w.d_iflags) cudaFree(w.d_iflags);
+    if (w.d_force) cudaFree(w.d_force);
+    if (w.d_fd) cudaFree(w.d_fd);
+    if (w.d_ld) cudaFree(w.d_ld);
+    if (w.h_out) cudaFreeHost(w.h_out);
+    if (w.h_scal) cudaFreeHost(w.h_scal);
+    if (w.h_iflags) cudaFreeHost(w.h_iflags);
+    if (w.h_fd) cudaFreeHost(w.h_fd);
+    if (w.h_ld) cudaFreeHost(w.h_ld);
+    w.flags = nullptr; w.bexp = nullptr; w.d_out = nullptr; w.d_iflags = nullptr; w.d_force = nullptr;
+    w.d_fd = nullptr; w.d_ld = nullptr; w.h_out = nullptr; w.h_scal = nullptr; w.h_iflags = nullptr;
+    w.h_fd = nullptr; w.h_ld = nullptr;
+    w.ncap = w.nbcap = 0;
+}
+
+int dalloc(double **p, size_t count)
+{
+    if (cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(double)) != cudaSuccess) return HT_ENOMEM;
+    return 0;
+}
+
+int work_get(int dev, int64_t n, int64_t nb, Work **out)
+{
+    if (dev < 0 || dev >= 16) return HT_ECUDA;
+    Work &w = g_work[dev];
+    if (w.ncap >= n && w.nbcap >= nb && w.ncap > 0) {
+        *out = &w;
+        return 0;
+    }
+    work_free(w);
+    w.dev = dev;
+    if (!w.own_stream && cudaStreamCreateWithFlags(&w.own_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return HT_ECUDA;
+    const int64_t N = std::max<int64_t>(n, 8), NB = std::max<int64_t>(nb, 1);
+    TRY(ht_panel_max_blocks(&w.gmax));
+    const size_t nnb = (size_t)N * NB, nb2 = (size_t)NB * NB;
+    TRY(dalloc(&w.U, nnb)); TRY(dalloc(&w.V, nnb)); TRY(dalloc(&w.Y, nnb));
+    TRY(dalloc(&w.S, nb2)); TRY(dalloc(&w.T, nb2));
+    TRY(dalloc(&w.vec, 8 * (size_t)N));
+    TRY(dalloc(&w.part, 2 * (size_t)w.gmax * (NB + 8)));
+    const size_t nblk = (size_t)(N / 64 + 4);
+    if (cudaMalloc((void **)&w.flags, nblk * sizeof(unsigned)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.bexp, nblk * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    cudaMemset(w.flags, 0, nblk * sizeof(unsigned));
+    w.epoch = 1;
+    if (cudaMalloc((void **)&w.d_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
+    TRY(dalloc(&w.d_scal, 8));
+    if (cudaMallocHost((void **)&w.h_scal, 8 * sizeof(double)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.d_iflags, 8 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_iflags, 8 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    TRY(dalloc(&w.VW, nnb)); TRY(dalloc(&w.UW, nnb));
+    TRY(dalloc(&w.Vhat, 2 * nnb + 4 * nb2));
+    TRY(dalloc(&w.Wt, 2 * nnb + 4 * nb2));
+    TRY(dalloc(&w.tau, (size_t)N + 2 * NB));
+    TRY(dalloc(&w.Gm, nnb + 2 * nb2));
+    TRY(dalloc(&w.Tm, nnb + 2 * nb2));
+    TRY(dalloc(&w.Qw, 4 * nnb + 8 * nb2));
+    TRY(dalloc(&w.tmp, 3 * (size_t)N * 2 * NB));
+    TRY(dalloc(&w.W1, nnb + 4 * nb2)); TRY(dalloc(&w.W2, nnb + 4 * nb2));
+    TRY(dalloc(&w.UR, 2 * nb2));
+    TRY(dalloc(&w.fscr, 4 * nb2 + 64));
+    if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
+    w.ndesc = 4 * (N + 16);
+    if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
+    w.ncap = N;
+    w.nbcap = NB;
+    *out = &w;
+    return 0;
+}
+
+// One reduction in flight.
+struct Run {
+    Work *w;
+    cudaStream_t st;
+    int64_t n, nb;
+    double *A, *B, *Q, *Z;
+    int64_t lda, ldb, ldq, ldz;
+    bool wq, wz;
+    ht_report rep;
+    double extra_flops = 0.0;
+
+    // ---------------- helpers --------------------------------------------
+    int gemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double al, const double *Ap, int64_t la,
+             const double *Bp, int64_t lb, double be, double *Cp, int64_t lc)
+    {
+        return ht_gemm(st, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
+    }
+    // X(rows, c0:c0+nc) <- X (I - Vp T Vp^T), Vp nc x k (ld ldv)
+    int right_wy(double *X, int64_t ldx, int64_t rows, int64_t c0, int64_t nc, const double *Vp, int64_t ldv,
+                 const double *Tp, int64_t ldt, int64_t k)
+    {
+        TRY(gemm('N', 'N', rows, k, nc, 1.0, X + c0 * ldx, ldx, Vp, ldv, 0.0, w->W1, n));
+        TRY(gemm('N', 'N', rows, k, k, 1.0, w->W1, n, Tp, ldt, 0.0, w->W2, n));
+        TRY(gemm('N', 'T', rows, nc, k, -1.0, w->W2, n, Vp, ldv, 1.0, X + c0 * ldx, ldx));
+        return 0;
+    }
+    // X(r0:r0+nr, c0:c0+nc) <- (I - Up S^T Up^T) X   (the transposed left WY, eq. tildeB)
+    int left_wy(double *X, int64_t ldx, int64_t r0, int64_t nr, int64_t c0, int64_t nc, const double *Up, int64_t ldu,
+                const double *Sp, int64_t lds, int64_t k)
+    {
+        double *Xp = X + r0 + c0 * ldx;
+        TRY(gemm('T', 'N', k, nc, nr, 1.0, Up, ldu, Xp, ldx, 0.0, w->W1, k));
+        TRY(gemm('T', 'N', k, nc, k, 1.0, Sp, lds, w->W1, k, 0.0, w->W2, k));
+        TRY(gemm('N', 'N', nr, nc, k, -1.0, Up, ldu, w->W2, k, 1.0, Xp, ldx));
+        return 0;
+    }
+
+    // Window bookkeeping for one chain: packed offsets into Vhat/Qw/Gm/Tm/tau.
+    struct Win {
+        int p, q;
+        size_t ov, oq, og, ot;
+    };
+    std::vector<Win> wins;
+    void wins_reset() { wins.clear(); }
+    Win add_win(int p, int q)
+    {
+        Win x{p, q, 0, 0, 0, 0};
+        if (!wins.empty()) {
+            const Win &b = wins.back();
+            x.ov = b.ov + (size_t)b.p * b.q;
+            x.oq = b.oq + (size_t)b.p * b.p;
+            x.og = b.og + (size_t)b.q * b.q;
+            x.ot = b.ot + (size_t)b.q;
+        }
+        wins.push_back(x);
+        return x;
+    }
+
+    // Factor windows [i0, i1) of `wins` (descs in h_fd at fd_cur..), then form Qw for them.
+    int factor_and_form(const std::vector<FactorDesc> &fds, size_t i0)
+    {
+        const int nd = (int)fds.size();
+        if (nd == 0) return 0;
+        if (w->fd_cur + nd > w->ndesc || w->ld_cur + nd > w->ndesc) return HT_ENUMERIC;
+        FactorDesc *hf = w->h_fd + w->fd_cur;
+        LarftDesc *hl = w->h_ld + w->ld_cur;
+        int maxpq = 0;
+        for (int i = 0; i < nd; ++i) {
+            hf[i] = fds[i];
+            maxpq = std::max(maxpq, fds[i].p * fds[i].q);
+            const Win &x = wins[i0 + i];
+            hl[i] = LarftDesc{w->Gm + x.og, x.q, w->tau + x.ot, w->Tm + x.og, x.q, x.q};
+            extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
+        }
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, st));
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_ld + w->ld_cur, hl, nd * sizeof(LarftDesc), cudaMemcpyHostToDevice, st));
+        TRY(ht_factor_run(st, w->d_fd + w->fd_cur, nd, w->fscr, maxpq));
+        // G = V^T V
+        std::vector<GemmBatchItem> it(nd);
+        for (int i = 0; i < nd; ++i) {
+            const Win &x = wins[i0 + i];
+            it[i] = GemmBatchItem{w->Vhat + x.ov, w->Vhat + x.ov, w->Gm + x.og, x.p, x.p, x.q,
+                                  x.q, x.q, x.p, 1.0, 0.0, 0.0};
+        }
+        TRY(ht_gemm_multi(st, 'T', 'N', it.data(), nd));
+        TRY(ht_larft_run(st, w->d_ld + w->ld_cur, nd));
+        // Wt = V T
+        for (int i = 0; i < nd; ++i) {
+            const Win &x = wins[i0 + i];
+            it[i] = GemmBatchItem{w->Vhat + x.ov, w->Tm + x.og, w->Wt + x.ov, x.p, x.q, x.p,
+                                  x.p, x.q, x.q, 1.0, 0.0, 0.0};
+        }
+        TRY(ht_gemm_multi(st, 'N', 'N', it.data(), nd));
+        // Qw = I - Wt V^T
+        for (int i = 0; i < nd; ++i) {
+            const Win &x = wins[i0 + i];
+            it[i] = GemmBatchItem{w->Wt + x.ov, w->Vhat + x.ov, w->Qw + x.oq, x.p, x.p, x.p,
+                                  x.p, x.p, x.q, -1.0, 0.0, 1.0};
+        }
+        TRY(ht_gemm_multi(st, 'N', 'T', it.data(), nd));
+        w->fd_cur += nd;
+        w->ld_cur += nd;
+        return 0;
+    }
+
+    struct Tgt {
+        double *X;
+        int64_t ldx, r0, rows, c0, cols;  // right: rows r0..r0+rows, cols c0..c0+p ; left: rows r0..r0+p, cols c0..
+    };
+    // X(r0:, c0:c0+p) <- X(...) Qw  for each target
+    int apply_right(const std::vector<Tgt> &tg, const double *Qwp, int p)
+    {
+        std::vector<GemmBatchItem> it;
+        for (size_t i = 0; i < tg.size(); ++i) {
+            if (tg[i].rows <= 0) continue;
+            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
+            it.push_back(GemmBatchItem{tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, Qwp, tmp, tg[i].ldx, p, tg[i].rows,
+                                       (int)tg[i].rows, p, p, 1.0, 0.0, 0.0});
+        }
+        TRY(ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size()));
+        for (size_t i = 0; i < tg.size(); ++i) {
+            if (tg[i].rows <= 0) continue;
+            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
+            TRY(ht_copy2d(st, tg[i].rows, p, tmp, tg[i].rows, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
+        }
+        return 0;
+    }
+    // X(r0:r0+p, c0:c0+cols) <- Qw^T X(...)
+    int apply_left(const std::vector<Tgt> &tg, const double *Qwp, int p)
+    {
+        std::vector<GemmBatchItem> it;
+        for (size_t i = 0; i < tg.size(); ++i) {
+            if (tg[i].cols <= 0) continue;
+            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
+            it.push_back(GemmBatchItem{Qwp, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tmp, p, tg[i].ldx, p, p,
+                                       (int)tg[i].cols, p, 1.0, 0.0, 0.0});
+        }
+        TRY(ht_gemm_multi(st, 'T', 'N', it.data(), (int)it.size()));
+        for (size_t i = 0; i < tg.size(); ++i) {
+            if (tg[i].cols <= 0) continue;
+            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
+            TRY(ht_copy2d(st, p, tg[i].cols, tmp, p, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
+        }
+        return 0;
+    }
+
+    // ---------------- absorption (sec. 3.3) ---------------------------------
+    int absorb(int64_t s0, int64_t k)
+    {
+        const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
+        double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
+        w->fd_cur = w->ld_cur = 0;
+        // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns
+        TRY(gemm('N', 'N', p0, k, n - p0, 1.0, A + p0 * lda, lda, V + p0, n, 0.0, w->W1, n));
+        TRY(gemm('N', 'N', p0, k, k, 1.0, w->W1, n, T, nb, 0.0, Y, n));
+        if (J > p0) TRY(gemm('N', 'T', p0, J - p0, k, -1.0, Y, n, V + p0, n, 1.0, A + p0 * lda, lda));
+        if (m <= 2 * k) return absorb_tail(s0, k);
+
+        // geometry (Remark 4): right boundaries rb = {0, kt-k, kt, ..., m}
+        const int64_t rem = (m - k) % k;
+        const int64_t kt = k + (rem == 0 ? k : rem);
+        const int r = (int)((m - kt) / k + 1);
+        std::vector<int64_t> rb(r + 2), lb(r + 2);
+        rb[0] = 0;
+        for (int t = 1; t <= r + 1; ++t) rb[t] = kt - k + (int64_t)(t - 1) * k;
+        for (int t = 0; t <= r + 1; ++t) lb[t] = m - rb[r + 1 - t];
+        const int64_t ldw = n;  // VW/UW leading dimension
+        TRY(ht_copy2d(st, m, k, V + J + 1, n, w->VW, ldw));
+        TRY(ht_copy2d(st, m, k, U + J + 1, n, w->UW, ldw));
+        const int K = (int)k;
+
+        // ===== R1: QL staircase of V2, top -> bottom (sec. 3.3.1b) =====
+        wins_reset();
+        std::vector<FactorDesc> fds;
+        for (int i = 0; i < r; ++i) {
+            const int p = (int)(rb[i + 2] - rb[i]);
+            Win x = add_win(p, K);
+            fds.push_back(FactorDesc{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1,
+                                     w->Vhat + x.ov, p, w->tau + x.ot});
+        }
+        TRY(factor_and_form(fds, 0));
+        // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e) =====
+        for (int i = 0; i < r; ++i) {
+            const Win &x = wins[i];
+            const int64_t c0 = J + 1 + rb[i];
+            std::vector<Tgt> tg;
+            tg.push_back(Tgt{B, ldb, 0, J + 1 + rb[i + 2], c0, 0});
+            tg.push_back(Tgt{A, lda, 0, n, c0, 0});
+            if (wz) tg.push_back(Tgt{Z, ldz, 0, n, c0, 0});
+            TRY(apply_right(tg, w->Qw + x.oq, x.p));
+        }
+        const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
+        {
+            double *Xs[2] = {B, wz ? Z : nullptr};
+            int64_t lds[2] = {ldb, ldz};
+            for (int q = 0; q < 2; ++q) {
+                double *X = Xs[q];
+                if (!X) continue;
+                const int64_t ldx = lds[q];
+                TRY(gemm('N', 'N', n, k, k, 1.0, X + p0 * ldx, ldx, V + p0, n, 0.0, w->W1, n));
+                TRY(gemm('N', 'N', n, k, k, 1.0, X + (n - k) * ldx, ldx, L1, ldw, 1.0, w->W1, n));
+                TRY(gemm('N', 'N', n, k, k, 1.0, w->W1, n, T, nb, 0.0, w->W2, n));
+                TRY(gemm('N', 'T', n, k, k, -1.0, w->W2, n, V + p0, n, 1.0, X + p0 * ldx, ldx));
+                TRY(gemm('N', 'T', n, k, k, -1.0, w->W2, n, L1, ldw, 1.0, X + (n - k) * ldx, ldx));
+            }
+            TRY(gemm('N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
+            TRY(gemm('N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
+        }
+        // ===== R3: RQ staircase restoring B, bottom -> top (sec. 3.3.1 second "e)") =====
+        for (int t = r; t >= 0; --t) {
+            int64_t R0, h, C0, wdt;
+            if (t >= 1) {
+                R0 = J + 1 + rb[t];
+                h = rb[t + 1] - rb[t];
+                C0 = J + 1 + rb[t - 1];
+                wdt = rb[t + 1] - rb[t - 1];
+            } else {
+                R0 = J + 1;
+                h = rb[1];
+                C0 = J + 1;
+                wdt = h;
+            }
+            if (wdt <= 1) continue;
+            wins_reset();
+            Win x = add_win((int)wdt, (int)h);
+            std::vector<FactorDesc> f1{FactorDesc{B + (R0 + h - 1) + (C0 + wdt - 1) * ldb, -ldb, -1, (int)wdt, (int)h,
+                                                  1, w->Vhat + x.ov, wdt, w->tau + x.ot}};
+            TRY(factor_and_form(f1, 0));
+            std::vector<Tgt> tg;
+            tg.push_back(Tgt{B, ldb, 0, R0, C0, 0});
+            tg.push_back(Tgt{A, lda, 0, n, C0, 0});
+            if (wz) tg.push_back(Tgt{Z, ldz, 0, n, C0, 0});
+            TRY(apply_right(tg, w->Qw + x.oq, (int)wdt));
+        }
+        // ===== L1: QR staircase of U2, bottom -> top (sec. 3.3.2b) =====
+        wins_reset();
+        fds.clear();
+        for (int i = 0; i < r; ++i) {
+            const int64_t top = lb[r - 1 - i], bot = lb[r + 1 - i];
+            const int p = (int)(bot - top);
+            Win x = add_win(p, K);
+            fds.push_back(FactorDesc{w->UW + top, 1, ldw, p, K, 0, w->Vhat + x.ov, p, w->tau + x.ot});
+        }
+        TRY(factor_and_form(fds, 0));
+        // ===== L2: spike, chain on B, A, Q, W-updates =====
+        TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
+        TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
+        TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
+        TRY(ht_zero_lower(st, n - p0, k, B + p0 + p0 * ldb, ldb, 0));
+        for (int i = 0; i < r; ++i) {
+            const Win &x = wins[i];
+            const int64_t R0 = J + 1 + lb[r - 1 - i];
+            std::vector<Tgt> tg;
+            tg.push_back(Tgt{B, ldb, R0, 0, R0, n - R0});
+            tg.push_back(Tgt{A, lda, R0, 0, J, n - J});
+            TRY(apply_left(tg, w->Qw + x.oq, x.p));
+            if (wq) {
+                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
+                TRY(apply_right(tq, w->Qw + x.oq, x.p));
+            }
+        }
+        // UR = [U1; R~1]  (2k x k)
+        const int64_t ldur = 2 * k;
+        TRY(ht_copy2d(st, k, k, U + p0, n, w->UR, ldur));
+        TRY(ht_copy2d(st, k, k, w->UW, ldw, w->UR + k, ldur));
+        TRY(ht_zero_lower(st, k, k, w->UR + k, ldur, 0));
+        {
+            // B(p0:p0+2k, J+1:n) and A(p0:p0+2k, J:n):  X <- X - UR S^T (X^T UR)^T
+            struct LX { double *X; int64_t ld, c0; } lx[2] = {{B, ldb, J + 1}, {A, lda, J}};
+            for (auto &e : lx) {
+                const int64_t nc = n - e.c0;
+                double *Xp = e.X + p0 + e.c0 * e.ld;
+                TRY(gemm('T', 'N', nc, k, 2 * k, 1.0, Xp, e.ld, w->UR, ldur, 0.0, w->W1, n));
+                TRY(gemm('N', 'N', nc, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
+                TRY(gemm('N', 'T', 2 * k, nc, k, -1.0, w->UR, ldur, w->W2, n, 1.0, Xp, e.ld));
+            }
+            if (wq) {  // Q(:, p0:p0+2k) <- Q (I - UR S UR^T)
+                double *Xp = Q + p0 * ldq;
+                TRY(gemm('N', 'N', n, k, 2 * k, 1.0, Xp, ldq, w->UR, ldur, 0.0, w->W1, n));
+                TRY(gemm('N', 'N', n, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
+                TRY(gemm('N', 'T', n, 2 * k, k, -1.0, w->W2, n, w->UR, ldur, 1.0, Xp, ldq));
+            }
+        }
+        // ===== L3: QR staircase restoring B, top -> bottom (sec. 3.3.2f) =====
+        for (int t = 0; t <= r; ++t) {
+            const int64_t R0 = J + 1 + lb[t];
+            const int64_t q = lb[t + 1] - lb[t];
+            const int64_t p = (t < r) ? lb[t + 2] - lb[t] : q;
+            if (p <= 1) continue;
+            wins_reset();
+            Win x = add_win((int)p, (int)q);
+            std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)p, (int)q, 0, w->Vhat + x.ov, p,
+                                                  w->tau + x.ot}};
+            TRY(factor_and_form(f1, 0));
+            std::vector<Tgt> tg;
+            tg.push_back(Tgt{B, ldb, R0, 0, R0 + q, n - (R0 + q)});
+            tg.push_back(Tgt{A, lda, R0, 0, J, n - J});
+            TRY(apply_left(tg, w->Qw + x.oq, (int)p));
+            if (wq) {
+                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
+                TRY(apply_right(tq, w->Qw + x.oq, (int)p));
+            }
+        }
+        return 0;
+    }
+
+    // Reading R-Z11: explicit absorption when m <= 2k.
+    int absorb_tail(int64_t s0, int64_t k)
+    {
+        const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
+        double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
+        // right: A(:, J:n) -= Y V(J:n,:)^T ; B, Z <- . (I - V T V^T)
+        TRY(gemm('N', 'T', n, n - J, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
+        TRY(right_wy(B, ldb, n, p0, n - p0, V + p0, n, T, nb, k));
+        if (wz) TRY(right_wy(Z, ldz, n, p0, n - p0, V + p0, n, T, nb, k));
+        // left: A(p0:n, J:n), B(p0:n, p0:n) <- (I - U S^T U^T) . ; Q <- Q (I - U S U^T)
+        TRY(left_wy(A, lda, p0, n - p0, J, n - J, U + p0, n, S, nb, k));
+        TRY(left_wy(B, ldb, p0, n - p0, p0, n - p0, U + p0, n, S, nb, k));
+        TRY(ht_zero_lower(st, n - p0, k, B + p0 + p0 * ldb, ldb, 0));  // Fact 3
+        if (wq) TRY(right_wy(Q, ldq, n, p0, n - p0, U + p0, n, S, nb, k));
+        if (m >= 2) {
+            const int64_t R0 = J + 1;
+            wins_reset();
+            Win x = add_win((int)m, (int)m);
+            std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)m, (int)m, 0, w->Vhat + x.ov, m,
+                                                  w->tau + x.ot}};
+            TRY(factor_and_form(f1, 0));
+            std::vector<Tgt> tg{Tgt{A, lda, R0, 0, J, n - J}};
+            TRY(apply_left(tg, w->Qw + x.oq, (int)m));
+            if (wq) {
+                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
+                TRY(apply_right(tq, w->Qw + x.oq, (int)m));
+            }
+        }
+        return 0;
+    }
+};
+
+int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, const double *Q, int64_t ldq,
+             const double *Z, int64_t ldz, int wantq, int wantz, const ht_options *opt)
+{
+    if (n < 0 || n > (int64_t)1 << 20) return HT_EARG_N;
+    if (n > 0 && (!A || lda < n)) return HT_EARG_A;
+    if (n > 0 && (!B || ldb < n)) return HT_EARG_B;
+    if (n > 0 && wantq && (!Q || ldq < n)) return HT_EARG_Q;
+    if (n > 0 && wantz && (!Z || ldz < n)) return HT_EARG_Z;
+    if (opt && opt->n_force_ir_fail > 0 && !opt->force_ir_fail) return HT_EARG_OPT;
+    return 0;
+}
+
+double panel_flops(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
+{
+    const double M = (double)(n - s0 - 1);
+    double f = 0.0;
+    for (int64_t i = 0; i < k; ++i) {
+        const double j0 = (double)(s0 + i);
+        f += M * M;                                 // factored solve (trsv)
+        if (i > 0) f += M * M;                      // residual (trmv)
+        f += 2.0 * M * (n - j0 - 1);                // A v
+        f += (4.0 * n + 22.0 * M) * (double)i;      // small WY terms
+    }
+    f += 2.0 * M * M * (double)ir_steps;            // IR: solve + residual
+    return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ht_strerror(int code)
+{
+    switch (code) {
+    case HT_OK: return "ok";
+    case HT_EARG_N: return "invalid n";
+    case HT_EARG_A: return "invalid A / lda";
+    case HT_EARG_B: return "invalid B / ldb, or B not upper triangular";
+    case HT_EARG_Q: return "invalid Q / ldq";
+    case HT_EARG_Z: return "invalid Z / ldz";
+    case HT_EARG_OPT: return "invalid options";
+    case HT_ENONFINITE: return "A or B contains Inf/NaN";
+    case HT_ECUDA: return "CUDA error or no CUDA device";
+    case HT_ENOMEM: return "device allocation failed";
+    case HT_ENUMERIC: return "internal numerical guard";
+    default: return "unknown error";
+    }
+}
+
+int ht_version(void) { return 100; }
+
+int ht_release_workspace(void)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return HT_ECUDA;
+    if (dev >= 0 && dev < 16) work_free(g_work[dev]);
+    return HT_OK;
+}
+
+int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
+                 int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep)
+{
+    int rc = validate(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt);
+    if (rc) return rc;
+    if (n == 0) {
+        if (rep) memset(rep, 0, sizeof(*rep));
+        return HT_OK;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    HT_CUDA_TRY(cudaGetDevice(&dev));
+    int64_t nb = (opt && opt->nb > 0) ? opt->nb : 128;
+    nb = std::max<int64_t>(1, std::min<int64_t>({nb, 256, std::max<int64_t>(1, n - 2)}));
+    Work *w = nullptr;
+    TRY(work_get(dev, n, nb, &w));
+    Run R;
+    memset(&R.rep, 0, sizeof(R.rep));
+    R.w = w;
+    R.st = (opt && opt->stream) ? (cudaStream_t)opt->stream : w->own_stream;
+    R.n = n; R.nb = nb;
+    R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
+    R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
+    R.wq = wantq != 0; R.wz = wantz != 0;
+    cudaStream_t st = R.st;
+    g_ht_flops = 0.0;
+
+    // validation that needs the data: finite entries, B upper triangular (before any write)
+    TRY(ht_check_input(st, n, dA, ldda, dB, lddb, w->d_iflags));
+    HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    HT_CUDA_TRY(cudaStreamSynchronize(st));
+    if (w->h_iflags[0]) return HT_ENONFINITE;
+    if (w->h_iflags[1]) return HT_EARG_B;
+
+    cudaEvent_t e0, e1;
+    HT_CUDA_TRY(cudaEventCreate(&e0));
+    HT_CUDA_TRY(cudaEventCreate(&e1));
+    HT_CUDA_TRY(cudaEventRecord(e0, st));
+    if (R.wq) TRY(ht_fill2d(st, n, n, dQ, lddq, 0.0, 1.0));
+    if (R.wz) TRY(ht_fill2d(st, n, n, dZ, lddz, 0.0, 1.0));
+    if (n > 2) {
+        TRY(ht_fro_norm_sq(st, n, n, dB, lddb, w->d_scal));
+        HT_CUDA_TRY(cudaMemcpyAsync(w->h_scal, w->d_scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+        HT_CUDA_TRY(cudaStreamSynchronize(st));
+        const double nB = sqrt(w->h_scal[0]);
+        const double tolf = (opt && opt->tol_factor > 0) ? opt->tol_factor : 2.0;
+        const int max_ir = (opt && opt->max_ir > 0) ? opt->max_ir : 10;
+        const uint64_t seed = opt ? opt->seed : 0;
+        int nforce = 0;
+        if (opt && opt->n_force_ir_fail > 0) {
+            std::vector<int64_t> fl(opt->force_ir_fail, opt->force_ir_fail + opt->n_force_ir_fail);
+            std::sort(fl.begin(), fl.end());
+            nforce = (int)std::min<int64_t>((int64_t)fl.size(), w->ncap);
+            HT_CUDA_TRY(cudaMemcpy(w->d_force, fl.data(), nforce * sizeof(int64_t), cudaMemcpyHostToDevice));
+        }
+        HT_CUDA_TRY(cudaMemsetAsync(w->d_iflags, 0, sizeof(int), st));
+        int64_t s0 = 0;
+        while (s0 <= n - 3) {
+            const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
+            TRY(ht_desingularize(st, n, dB, lddb, s0 + 1, HT_U * nB, 2.0 * HT_U * nB, seed, s0, w->d_iflags));
+            HT_CUDA_TRY(cudaMemsetAsync(w->S, 0, (size_t)nb * nb * sizeof(double), st));
+            HT_CUDA_TRY(cudaMemsetAsync(w->T, 0, (size_t)nb * nb * sizeof(double), st));
+            PanelArgs pa;
+            memset(&pa, 0, sizeof(pa));
+            pa.n = n; pa.lda = ldda; pa.ldb = lddb; pa.A = dA; pa.B = dB;
+            pa.s0 = s0; pa.kmax = (int)kmax; pa.nb = (int)nb;
+            pa.U = w->U; pa.V = w->V; pa.Y = w->Y; pa.S = w->S; pa.T = w->T;
+            double *vv = w->vec;
+            const int64_t N = w->ncap;
+            pa.vsave = vv; pa.vrhs = vv + N; pa.vy = vv + 2 * N; pa.vx = vv + 3 * N;
+            pa.vw = vv + 4 * N; pa.vw2 = vv + 5 * N; pa.vr = vv + 6 * N;
+            pa.part = w->part; pa.pw = (int)nb + 8;
+            pa.flags = w->flags; pa.bexp = w->bexp; pa.epoch = w->epoch;
+            pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
+            pa.force_fail = w->d_force; pa.n_force_fail = nforce;
+            pa.out = w->d_out;
+            const int64_t M = n - s0 - 1;
+            int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 63) / 64));
+            TRY(ht_panel_run(st, &pa, G));
+            HT_CUDA_TRY(cudaMemcpyAsync(w->h_out, w->d_out, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            const int64_t k = w->h_out[0];
+            const int failed = (int)w->h_out[1];
+            w->epoch = (unsigned)w->h_out[5] + 1;
+            R.rep.panels++;
+            R.rep.absorptions++;
+            R.rep.ir_steps_total += w->h_out[2];
+            R.rep.ir_extra_columns += w->h_out[3];
+            R.rep.solve_rescales += w->h_out[4];
+            if (failed) { R.rep.ir_failed_columns++; R.rep.premature_absorptions++; }
+            R.extra_flops += panel_flops(n, s0, k, w->h_out[2]);
+            if (k <= 0) return HT_ENUMERIC;
+            TRY(R.absorb(s0, k));
+            s0 += k;
+        }
+        HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    }
+    // exact structural zeros of H and T (Alg. 2 "Set ... <- 0")
+    TRY(ht_zero_lower(st, n, n, dA, ldda, 1));
+    TRY(ht_zero_lower(st, n, n, dB, lddb, 0));
+    HT_CUDA_TRY(cudaEventRecord(e1, st));
+    HT_CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    HT_CUDA_TRY(cudaGetLastError());
+    R.rep.seconds = ms * 1e-3;
+    R.rep.flops_level3 = g_ht_flops;
+    R.rep.flops = g_ht_flops + R.extra_flops;
+    R.rep.desingularizations = (n > 2) ? w->h_iflags[0] : 0;
+    if (rep) *rep = R.rep;
+    return HT_OK;
+}
+
+int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb)
+{
+    int rc = validate(n, A, n, B, n, Q, n, Z, n, wantq, wantz, nullptr);
+    if (rc) return rc;
+    if (n == 0) return HT_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
+    const size_t bytes = (size_t)n * n * sizeof(double);
+    double *d[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int i = 0; i < 4; ++i)
+        if (cudaMalloc((void **)&d[i], bytes) != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaFree(d[j]);
+            return HT_ENOMEM;
+        }
+    auto cleanup = [&]() { for (int i = 0; i < 4; ++i) cudaFree(d[i]); };
+    if (cudaMemcpy(d[0], A, bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d[1], B, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cleanup();
+        return HT_ECUDA;
+    }
+    ht_options opt;
+    memset(&opt, 0, sizeof(opt));
+    opt.nb = nb;
+    rc = ht_reduce_ex(n, d[0], n, d[1], n, wantq ? d[2] : nullptr, n, wantz ? d[3] : nullptr, n, wantq, wantz, &opt,
+                      nullptr);
+    if (rc == HT_OK) {
+        if (cudaMemcpy(A, d[0], bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(B, d[1], bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            (wantq && cudaMemcpy(Q, d[2], bytes, cudaMemcpyDeviceToHost) != cudaSuccess) ||
+            (wantz && cudaMemcpy(Z, d[3], bytes, cudaMemcpyDeviceToHost) != cudaSuccess))
+            rc = HT_ECUDA;
+    }
+    cleanup();
+    return rc;
+}
+
+}  // extern "C"

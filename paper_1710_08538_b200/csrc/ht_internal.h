@@ -1,0 +1,62 @@
+// ht_internal.h -- internal (non-ABI) declarations of the B200 HouseHT library.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// One window of a staircase factorization: Householder QR of the strided view
+// W(i,j) = W[i*rs + j*cs], i < p, j < q (p >= q).  R (upper trapezoid, exact
+// zeros below) is written back through the view; the reflectors go to
+// V(:, j) in natural row order (row rev ? p-1-i : i), tau to tau[j].
+struct FactorDesc {
+    double *W;
+    int64_t rs, cs;
+    int p, q;
+    int rev;
+    double *V;
+    int64_t ldv;
+    double *tau;
+};
+struct LarftDesc {
+    const double *G;  // V^T V (q x q)
+    int64_t ldg;
+    const double *tau;
+    double *T;  // out (q x q, upper)
+    int64_t ldt;
+    int q;
+};
+
+int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxpq);
+int ht_larft_run(cudaStream_t st, const LarftDesc *d_descs, int nd);
+
+// panel kernel (ht_panel.cu)
+struct PanelArgs {
+    int64_t n, lda, ldb;
+    double *A;
+    double *B;
+    int64_t s0;    // first unreduced column (0-based)
+    int kmax;      // max reflector pairs in this panel
+    int nb;        // ld of S, T
+    double *U, *V, *Y;  // n x nb, ld = n, absolute row index
+    double *S, *T;      // nb x nb
+    double *vsave, *vrhs, *vy, *vx, *vw, *vw2, *vr;  // n-vectors, absolute row index
+    double *part;       // gridDim x PW partial sums
+    int pw;
+    unsigned *flags;    // trsv flags (per 64-row block)
+    int *bexp;          // trsv block exponents
+    unsigned epoch;     // trsv flag epoch base
+    double tol;         // 2 u ||B||_F
+    int max_ir;         // 10
+    const int64_t *force_fail;  // sorted list of columns whose IR is forced to fail (test hook)
+    int n_force_fail;
+    int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
+};
+int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);
+int ht_panel_max_blocks(int *nblocks_out);
+
+// misc kernels (ht_util.cu)
+int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out);
+int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
+                   int *d_flags);
+int ht_desingularize(cudaStream_t st, int64_t n, double *B, int64_t ldb, int64_t r0, double thresh, double repl,
+                     uint64_t seed, int64_t key, int *d_count);
+int ht_zero_lower(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, int64_t diag_offset);

@@ -1,0 +1,126 @@
+// ht_util.cu -- small utility kernels of the B200 HouseHT library.
+#include "ht_common.cuh"
+#include "ht_internal.h"
+#include <stdio.h>
+
+namespace {
+
+__global__ void fro_kernel(int64_t rows, int64_t cols, const double *M, int64_t ld, double *out)
+{
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+            double v = M[j * ld + i];
+            s += v * v;
+        }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+// flags[0] |= non-finite in A or B; flags[1] |= nonzero strictly-lower entry of B
+__global__ void check_kernel(int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *flags)
+{
+    int bad = 0, low = 0;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            double a = A[j * lda + i], b = B[j * ldb + i];
+            if (!isfinite(a) || !isfinite(b)) bad = 1;
+            if (i > j && b != 0.0) low = 1;
+        }
+    if (bad) atomicOr(&flags[0], 1);
+    if (low) atomicOr(&flags[1], 1);
+}
+
+// Counter-based normal draw (reading R-Z7): splitmix64 hash of (seed, key, row, ctr)
+// -> two uniforms -> Box-Muller.  Independent implementation of the same idea as the
+// oracle's (the two share no code).
+__device__ __forceinline__ uint64_t mix64(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ double rho_draw(uint64_t seed, int64_t key, int64_t row, uint32_t ctr)
+{
+    uint64_t h = mix64(seed ^ mix64((uint64_t)key * 0x100000001B3ULL ^ mix64((uint64_t)row + ((uint64_t)ctr << 40))));
+    uint64_t h2 = mix64(h);
+    double u1 = ((double)(h >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    double u2 = ((double)(h2 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+// Desingularisation of tiny pivots of B(r0:n, r0:n) (Remark 1 P:135-139):
+// |b_ii| < thresh -> repl * rho, |rho| >= 1/2 (readings R-Z6, R-Z7), persisted in B.
+__global__ void desing_kernel(int64_t n, double *B, int64_t ldb, int64_t r0, double thresh, double repl,
+                              uint64_t seed, int64_t key, int *count)
+{
+    for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double *d = B + i * ldb + i;
+        if (fabs(*d) < thresh) {
+            uint32_t ctr = 0;
+            double rho;
+            do { rho = rho_draw(seed, key, i, ctr++); } while (fabs(rho) < 0.5);
+            *d = repl * rho;
+            atomicAdd(count, 1);
+        }
+    }
+}
+
+// M(i, j) = 0 for i > j + diag_offset  (exact structural zeros)
+__global__ void zero_lower_kernel(int64_t rows, int64_t cols, double *M, int64_t ld, int64_t off)
+{
+    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+        for (int64_t i = j + off + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+             i += (int64_t)gridDim.x * blockDim.x)
+            if (i >= 0) M[j * ld + i] = 0.0;
+}
+
+}  // namespace
+
+int ht_cuda_fail(cudaError_t e, const char *what, const char *file, int line)
+{
+    fprintf(stderr, "[ht_b200] CUDA error %s (%s) at %s:%d: %s\n", cudaGetErrorName(e), cudaGetErrorString(e), file,
+            line, what);
+    return 2;  // HT_ECUDA
+}
+
+int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out)
+{
+    HT_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double), st));
+    if (rows <= 0 || cols <= 0) return 0;
+    dim3 grid(4, (unsigned)(cols < 2048 ? cols : 2048));
+    fro_kernel<<<grid, 256, 0, st>>>(rows, cols, M, ld, d_out);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *d_flags)
+{
+    HT_CUDA_TRY(cudaMemsetAsync(d_flags, 0, 2 * sizeof(int), st));
+    if (n <= 0) return 0;
+    dim3 grid(4, (unsigned)(n < 2048 ? n : 2048));
+    check_kernel<<<grid, 256, 0, st>>>(n, A, lda, B, ldb, d_flags);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_desingularize(cudaStream_t st, int64_t n, double *B, int64_t ldb, int64_t r0, double thresh, double repl,
+                     uint64_t seed, int64_t key, int *d_count)
+{
+    if (r0 >= n) return 0;
+    int64_t m = n - r0;
+    desing_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(n, B, ldb, r0, thresh, repl, seed, key, d_count);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_zero_lower(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, int64_t diag_offset)
+{
+    if (rows <= 0 || cols <= 0) return 0;
+    dim3 grid((unsigned)((rows + 255) / 256 < 32 ? (rows + 255) / 256 : 32), (unsigned)(cols < 4096 ? cols : 4096));
+    zero_lower_kernel<<<grid, 256, 0, st>>>(rows, cols, M, ld, diag_offset);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}

@@ -1,0 +1,172 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances are the north star's (BASELINE.json):
+  ||Q^T A Z - H||_F/||A||_F, ||Q^T B Z - T||_F/||B||_F, ||Q^T Q - I||_F, ||Z^T Z - I||_F <= 20 n 2.2e-16
+  || |H| - |H_oracle| ||_F <= 1e-9 ||A||_F  and the same for T   (unique up to signs)
+Structure is checked bitwise (exact zeros).  Config-4 (singular B) parity is
+against Oracle-G (the HT form of a singular pencil is not unique).
+"""
+import numpy as np
+import pytest
+
+import ht_inputs
+import htcheck as C
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1710_08538_b200 as ht  # noqa: E402
+
+PARITY = 1e-9
+
+
+def to_dev(M):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(M, dtype=np.float64).T)).cuda()
+
+
+def from_dev(t):
+    return np.asfortranarray(t.cpu().numpy().T)
+
+
+def gpu_reduce(A, B, nb=0, wantq=True, wantz=True, **kw):
+    n = A.shape[0]
+    dA, dB = to_dev(A), to_dev(B)
+    dQ = torch.empty((n, n), dtype=torch.float64, device="cuda") if wantq else None
+    dZ = torch.empty((n, n), dtype=torch.float64, device="cuda") if wantz else None
+    rep = ht.reduce_device(dA, dB, dQ, dZ, nb=nb, **kw)
+    torch.cuda.synchronize()
+    out = [from_dev(dA), from_dev(dB), from_dev(dQ) if wantq else None, from_dev(dZ) if wantz else None]
+    return (*out, rep)
+
+
+def check_props(A, B, H, T, Q, Z, tolmul=1.0):
+    n = A.shape[0]
+    assert C.structure_ok(H, T)
+    ra, rb, oq, oz = C.backward_errors(A, B, H, T, Q, Z)
+    tol = C.tol_ns(n) * tolmul
+    assert ra <= tol and rb <= tol and oq <= tol and oz <= tol, (ra, rb, oq, oz, tol)
+    return ra, rb, oq, oz
+
+
+def check_parity(A, B, H, T, Hr, Tr):
+    dh = C.abs_diff(H, Hr, C.fro(A))
+    dt = C.abs_diff(T, Tr, C.fro(B))
+    assert dh <= PARITY and dt <= PARITY, (dh, dt)
+    return dh, dt
+
+
+@pytest.mark.parametrize("kind", ["qrnormal", "shifted", "qruniform"])
+@pytest.mark.parametrize("n,nb", [(3, 1), (4, 2), (5, 8), (8, 3), (17, 4), (40, 5), (64, 8), (100, 16),
+                                  (130, 32), (161, 13)])
+def test_small_sweep_vs_oracle_T(kind, n, nb):
+    A, B = ht_inputs.pencil(kind, n, 1000 + n + nb)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+    assert rep["ir_failed_columns"] == 0
+
+
+def test_config1_full_size():
+    A, B, nb = ht_inputs.config_pencil(1)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+    assert rep["ir_failed_columns"] == 0
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 600), (5, 700), (2, 520)])
+def test_config_shapes_multi_panel(cfg, n):
+    """Config recipes at sizes the oracle finishes in seconds: several panels,
+    staircase windows with Remark-4 ragged first windows, and the tail rule."""
+    A, B, nb = ht_inputs.config_pencil(cfg, n=n)
+    nb = min(nb, 64)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+
+
+@pytest.mark.parametrize("n,nb", [(120, 16), (300, 32)])
+def test_config4_singular_vs_givens(n, nb):
+    A, B, _ = ht_inputs.config_pencil(4, n=n)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hg, Tg, _, _ = oracle.ht_G(A, B)
+    dh = C.abs_diff(H, Hg, C.fro(A))
+    dt = C.abs_diff(T, Tg, C.fro(B))
+    print(f"cfg4 n={n}: |H| diff {dh:.2e}, |T| diff {dt:.2e}, report {rep}")
+    assert dh <= PARITY and dt <= PARITY
+
+
+def test_forced_ir_failures_premature_absorption():
+    """IR-failure fallback (Algorithm 1): forced failures make
+    the panel stop early (k < nb) and restart at the failed column."""
+    A, B = ht_inputs.pencil("qrnormal", 200, 77)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=16, force_ir_fail=(5, 6, 40, 41, 42, 130))
+    assert rep["premature_absorptions"] >= 4
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+
+
+def test_no_q_no_z():
+    A, B = ht_inputs.pencil("shifted", 90, 3)
+    H1, T1, Q, Z, _ = gpu_reduce(A, B, nb=8)
+    H2, T2, _, _, _ = gpu_reduce(A, B, nb=8, wantq=False, wantz=False)
+    assert np.array_equal(H1, H2) and np.array_equal(T1, T2)
+
+
+def test_degenerate_sizes_and_ht_input():
+    for n in (0, 1, 2):
+        A, B = ht_inputs.pencil("shifted", n, 1)
+        if n == 0:
+            continue
+        H, T, Q, Z, _ = gpu_reduce(A, B)
+        assert np.array_equal(H, A) and np.array_equal(T, B)
+        assert np.array_equal(Q, np.eye(n)) and np.array_equal(Z, np.eye(n))
+    A, B = ht_inputs.pencil("ht", 70, 5)
+    H, T, Q, Z, _ = gpu_reduce(A, B, nb=16)
+    assert np.array_equal(H, A) and np.array_equal(T, B)
+    assert np.array_equal(Q, np.eye(70)) and np.array_equal(Z, np.eye(70))
+
+
+def test_error_codes_on_device():
+    A, B = ht_inputs.pencil("shifted", 16, 2)
+    Bbad = B.copy()
+    Bbad[5, 2] = 1.0
+    with pytest.raises(ht.HTError) as e:
+        gpu_reduce(A, Bbad)
+    assert e.value.code == -3
+    Abad = A.copy()
+    Abad[3, 3] = np.nan
+    with pytest.raises(ht.HTError) as e:
+        gpu_reduce(Abad, B)
+    assert e.value.code == 1
+
+
+def test_host_entry_point_matches_device():
+    A, B = ht_inputs.pencil("qrnormal", 77, 9)
+    H, T, Q, Z = ht.ht_reduce(A, B, nb=8)
+    H2, T2, Q2, Z2, _ = gpu_reduce(A, B, nb=8)
+    assert np.array_equal(H, H2) and np.array_equal(T, T2)
+    assert np.array_equal(Q, Q2) and np.array_equal(Z, Z2)
+
+
+def test_deterministic():
+    A, B = ht_inputs.pencil("qruniform", 300, 4)
+    r1 = gpu_reduce(A, B, nb=32)
+    r2 = gpu_reduce(A, B, nb=32)
+    for x, y in zip(r1[:4], r2[:4]):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.slow
+def test_config2_full_size_vs_oracle():
+    A, B, nb = ht_inputs.config_pencil(2)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
