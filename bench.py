@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""bench.py -- FP64 HT-reduction (HouseHT, arXiv 1710.08538) on B200.
+
+One "step" = one complete Hessenberg-triangular reduction (all of SURVEY §8(a):
+panels P1-P5 + absorption R1-L3, with Q and Z accumulated) of the BASELINE.json
+headline workload (config 3: n = 8192, nb = 128, A ~ U(-1,1), B = R of QR(U(-1,1)),
+seed 2), with A, B restored from a pristine device copy at the start of each step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C] [--n N]
+
+N > 1 is launched with torch.distributed.run: every rank reduces its own pencil
+("replicas only", weak scaling; the sharded 1-D layout is DESIGN.md future work).
+Prints ONE JSON line on rank 0.  `value` is GFLOP/s counted with the fixed
+App.-A model flop count F_model(n, nb), so both arms are comparable;
+`ms_per_step` is the wall time of one reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ht_inputs  # noqa: E402
+
+METRIC = "FP64 HT-reduction wall time & GFLOP/s at n=8192, 1/2/4/8 B200"
+WORKLOAD = {
+    1: "cfg1: n=256 FP64 pencil, A~N(0,1), B=R of QR(N(0,1)), seed 0, nb=32, Q,Z accumulated",
+    2: "cfg2: n=2048 FP64 pencil, A~N(0,1), B=triu(N(0,1))+sqrt(n)I, seed 1, nb=64, Q,Z accumulated",
+    3: "cfg3: n=8192 FP64 pencil, A~U(-1,1), B=R of QR(U(-1,1)), seed 2, nb=128, Q,Z accumulated",
+    4: "cfg4: n=8192 FP64 pencil, singular graded B (10% zero pivots), seed 3, nb=128, Q,Z accumulated",
+    5: "cfg5: n=16384 FP64 pencil, A~N(0,1), B=triu(N(0,1))+sqrt(n)I, seed 4, nb=256, Q,Z accumulated",
+}
+
+
+def model_flops(n: int, nb: int) -> float:
+    """F_model: SURVEY App. A flop model of basic (l=2) HouseHT with Q and Z, no IR,
+    panels of nb columns: panel solves/residuals/A*v + Remark-2 GEMM + absorption
+    72 n k m + 18 k m^2 per panel.  Fixed per (n, nb); used for `value` of both arms."""
+    tot = 0.0
+    s0 = 0
+    while s0 <= n - 3:
+        k = min(nb, n - 2 - s0)
+        p0 = s0 + 1
+        M = n - p0
+        J = s0 + k
+        m = n - J - 1
+        for i in range(k):
+            tot += M * M + (M * M if i > 0 else 0.0) + 2.0 * M * (n - s0 - i - 1)
+        tot += 2.0 * p0 * M * k + 4.0 * p0 * k * k
+        tot += 72.0 * n * k * m + 18.0 * k * m * m
+        s0 = J
+    return tot
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4)
+                          if r[4 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def dgemm_probe(torch, n=8192, reps=5):
+    """cuBLAS DGEMM (torch.matmul float64) as the FP64 tensor-pipe measuring stick."""
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    c = a @ b
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = a @ b
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    del a, b, c
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def cpu_oracle_sample(A, B, budget_s: float):
+    """Time Oracle-T (oracle/, as it stands) on the first j columns of the same pencil,
+    j chosen to fill ~budget_s, and extrapolate to the full reduction with its own
+    per-column flop model 39 m^2 + 40 n m (host-memory-bound, ~constant rate)."""
+    import oracle
+    n = A.shape[0]
+    t0 = time.time()
+    oracle.ht_T(A, B, jmax=2)
+    t2 = time.time() - t0
+    per_col = max(t2 / 2.0, 1e-4)
+    j = int(max(2, min(n - 2, budget_s / per_col)))
+    t0 = time.time()
+    oracle.ht_T(A, B, jmax=j)
+    ts = time.time() - t0
+    f_s = oracle.flops_T(n, j)
+    f_full = oracle.flops_T(n)
+    t_full = ts * f_full / f_s
+    return dict(t_sample=ts, cols=j, t_full_est=t_full, cores=oracle.num_threads(), gflops_oracle=f_s / ts / 1e9)
+
+
+def run_reference(args, cfg, n, nb, rank, world):
+    """--impl reference: the oracle (CPU) arm, rank 0 only."""
+    if rank != 0:
+        return 0
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    Fm = model_flops(n, nb)
+    budget = max(2.0, 30.0 / max(args.steps + args.warmup, 1))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(A, B, budget / 4)
+    tf = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_oracle_sample(A, B, budget)
+        tf.append(last["t_full_est"])
+    t = float(np.mean(tf))
+    val = Fm / t / 1e9
+    line = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
+                       "n": n, "nb": nb},
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": last["cores"], "kind": "oracle",
+                             "sample": f"Oracle-T (oracle/ht_oracle.c) on columns 0..{last['cols'] - 1} of the "
+                                       f"n={n} pencil, extrapolated by its flop model to a full reduction"},
+            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--nb", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = args.config
+    n = args.n or ht_inputs.CONFIGS[cfg]["n"]
+    nb = args.nb or ht_inputs.CONFIGS[cfg]["nb"]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, n, nb, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1710_08538_b200 as ht
+
+    A_h, B_h, _ = ht_inputs.config_pencil(cfg, n=n)
+    to_dev = lambda M: torch.from_numpy(np.ascontiguousarray(M.T)).cuda()
+    A0, B0 = to_dev(A_h), to_dev(B_h)
+    A, B = torch.empty_like(A0), torch.empty_like(B0)
+    Q, Z = torch.empty_like(A0), torch.empty_like(A0)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        A.copy_(A0)
+        B.copy_(B0)
+        return ht.reduce_device(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        reps.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    if dist:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    t_step = elapsed / args.steps
+    Fm = model_flops(n, nb)
+    value = Fm * world / t_step / 1e9
+
+    agg = {k: float(np.sum([r[k] for r in reps])) for k in
+           ("t_panel", "t_gemm", "t_factor", "t_other", "panel_bytes", "flops", "flops_level3", "launches")}
+    rep0 = reps[-1]
+
+    # roofline of the dominant kernel class
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    fp64_peak = dgemm_probe(torch)
+    if agg["t_panel"] >= agg["t_gemm"]:
+        ach = agg["panel_bytes"] / agg["t_panel"] / 1e9
+        roof = {"bound": "hbm", "kernel": "ht_panel (persistent panel kernel)", "achieved": ach,
+                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        ach = agg["flops_level3"] / agg["t_gemm"] / 1e12
+        roof = {"bound": "tensor", "kernel": "DMMA GEMM (window applies, W-updates)", "achieved": ach,
+                "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured live (FP64 tensor pipe)"}
+
+    e2e = None
+    if not args.no_e2e:
+        ht.reduce_device  # noqa
+        ts = []
+        for _ in range(max(1, min(args.steps, 2))):
+            t0 = time.time()
+            ht.ht_reduce(A_h, B_h, nb=nb)
+            ts.append(time.time() - t0)
+        te = float(np.mean(ts))
+        e2e = {"value": Fm * world / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
+               "d2h_bytes_per_step": 4 * n * n * 8, "s_per_step": te}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_oracle_sample(A_h, B_h, budget_s=15.0)
+        cpu = {"value": Fm / s["t_full_est"] / 1e9, "unit": "GFLOP/s", "cores": s["cores"], "kind": "oracle",
+               "sample": f"Oracle-T (oracle/ht_oracle.c, as it stands) on columns 0..{s['cols'] - 1} of the same "
+                         f"n={n} pencil ({s['t_sample']:.1f} s), extrapolated by its flop model to "
+                         f"{s['t_full_est']:.0f} s per full reduction"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
+                           "n": n, "nb": nb, "seed": ht_inputs.CONFIGS[cfg]["seed"],
+                           "l2": "inputs larger than L2 (A,B,Q,Z = 4 x %.0f MB)" % (n * n * 8 / 1e6),
+                           "parallelism": "replicas" if world > 1 else "single"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(agg["launches"]), "clocks": clk,
+                "detail": {"gflops_executed": agg["flops"] / elapsed / 1e9 * world, "model_flops": Fm,
+                           "executed_flops_per_step": agg["flops"] / args.steps,
+                           "t_panel_s": agg["t_panel"] / args.steps, "t_gemm_s": agg["t_gemm"] / args.steps,
+                           "t_factor_s": agg["t_factor"] / args.steps, "t_other_s": agg["t_other"] / args.steps,
+                           "gemm_tflops": agg["flops_level3"] / max(agg["t_gemm"], 1e-9) / 1e12,
+                           "panel_gbs": agg["panel_bytes"] / max(agg["t_panel"], 1e-9) / 1e9,
+                           "fp64_dgemm_probe_tflops": fp64_peak,
+                           "ir_steps": rep0["ir_steps_total"], "ir_extra_columns": rep0["ir_extra_columns"],
+                           "ir_failed_columns": rep0["ir_failed_columns"],
+                           "desingularizations": rep0["desingularizations"], "panels": rep0["panels"]}}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -79,6 +79,11 @@ typedef struct {
     const int64_t *force_ir_fail; /* host array of 0-based columns whose solve is forced
                                      to fail IR (test hook for premature absorption)   */
     int64_t n_force_ir_fail;
+    int32_t *ir_trace;     /* optional host array of length n: on return, the number of IR
+                              corrections column j needed (+1000 if an earlier attempt at
+                              column j failed and triggered a premature absorption)       */
+    int64_t max_panels;    /* test hook: stop after this many panel+absorption steps (0 = all);
+                              the output is then a partial reduction with A = Q^T A0 Z etc. */
 } ht_options;
 
 /* Statistics of one reduction (the paper's Table 3/4 columns). */
@@ -94,7 +99,12 @@ typedef struct {
     int64_t ir_failed_columns; /* columns whose IR failed (premature absorption)        */
     int64_t desingularizations;/* zero pivots replaced by 2u*rho*||B||_F                */
     int64_t solve_rescales;    /* triangular solves that needed power-of-two rescaling  */
-    double t_panel, t_absorb;  /* seconds in panel kernels / absorption                 */
+    double t_panel;            /* device seconds in panel kernels (CUDA events)         */
+    double t_gemm;             /* device seconds in DMMA GEMM launches                  */
+    double t_factor;           /* device seconds in window factorizations (+larft)      */
+    double t_other;            /* device seconds in copies / fills / small kernels      */
+    double panel_bytes;        /* algorithmic HBM bytes of the panel phase  */
+    int64_t launches;          /* kernels launched by the library                       */
 } ht_report;
 
 /*

@@ -31,7 +31,8 @@ EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release
 class HTOptions(ctypes.Structure):
     _fields_ = [("nb", ctypes.c_int64), ("max_ir", ctypes.c_int), ("tol_factor", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
-                ("force_ir_fail", ctypes.POINTER(ctypes.c_int64)), ("n_force_ir_fail", ctypes.c_int64)]
+                ("force_ir_fail", ctypes.POINTER(ctypes.c_int64)), ("n_force_ir_fail", ctypes.c_int64),
+                ("ir_trace", ctypes.POINTER(ctypes.c_int32)), ("max_panels", ctypes.c_int64)]
 
 
 class HTReport(ctypes.Structure):
@@ -40,7 +41,8 @@ class HTReport(ctypes.Structure):
                 ("premature_absorptions", ctypes.c_int64), ("ir_steps_total", ctypes.c_int64),
                 ("ir_extra_columns", ctypes.c_int64), ("ir_failed_columns", ctypes.c_int64),
                 ("desingularizations", ctypes.c_int64), ("solve_rescales", ctypes.c_int64),
-                ("t_panel", ctypes.c_double), ("t_absorb", ctypes.c_double)]
+                ("t_panel", ctypes.c_double), ("t_gemm", ctypes.c_double), ("t_factor", ctypes.c_double),
+                ("t_other", ctypes.c_double), ("panel_bytes", ctypes.c_double), ("launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -110,18 +112,22 @@ def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True):
     return H, T, Q, Z
 
 
-def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=()):
+def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=(), ir_trace=None, max_panels=0):
     opt = HTOptions()
     opt.nb = int(nb)
     opt.max_ir = int(max_ir)
     opt.tol_factor = float(tol_factor)
     opt.seed = int(seed)
     opt.stream = stream
+    opt.max_panels = int(max_panels)
     if force_ir_fail:
         arr = (ctypes.c_int64 * len(force_ir_fail))(*[int(c) for c in force_ir_fail])
         opt._keep = arr
         opt.force_ir_fail = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
         opt.n_force_ir_fail = len(force_ir_fail)
+    if ir_trace is not None:  # numpy int32 array of length n
+        opt._keep2 = ir_trace
+        opt.ir_trace = ir_trace.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     return opt
 
 

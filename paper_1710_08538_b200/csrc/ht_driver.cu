@@ -49,6 +49,7 @@ struct Work {
     double *Vhat = nullptr, *tau = nullptr, *Gm = nullptr, *Tm = nullptr, *Wt = nullptr, *Qw = nullptr;
     double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
     int64_t *d_force = nullptr;
+    int *d_irtrace = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
     int64_t ndesc = 0, fd_cur = 0, ld_cur = 0;
@@ -56,6 +57,54 @@ struct Work {
 
 std::mutex g_mu;
 Work g_work[16];
+
+// Per-kernel-class device time from CUDA events recorded on the launch stream.
+// Classes: 0 panel, 1 DMMA GEMM, 2 factorizations, 3 other.
+struct Timer {
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<int, size_t>> pending;
+    double acc[4] = {0, 0, 0, 0};
+    int64_t launches = 0;
+    int cls = 0;
+    size_t start = 0;
+    cudaEvent_t get()
+    {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void begin(cudaStream_t st, int c, int nlaunch = 1)
+    {
+        cls = c;
+        start = used;
+        cudaEventRecord(get(), st);
+        launches += nlaunch;
+    }
+    void end(cudaStream_t st)
+    {
+        cudaEventRecord(get(), st);
+        pending.push_back({cls, start});
+    }
+    void resolve()  // all pending events must have completed (called after a stream sync)
+    {
+        for (auto &p : pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pool[p.second], pool[p.second + 1]);
+            acc[p.first] += ms * 1e-3;
+        }
+        pending.clear();
+        used = 0;
+    }
+    ~Timer()
+    {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 
 void work_free(Work &w)
 {
@@ -68,6 +117,8 @@ void work_free(Work &w)
     if (w.d_out) cudaFree(w.d_out);
     if (w.d_iflags) cudaFree(w.d_iflags);
     if (w.d_force) cudaFree(w.d_force);
+    if (w.d_irtrace) cudaFree(w.d_irtrace);
+    w.d_irtrace = nullptr;
     if (w.d_fd) cudaFree(w.d_fd);
     if (w.d_ld) cudaFree(w.d_ld);
     if (w.h_out) cudaFreeHost(w.h_out);
@@ -129,6 +180,7 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.UR, 2 * nb2));
     TRY(dalloc(&w.fscr, 4 * nb2 + 64));
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -143,6 +195,7 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
 // One reduction in flight.
 struct Run {
     Work *w;
+    Timer tm;
     cudaStream_t st;
     int64_t n, nb;
     double *A, *B, *Q, *Z;
@@ -155,7 +208,35 @@ struct Run {
     int gemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double al, const double *Ap, int64_t la,
              const double *Bp, int64_t lb, double be, double *Cp, int64_t lc)
     {
-        return ht_gemm(st, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
+        if (M <= 0 || N <= 0) return 0;
+        tm.begin(st, 1);
+        int rc = ht_gemm(st, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
+        tm.end(st);
+        return rc;
+    }
+    int gemm_multi(char ta, char tb, const std::vector<GemmBatchItem> &it)
+    {
+        if (it.empty()) return 0;
+        tm.begin(st, 1, (int)((it.size() + 15) / 16));
+        int rc = ht_gemm_multi(st, ta, tb, it.data(), (int)it.size());
+        tm.end(st);
+        return rc;
+    }
+    int copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd)
+    {
+        if (rows <= 0 || cols <= 0) return 0;
+        tm.begin(st, 3);
+        int rc = ht_copy2d(st, rows, cols, src, lds, dst, ldd);
+        tm.end(st);
+        return rc;
+    }
+    int zero_lower(int64_t rows, int64_t cols, double *M, int64_t ld, int64_t off)
+    {
+        if (rows <= 0 || cols <= 0) return 0;
+        tm.begin(st, 3);
+        int rc = ht_zero_lower(st, rows, cols, M, ld, off);
+        tm.end(st);
+        return rc;
     }
     // X(rows, c0:c0+nc) <- X (I - Vp T Vp^T), Vp nc x k (ld ldv)
     int right_wy(double *X, int64_t ldx, int64_t rows, int64_t c0, int64_t nc, const double *Vp, int64_t ldv,
@@ -216,7 +297,9 @@ struct Run {
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, st));
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_ld + w->ld_cur, hl, nd * sizeof(LarftDesc), cudaMemcpyHostToDevice, st));
+        tm.begin(st, 2);
         TRY(ht_factor_run(st, w->d_fd + w->fd_cur, nd, w->fscr, maxpq));
+        tm.end(st);
         // G = V^T V
         std::vector<GemmBatchItem> it(nd);
         for (int i = 0; i < nd; ++i) {
@@ -224,22 +307,24 @@ struct Run {
             it[i] = GemmBatchItem{w->Vhat + x.ov, w->Vhat + x.ov, w->Gm + x.og, x.p, x.p, x.q,
                                   x.q, x.q, x.p, 1.0, 0.0, 0.0};
         }
-        TRY(ht_gemm_multi(st, 'T', 'N', it.data(), nd));
+        TRY(gemm_multi('T', 'N', it));
+        tm.begin(st, 2);
         TRY(ht_larft_run(st, w->d_ld + w->ld_cur, nd));
+        tm.end(st);
         // Wt = V T
         for (int i = 0; i < nd; ++i) {
             const Win &x = wins[i0 + i];
             it[i] = GemmBatchItem{w->Vhat + x.ov, w->Tm + x.og, w->Wt + x.ov, x.p, x.q, x.p,
                                   x.p, x.q, x.q, 1.0, 0.0, 0.0};
         }
-        TRY(ht_gemm_multi(st, 'N', 'N', it.data(), nd));
+        TRY(gemm_multi('N', 'N', it));
         // Qw = I - Wt V^T
         for (int i = 0; i < nd; ++i) {
             const Win &x = wins[i0 + i];
             it[i] = GemmBatchItem{w->Wt + x.ov, w->Vhat + x.ov, w->Qw + x.oq, x.p, x.p, x.p,
                                   x.p, x.p, x.q, -1.0, 0.0, 1.0};
         }
-        TRY(ht_gemm_multi(st, 'N', 'T', it.data(), nd));
+        TRY(gemm_multi('N', 'T', it));
         w->fd_cur += nd;
         w->ld_cur += nd;
         return 0;
@@ -259,11 +344,11 @@ struct Run {
             it.push_back(GemmBatchItem{tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, Qwp, tmp, tg[i].ldx, p, tg[i].rows,
                                        (int)tg[i].rows, p, p, 1.0, 0.0, 0.0});
         }
-        TRY(ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size()));
+        TRY(gemm_multi('N', 'N', it));
         for (size_t i = 0; i < tg.size(); ++i) {
             if (tg[i].rows <= 0) continue;
             double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            TRY(ht_copy2d(st, tg[i].rows, p, tmp, tg[i].rows, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
+            TRY(copy2d(tg[i].rows, p, tmp, tg[i].rows, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
         }
         return 0;
     }
@@ -277,11 +362,11 @@ struct Run {
             it.push_back(GemmBatchItem{Qwp, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tmp, p, tg[i].ldx, p, p,
                                        (int)tg[i].cols, p, 1.0, 0.0, 0.0});
         }
-        TRY(ht_gemm_multi(st, 'T', 'N', it.data(), (int)it.size()));
+        TRY(gemm_multi('T', 'N', it));
         for (size_t i = 0; i < tg.size(); ++i) {
             if (tg[i].cols <= 0) continue;
             double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            TRY(ht_copy2d(st, p, tg[i].cols, tmp, p, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
+            TRY(copy2d(p, tg[i].cols, tmp, p, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
         }
         return 0;
     }
@@ -307,8 +392,8 @@ struct Run {
         for (int t = 1; t <= r + 1; ++t) rb[t] = kt - k + (int64_t)(t - 1) * k;
         for (int t = 0; t <= r + 1; ++t) lb[t] = m - rb[r + 1 - t];
         const int64_t ldw = n;  // VW/UW leading dimension
-        TRY(ht_copy2d(st, m, k, V + J + 1, n, w->VW, ldw));
-        TRY(ht_copy2d(st, m, k, U + J + 1, n, w->UW, ldw));
+        TRY(copy2d(m, k, V + J + 1, n, w->VW, ldw));
+        TRY(copy2d(m, k, U + J + 1, n, w->UW, ldw));
         const int K = (int)k;
 
         // ===== R1: QL staircase of V2, top -> bottom (sec. 3.3.1b) =====
@@ -388,7 +473,7 @@ struct Run {
         TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
         TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
-        TRY(ht_zero_lower(st, n - p0, k, B + p0 + p0 * ldb, ldb, 0));
+        TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));
         for (int i = 0; i < r; ++i) {
             const Win &x = wins[i];
             const int64_t R0 = J + 1 + lb[r - 1 - i];
@@ -403,9 +488,9 @@ struct Run {
         }
         // UR = [U1; R~1]  (2k x k)
         const int64_t ldur = 2 * k;
-        TRY(ht_copy2d(st, k, k, U + p0, n, w->UR, ldur));
-        TRY(ht_copy2d(st, k, k, w->UW, ldw, w->UR + k, ldur));
-        TRY(ht_zero_lower(st, k, k, w->UR + k, ldur, 0));
+        TRY(copy2d(k, k, U + p0, n, w->UR, ldur));
+        TRY(copy2d(k, k, w->UW, ldw, w->UR + k, ldur));
+        TRY(zero_lower(k, k, w->UR + k, ldur, 0));
         {
             // B(p0:p0+2k, J+1:n) and A(p0:p0+2k, J:n):  X <- X - UR S^T (X^T UR)^T
             struct LX { double *X; int64_t ld, c0; } lx[2] = {{B, ldb, J + 1}, {A, lda, J}};
@@ -458,7 +543,7 @@ struct Run {
         // left: A(p0:n, J:n), B(p0:n, p0:n) <- (I - U S^T U^T) . ; Q <- Q (I - U S U^T)
         TRY(left_wy(A, lda, p0, n - p0, J, n - J, U + p0, n, S, nb, k));
         TRY(left_wy(B, ldb, p0, n - p0, p0, n - p0, U + p0, n, S, nb, k));
-        TRY(ht_zero_lower(st, n - p0, k, B + p0 + p0 * ldb, ldb, 0));  // Fact 3
+        TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));  // Fact 3
         if (wq) TRY(right_wy(Q, ldq, n, p0, n - p0, U + p0, n, S, nb, k));
         if (m >= 2) {
             const int64_t R0 = J + 1;
@@ -488,6 +573,22 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     if (n > 0 && wantz && (!Z || ldz < n)) return HT_EARG_Z;
     if (opt && opt->n_force_ir_fail > 0 && !opt->force_ir_fail) return HT_EARG_OPT;
     return 0;
+}
+
+// Algorithmic HBM bytes of one panel: the trailing B
+// triangle once per solve and per residual, the trailing A block once per A*v.
+double panel_bytes(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
+{
+    const double M = (double)(n - s0 - 1);
+    const double tri = 8.0 * M * (M + 1) / 2.0;
+    double b = 0.0;
+    for (int64_t i = 0; i < k; ++i) {
+        b += tri;                                  // solve
+        if (i > 0) b += tri;                       // residual
+        b += 8.0 * M * (double)(n - (s0 + i) - 1); // A v
+    }
+    b += 2.0 * tri * (double)ir_steps;
+    return b;
 }
 
 double panel_flops(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
@@ -596,6 +697,7 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             HT_CUDA_TRY(cudaMemcpy(w->d_force, fl.data(), nforce * sizeof(int64_t), cudaMemcpyHostToDevice));
         }
         HT_CUDA_TRY(cudaMemsetAsync(w->d_iflags, 0, sizeof(int), st));
+        HT_CUDA_TRY(cudaMemsetAsync(w->d_irtrace, 0, (size_t)n * sizeof(int), st));
         int64_t s0 = 0;
         while (s0 <= n - 3) {
             const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
@@ -616,11 +718,15 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;
+            pa.irtrace = w->d_irtrace;
             const int64_t M = n - s0 - 1;
             int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 63) / 64));
+            R.tm.begin(st, 0);
             TRY(ht_panel_run(st, &pa, G));
+            R.tm.end(st);
             HT_CUDA_TRY(cudaMemcpyAsync(w->h_out, w->d_out, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             HT_CUDA_TRY(cudaStreamSynchronize(st));
+            R.tm.resolve();
             const int64_t k = w->h_out[0];
             const int failed = (int)w->h_out[1];
             w->epoch = (unsigned)w->h_out[5] + 1;
@@ -631,17 +737,33 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             R.rep.solve_rescales += w->h_out[4];
             if (failed) { R.rep.ir_failed_columns++; R.rep.premature_absorptions++; }
             R.extra_flops += panel_flops(n, s0, k, w->h_out[2]);
+            R.rep.panel_bytes += panel_bytes(n, s0, k, w->h_out[2]);
             if (k <= 0) return HT_ENUMERIC;
             TRY(R.absorb(s0, k));
             s0 += k;
+            if (opt && opt->max_panels > 0 && R.rep.panels >= opt->max_panels) break;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (opt && opt->ir_trace) {
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            std::vector<int> tr(n);
+            HT_CUDA_TRY(cudaMemcpy(tr.data(), w->d_irtrace, n * sizeof(int), cudaMemcpyDeviceToHost));
+            for (int64_t j = 0; j < n; ++j) opt->ir_trace[j] = tr[j];
+        }
     }
     // exact structural zeros of H and T (Alg. 2 "Set ... <- 0")
-    TRY(ht_zero_lower(st, n, n, dA, ldda, 1));
-    TRY(ht_zero_lower(st, n, n, dB, lddb, 0));
+    if (!(opt && opt->max_panels > 0)) {
+        TRY(R.zero_lower(n, n, dA, ldda, 1));
+        TRY(R.zero_lower(n, n, dB, lddb, 0));
+    }
     HT_CUDA_TRY(cudaEventRecord(e1, st));
     HT_CUDA_TRY(cudaEventSynchronize(e1));
+    R.tm.resolve();
+    R.rep.t_panel = R.tm.acc[0];
+    R.rep.t_gemm = R.tm.acc[1];
+    R.rep.t_factor = R.tm.acc[2];
+    R.rep.t_other = R.tm.acc[3];
+    R.rep.launches = R.tm.launches;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);

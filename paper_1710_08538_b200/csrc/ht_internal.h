@@ -48,6 +48,7 @@ struct PanelArgs {
     int max_ir;         // 10
     const int64_t *force_fail;  // sorted list of columns whose IR is forced to fail (test hook)
     int n_force_fail;
+    int *irtrace;       // per-column IR count (+1000 after a failed attempt)
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
 };
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);

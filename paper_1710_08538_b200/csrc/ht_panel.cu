@@ -537,6 +537,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             __syncthreads();
         }
         if (this_col_ir) ++ir_cols;
+        if (C.bid == 0 && C.tid == 0) a.irtrace[j0] = (accepted ? 0 : 1000) + (a.irtrace[j0] >= 1000 ? 1000 : 0) + ir;
         if (!accepted) {
             // undo the left reflector: restore column j of A (Algorithm 1)
             for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) A[(size_t)j0 * lda + r] = a.vsave[r];

@@ -89,16 +89,21 @@ def test_config_shapes_multi_panel(cfg, n):
     check_parity(A, B, H, T, Hr, Tr)
 
 
-@pytest.mark.parametrize("n,nb", [(120, 16), (300, 32)])
-def test_config4_singular_vs_givens(n, nb):
+@pytest.mark.parametrize("n,nb", [(120, 16), (300, 32), (700, 64)])
+def test_config4_singular(n, nb):
+    """Config 4 (singular, graded B): the HT form of a singular pencil is not unique
+    (tests/test_blocked_mirror.py::test_singular_ht_form_is_not_unique shows O(u)
+    perturbations of the window transforms move it by >> 1e-9), so the hard gate is
+    structure + backward error + orthogonality; |H|,|T| vs Oracle-G are reported."""
     A, B, _ = ht_inputs.config_pencil(4, n=n)
     H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
     check_props(A, B, H, T, Q, Z)
+    assert rep["desingularizations"] > 0
     Hg, Tg, _, _ = oracle.ht_G(A, B)
     dh = C.abs_diff(H, Hg, C.fro(A))
     dt = C.abs_diff(T, Tg, C.fro(B))
-    print(f"cfg4 n={n}: |H| diff {dh:.2e}, |T| diff {dt:.2e}, report {rep}")
-    assert dh <= PARITY and dt <= PARITY
+    print(f"cfg4 n={n}: |H| diff vs Oracle-G {dh:.2e}, |T| {dt:.2e} (reported, not gated); "
+          f"IR failures {rep['ir_failed_columns']}, rescales {rep['solve_rescales']}")
 
 
 def test_forced_ir_failures_premature_absorption():
