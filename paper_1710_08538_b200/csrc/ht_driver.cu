@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -50,6 +51,8 @@ struct Work {
     double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
+    double *Dinv = nullptr;
+    int *dsafe = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
     int64_t ndesc = 0, fd_cur = 0, ld_cur = 0;
@@ -119,6 +122,10 @@ void work_free(Work &w)
     if (w.d_force) cudaFree(w.d_force);
     if (w.d_irtrace) cudaFree(w.d_irtrace);
     w.d_irtrace = nullptr;
+    if (w.Dinv) cudaFree(w.Dinv);
+    if (w.dsafe) cudaFree(w.dsafe);
+    w.Dinv = nullptr;
+    w.dsafe = nullptr;
     if (w.d_fd) cudaFree(w.d_fd);
     if (w.d_ld) cudaFree(w.d_ld);
     if (w.h_out) cudaFreeHost(w.h_out);
@@ -181,6 +188,8 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.fscr, 4 * nb2 + 64));
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
+    if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -698,6 +707,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
         }
         HT_CUDA_TRY(cudaMemsetAsync(w->d_iflags, 0, sizeof(int), st));
         HT_CUDA_TRY(cudaMemsetAsync(w->d_irtrace, 0, (size_t)n * sizeof(int), st));
+        double *dbg = nullptr;
+        const bool dbg_on = getenv("HT_DEBUG_IR") != nullptr;
+        if (dbg_on) {
+            HT_CUDA_TRY(cudaMalloc((void **)&dbg, (size_t)n * 12 * sizeof(double)));
+            HT_CUDA_TRY(cudaMemset(dbg, 0, (size_t)n * 12 * sizeof(double)));
+        }
         int64_t s0 = 0;
         while (s0 <= n - 3) {
             const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
@@ -715,12 +730,14 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.vw = vv + 4 * N; pa.vw2 = vv + 5 * N; pa.vr = vv + 6 * N;
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.flags = w->flags; pa.bexp = w->bexp; pa.epoch = w->epoch;
+            pa.Dinv = w->Dinv; pa.dsafe = w->dsafe;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;
             pa.irtrace = w->d_irtrace;
+            pa.dbg = dbg;
             const int64_t M = n - s0 - 1;
-            int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 63) / 64));
+            int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 31) / 32));
             R.tm.begin(st, 0);
             TRY(ht_panel_run(st, &pa, G));
             R.tm.end(st);
@@ -744,6 +761,18 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             if (opt && opt->max_panels > 0 && R.rep.panels >= opt->max_panels) break;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (dbg_on) {
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            std::vector<double> hd((size_t)n * 12);
+            HT_CUDA_TRY(cudaMemcpy(hd.data(), dbg, hd.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int64_t j = 0; j < n; ++j) {
+                if (hd[j * 12] == 0.0) continue;
+                fprintf(stderr, "[ht dbg] col %lld:", (long long)j);
+                for (int it = 0; it < 12 && hd[j * 12 + it] != 0.0; ++it) fprintf(stderr, " %.3g", hd[j * 12 + it]);
+                fprintf(stderr, "\n");
+            }
+            cudaFree(dbg);
+        }
         if (opt && opt->ir_trace) {
             HT_CUDA_TRY(cudaStreamSynchronize(st));
             std::vector<int> tr(n);

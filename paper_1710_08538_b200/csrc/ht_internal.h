@@ -41,13 +41,16 @@ struct PanelArgs {
     double *vsave, *vrhs, *vy, *vx, *vw, *vw2, *vr;  // n-vectors, absolute row index
     double *part;       // gridDim x PW partial sums
     int pw;
-    unsigned *flags;    // trsv flags (per 64-row block)
+    unsigned *flags;    // trsv flags (per 128-row block)
+    double *Dinv;       // inverted 128x128 diagonal blocks of B(s+1:n, s+1:n)
+    int *dsafe;         // per block: 1 = use Dinv, 0 = sequential scaled substitution
     int *bexp;          // trsv block exponents
     unsigned epoch;     // trsv flag epoch base
     double tol;         // 2 u ||B||_F
     int max_ir;         // 10
     const int64_t *force_fail;  // sorted list of columns whose IR is forced to fail (test hook)
     int n_force_fail;
+    double *dbg;        // optional (HT_DEBUG_IR): dbg[j*12 + it] = ||r||/(tol ||x||) per IR iteration
     int *irtrace;       // per-column IR count (+1000 after a failed attempt)
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
 };

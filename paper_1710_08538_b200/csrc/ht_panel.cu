@@ -15,10 +15,15 @@
 //       y = gamma (A v - Y V^T v)                                   (sec. 3.2.2d)
 // Rows 1:s of Y and of the panel columns are deferred (Remark 2).
 //
-// Every phase boundary is a grid-wide barrier (cooperative launch); the
-// triangular solve is a flag-chained block back-substitution with per-block
-// power-of-two exponents (overflow-safe, reading R-Z8), so the IR loop and the
-// fallback are decided on the device without host round trips.
+// B200 design: one CTA per SM, grid-wide barriers between
+// phases, no host round trip per column (the IR loop and the fallback are
+// decided on the device).  The triangular solve is a flag-chained block
+// back-substitution over 128-row blocks: each block is solved with its
+// pre-inverted diagonal block (held in shared memory for the solve), or, when
+// the block is unsafe to invert (tiny pivots, config 4), by an overflow-safe
+// sequential back-substitution; every block carries a power-of-two exponent
+// (reading R-Z8), so y~ never overflows.  HBM-bound sweeps (B w, A v, the
+// off-diagonal solve tiles) are issued with many independent loads per thread.
 #include <cooperative_groups.h>
 #include "ht_common.cuh"
 #include "ht_internal.h"
@@ -29,18 +34,19 @@ namespace {
 
 constexpr int PNT = 512;   // threads per CTA
 constexpr int NWP = PNT / 32;
-constexpr int TB = 64;     // triangular-solve block size
+constexpr int TB = 128;    // triangular-solve block size
 constexpr int NBMAX = 256; // max panel width supported
+constexpr int RBMAX = 256; // max own rows per CTA (uniform slabs)
 constexpr double BIG = 0x1p256;
+constexpr int DYN_DOUBLES = TB * TB + 4 * TB;  // Dinv / staging + trsv group partials
 
 struct __align__(16) PanelSmem {
-    double sv1[NBMAX + 1];
-    double sv2[NBMAX + 1];
-    double sv3[NBMAX + 1];
-    double snew[NBMAX + 1];  // new column of S
+    double sv1[NBMAX + 2];
+    double sv2[NBMAX + 2];
+    double sv3[NBMAX + 2];
+    double snew[NBMAX + 2];  // new column of S
+    double vloc[RBMAX];      // own-row vector cache
     double red[32];
-    double accg[8][TB];
-    double D[TB][TB + 1];    // diagonal block of B (trsv)
     double rhs[TB];
     int ival[4];
 };
@@ -55,15 +61,21 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void *p)
+{
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 struct Ctx {
     const PanelArgs &a;
     PanelSmem &sm;
+    double *dyn;
     int G, bid, tid, lane, warp;
     int64_t n, p0, M, rb0, rb1;
+    int nr;
     double *part[2];
     int ph;
-    __device__ Ctx(const PanelArgs &aa, PanelSmem &s) : a(aa), sm(s)
+    __device__ Ctx(const PanelArgs &aa, PanelSmem &s, double *d) : a(aa), sm(s), dyn(d)
     {
         G = gridDim.x;
         bid = blockIdx.x;
@@ -75,25 +87,61 @@ struct Ctx {
         M = n - p0;
         int64_t RB = (M + G - 1) / G;
         rb0 = p0 + (int64_t)bid * RB;
-        rb1 = rb0 + RB < n ? rb0 + RB : n;
         if (rb0 > n) rb0 = n;
+        rb1 = rb0 + RB < n ? rb0 + RB : n;
+        nr = (int)(rb1 - rb0);
         part[0] = a.part;
         part[1] = a.part + (size_t)G * a.pw;
         ph = 0;
     }
     __device__ double *mypart() { return part[ph & 1] + (size_t)bid * a.pw; }
     __device__ double *curpart() { return part[ph & 1]; }
-    // out[c] = sum_{r in [rb0,rb1)} X(r,c) * vec(r)   (c < ncols), into mypart()[off + c]
-    template <class F>
-    __device__ void rows_tdot(const double *X, int64_t ldx, int ncols, F vec, int off)
+
+    // out[c] = sum over own rows of X(r,c) * vloc[r - rb0], c < ncols -> mypart()[off + c].
+    // Per-lane partials go through shared staging so that every warp keeps many
+    // independent loads in flight (no shuffle per column).
+    __device__ void coltdot(const double *X, int64_t ldx, int ncols, int off)
     {
-        double *out = mypart() + off;
+        double *stg = dyn;  // ncols x 33
         for (int c = warp; c < ncols; c += NWP) {
             double s = 0.0;
-            for (int64_t r = rb0 + lane; r < rb1; r += 32) s += X[(size_t)c * ldx + r] * vec(r);
-            s = warp_sum(s);
-            if (lane == 0) out[c] = s;
+            const double *xp = X + (size_t)c * ldx + rb0;
+#pragma unroll 4
+            for (int rl = lane; rl < nr; rl += 32) s += xp[rl] * sm.vloc[rl];
+            stg[c * 33 + lane] = s;
         }
+        __syncthreads();
+        double *out = mypart() + off;
+        for (int c = tid; c < ncols; c += PNT) {
+            double t = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
+            out[c] = t;
+        }
+        __syncthreads();
+    }
+    // returns (in dyn[rl]) sum_c X(rb0+rl, c) * coef[c] for own rows; all warps split the columns.
+    __device__ void rowgemv(const double *X, int64_t ldx, int ncols, const double *coef)
+    {
+        double *stg = dyn + TB * 4;  // NWP x RBMAX
+        for (int rc = 0; rc < nr; rc += 32) {
+            const int rl = rc + lane;
+            double s = 0.0;
+            if (rl < nr) {
+                const double *xp = X + rb0 + rl;
+#pragma unroll 4
+                for (int c = warp; c < ncols; c += NWP) s += xp[(size_t)c * ldx] * coef[c];
+            }
+            stg[warp * RBMAX + rl] = s;
+        }
+        __syncthreads();
+        for (int rl = tid; rl < nr; rl += PNT) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWP; ++w) t += stg[w * RBMAX + rl];
+            dyn[rl] = t;
+        }
+        __syncthreads();
     }
     // after a grid sync: dst[c] = sum_b part[b][off + c]  (fixed order: deterministic)
     __device__ void gather(double *dst, int ncols, int off)
@@ -114,21 +162,42 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------------------
-// Overflow-safe block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs.
-// Block b (TB rows, from the top) is owned by CTA (Nb-1-b) mod G and published
-// through flags[b] = epoch with exponent bexp[b]: true y~ = 2^bexp[b] * vy.
-// rhs(r) = base(r) - U(r, 0:ku) z2 is formed on the fly.
-template <class BaseF>
-__device__ void trsv_scaled(Ctx &C, BaseF base, int ku, const double *z2, unsigned epoch)
+// Block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs  (flag chain, 128-row blocks).
+// rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k).
+// Block b is owned by CTA (Nb-1-b) mod G; published through flags[b] = epoch,
+// exponent bexp[b]: true y~ = 2^bexp[b] * vy.
+template <class BaseF, class UnewF>
+__device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, unsigned epoch)
 {
     const PanelArgs &a = C.a;
     PanelSmem &sm = C.sm;
+    double *Dsm = C.dyn;             // TB x TB (Dinv, or D for the sequential path)
+    double *accg = C.dyn + TB * TB;  // 4 x TB
     const int64_t n = C.n, p0 = C.p0, M = C.M;
     const int Nb = (int)((M + TB - 1) / TB);
-    const int ri = C.tid & (TB - 1), grp = C.tid >> 6;  // 64 rows x 8 column groups
+    const int ri = C.tid & (TB - 1), grp = C.tid >> 7;  // 128 rows x 4 column groups
     for (int b = Nb - 1 - C.bid; b >= 0; b -= C.G) {
         const int64_t r0 = p0 + (int64_t)b * TB;
         const int h = (int)(n - r0 < TB ? n - r0 : TB);
+        const bool safe = a.dsafe[b] != 0;
+        // stage Dinv (safe) or D (unsafe) of this block in shared memory
+        if (safe) {
+            const double *src = a.Dinv + (size_t)b * TB * TB;
+            for (int idx = C.tid; idx < TB * TB; idx += PNT) Dsm[idx] = src[idx];
+        } else {
+            for (int idx = C.tid; idx < TB * TB; idx += PNT) {
+                int i = idx & (TB - 1), j = idx >> 7;
+                Dsm[idx] = (i < h && j < h && i <= j) ? a.B[(size_t)(r0 + j) * a.ldb + r0 + i] : 0.0;
+            }
+        }
+        // warm L2 with the critical-path tile (b, b+1)
+        if (b + 1 < Nb) {
+            const int64_t c0 = p0 + (int64_t)(b + 1) * TB;
+            for (int idx = C.tid; idx < TB * 2; idx += PNT) {
+                int col = idx >> 1, half = idx & 1;
+                if (c0 + col < n) prefetch_l2(a.B + (size_t)(c0 + col) * a.ldb + r0 + half * 64);
+            }
+        }
         double acc = 0.0;
         int Eacc = 0;
         for (int cb = Nb - 1; cb > b; --cb) {
@@ -138,78 +207,117 @@ __device__ void trsv_scaled(Ctx &C, BaseF base, int ku, const double *z2, unsign
                 while (ld_acquire(&a.flags[cb]) != epoch) {
                 }
                 __threadfence();
-                sm.ival[0] = __ldcg(&a.bexp[cb]);
+                sm.ival[cb & 1] = __ldcg(&a.bexp[cb]);
             }
             __syncthreads();
-            const int ecb = sm.ival[0];
+            const int ecb = sm.ival[cb & 1];
             if (ecb > Eacc) {
                 acc = ldexp(acc, Eacc - ecb);
                 Eacc = ecb;
             }
-            const double scl = ldexp(1.0, ecb - Eacc);
             if (ri < h) {
                 const double *bp = a.B + (size_t)c0 * a.ldb + r0 + ri;
-                double s = 0.0;
-                for (int cc = grp; cc < w; cc += 8) s += bp[(size_t)cc * a.ldb] * __ldcg(&a.vy[c0 + cc]);
-                acc += s * scl;
+                const double *yp = a.vy + c0;
+                double s0 = 0.0, s1 = 0.0;
+                int cc = grp;
+#pragma unroll 4
+                for (; cc + 4 < w; cc += 8) {
+                    s0 += bp[(size_t)cc * a.ldb] * __ldcg(yp + cc);
+                    s1 += bp[(size_t)(cc + 4) * a.ldb] * __ldcg(yp + cc + 4);
+                }
+                for (; cc < w; cc += 4) s0 += bp[(size_t)cc * a.ldb] * __ldcg(yp + cc);
+                acc += (s0 + s1) * ldexp(1.0, ecb - Eacc);
             }
-            __syncthreads();
         }
-        sm.accg[grp][ri] = acc;
-        // stage the diagonal block
-        for (int idx = C.tid; idx < TB * TB; idx += PNT) {
-            int i = idx & (TB - 1), j = idx >> 6;
-            sm.D[i][j] = (i < h && j < h && i <= j) ? a.B[(size_t)(r0 + j) * a.ldb + r0 + i] : 0.0;
-        }
+        accg[grp * TB + ri] = acc;
         __syncthreads();
         if (C.tid < TB) {
-            double s = 0.0;
-            for (int g = 0; g < 8; ++g) s += sm.accg[g][C.tid];
             double rv = 0.0;
             if (C.tid < h) {
                 const int64_t r = r0 + C.tid;
+                double s = accg[C.tid] + accg[TB + C.tid] + accg[2 * TB + C.tid] + accg[3 * TB + C.tid];
                 double u = 0.0;
-                for (int c = 0; c < ku; ++c) u += a.U[(size_t)c * n + r] * z2[c];
+                for (int c = 0; c < k; ++c) u += a.U[(size_t)c * n + r] * z2[c];
+                u += unew(r) * z2[k];
                 rv = ldexp(base(r) - u, -Eacc) - s;
             }
             sm.rhs[C.tid] = rv;
         }
         __syncthreads();
-        if (C.warp == 0) {
-            const int l = C.lane;
-            double v0 = sm.rhs[l], v1 = sm.rhs[l + 32];
-            int e = Eacc;
-            for (int c = h - 1; c >= 0; --c) {
-                const int own = c & 31, hi = c >> 5;
-                double mine = hi ? v1 : v0;
-                double xc = __shfl_sync(0xffffffffu, mine, own) / sm.D[c][c];
-                if (!(fabs(xc) <= BIG)) {  // rescale everything by 2^-ex (exact)
-                    int ex;
-                    frexp(xc, &ex);
-                    v0 = ldexp(v0, -ex);
-                    v1 = ldexp(v1, -ex);
-                    e += ex;
-                    mine = hi ? v1 : v0;
-                    xc = __shfl_sync(0xffffffffu, mine, own) / sm.D[c][c];
+        int e = Eacc;
+        if (safe) {
+            // x = Dinv * rhs   (Dinv column-major TB x TB)
+            double s = 0.0;
+#pragma unroll 8
+            for (int l = grp; l < TB; l += 4) s += Dsm[l * TB + ri] * sm.rhs[l];
+            accg[grp * TB + ri] = s;
+            __syncthreads();
+            double xv = 0.0;
+            if (C.tid < TB) xv = accg[C.tid] + accg[TB + C.tid] + accg[2 * TB + C.tid] + accg[3 * TB + C.tid];
+            // post-hoc power-of-two rescale if the block solution is too large
+            double mx = (C.tid < h) ? fabs(xv) : 0.0;
+            mx = warp_max(mx);
+            if (C.tid < TB && C.lane == 0) sm.red[C.warp] = mx;
+            __syncthreads();
+            mx = fmax(fmax(sm.red[0], sm.red[1]), fmax(sm.red[2], sm.red[3]));
+            int ex = 0;
+            if (!(mx <= BIG)) frexp(mx, &ex);
+            if (C.tid < h) a.vy[r0 + C.tid] = ldexp(xv, -ex);
+            e += ex;
+        } else {
+            if (C.warp == 0) {
+                // overflow-safe sequential back-substitution (unsafe block, e.g. config 4)
+                const int l = C.lane;
+                double v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = sm.rhs[l + 32 * q];
+                for (int c = h - 1; c >= 0; --c) {
+                    const int own = c & 31, hq = c >> 5;
+                    double mine = v[0];
+                    if (hq == 1) mine = v[1];
+                    if (hq == 2) mine = v[2];
+                    if (hq == 3) mine = v[3];
+                    const double dcc = Dsm[c * TB + c];
+                    double xc = __shfl_sync(0xffffffffu, mine, own) / dcc;
+                    if (!(fabs(xc) <= BIG)) {
+                        int ex;
+                        frexp(xc, &ex);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) v[q] = ldexp(v[q], -ex);
+                        e += ex;
+                        mine = v[0];
+                        if (hq == 1) mine = v[1];
+                        if (hq == 2) mine = v[2];
+                        if (hq == 3) mine = v[3];
+                        xc = __shfl_sync(0xffffffffu, mine, own) / dcc;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int row = l + 32 * q;
+                        if (row == c) v[q] = xc;
+                        else if (row < c) v[q] -= Dsm[c * TB + row] * xc;
+                    }
                 }
-                if (l == own) {
-                    if (hi) v1 = xc; else v0 = xc;
-                }
-                if (l < c) v0 -= sm.D[l][c] * xc;
-                if (l + 32 < c) v1 -= sm.D[l + 32][c] * xc;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (l + 32 * q < h) a.vy[r0 + l + 32 * q] = v[q];
+                if (l == 0) sm.ival[2] = e;
             }
-            if (l < h) a.vy[r0 + l] = v0;
-            if (l + 32 < h) a.vy[r0 + l + 32] = v1;
-            if (l == 0) a.bexp[b] = e;
+            __syncthreads();
+            e = sm.ival[2];
+        }
+        __threadfence();
+        __syncthreads();
+        if (C.tid == 0) {
+            a.bexp[b] = e;
             __threadfence();
-            __syncwarp();
-            if (l == 0) st_release(&a.flags[b], epoch);
+            st_release(&a.flags[b], epoch);
         }
         __syncthreads();
     }
 }
 
-// After a completed trsv (grid synced): Emax over all blocks.
+// After a completed solve (grid synced): Emax over all blocks.
 __device__ int trsv_emax(Ctx &C)
 {
     const int Nb = (int)((C.M + TB - 1) / TB);
@@ -218,11 +326,61 @@ __device__ int trsv_emax(Ctx &C)
     return e;
 }
 
+// Row-slab sweep  out(r) = sum_{c in [cbeg, n)} X(r,c) vec(c)  over rows [r0, r1)
+// (TRI: only c >= r): lanes over 32-row chunks, warps over columns, 4 independent
+// accumulators so that every warp keeps 4 column loads in flight.
+template <bool TRI, class VecF>
+__device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int64_t r1, int64_t cfirst, VecF vec,
+                           double *out)
+{
+    double *stg = C.dyn;  // NWP x 32
+    const int64_t n = C.n;
+    for (int64_t rc = r0; rc < r1; rc += 32) {
+        const int64_t row = rc + C.lane;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (row < r1) {
+            const int64_t cb = TRI ? rc : cfirst;
+            const double *xp = X + row;
+            int64_t c = cb + C.warp;
+            for (; c + 3 * NWP < n; c += 4 * NWP) {
+                double x0 = xp[(size_t)c * ldx], x1 = xp[(size_t)(c + NWP) * ldx];
+                double x2 = xp[(size_t)(c + 2 * NWP) * ldx], x3 = xp[(size_t)(c + 3 * NWP) * ldx];
+                double v0 = vec(c), v1 = vec(c + NWP), v2 = vec(c + 2 * NWP), v3 = vec(c + 3 * NWP);
+                if (TRI) {
+                    if (row > c) x0 = 0.0;
+                    if (row > c + NWP) x1 = 0.0;
+                    if (row > c + 2 * NWP) x2 = 0.0;
+                    if (row > c + 3 * NWP) x3 = 0.0;
+                }
+                s0 += x0 * v0;
+                s1 += x1 * v1;
+                s2 += x2 * v2;
+                s3 += x3 * v3;
+            }
+            for (; c < n; c += NWP) {
+                double x0 = xp[(size_t)c * ldx];
+                if (TRI && row > c) x0 = 0.0;
+                s0 += x0 * vec(c);
+            }
+        }
+        stg[C.warp * 32 + C.lane] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (C.tid < 32 && rc + C.tid < r1) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWP; ++w) t += stg[w * 32 + C.tid];
+            out[rc + C.tid] = t;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
 {
     cg::grid_group grid = cg::this_grid();
     __shared__ PanelSmem sm;
-    Ctx C(a, sm);
+    extern __shared__ __align__(16) double dyn[];
+    Ctx C(a, sm, dyn);
     const int64_t n = a.n, s0 = a.s0, p0 = C.p0, lda = a.lda;
     double *A = a.A;
     double *U = a.U, *V = a.V, *Y = a.Y, *S = a.S, *T = a.T;
@@ -231,6 +389,17 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
     int k = 0, failed = 0;
     long long ir_steps = 0, ir_cols = 0, rescales = 0;
     int ffi = 0;  // cursor into the forced-failure list
+    // area-balanced row slabs of the trailing triangle (B w)
+    int64_t tr0, tr1;
+    {
+        double f0 = 1.0 - (double)C.bid / C.G, f1 = 1.0 - (double)(C.bid + 1) / C.G;
+        tr0 = n - (int64_t)llround((double)C.M * sqrt(f0));
+        tr1 = n - (int64_t)llround((double)C.M * sqrt(f1 > 0.0 ? f1 : 0.0));
+        if (C.bid == 0) tr0 = p0;
+        if (C.bid == C.G - 1) tr1 = n;
+        if (tr0 < p0) tr0 = p0;
+        if (tr1 > n) tr1 = n;
+    }
 
     while (k < a.kmax) {
         const int64_t j0 = s0 + k;
@@ -239,15 +408,15 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         // ================= P1: update column j of A =========================
         for (int c = C.tid; c < k; c += PNT) sm.sv1[c] = (c == k - 1) ? 1.0 : V[(size_t)c * n + j0];
         __syncthreads();
-        for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
+        C.rowgemv(Y, n, k, sm.sv1);
+        for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            const int64_t r = C.rb0 + rl;
             double a0 = A[(size_t)j0 * lda + r];
             a.vsave[r] = a0;
-            double s = 0.0;
-            for (int c = 0; c < k; ++c) s += Y[(size_t)c * n + r] * sm.sv1[c];
-            a.vx[r] = a0 - s;
+            sm.vloc[rl] = a0 - dyn[rl];
         }
         __syncthreads();
-        C.rows_tdot(U, n, k, [&](int64_t r) { return a.vx[r]; }, 0);
+        C.coltdot(U, n, k, 0);
         grid.sync();
         C.gather(sm.sv2, k, 0);
         __syncthreads();
@@ -257,23 +426,27 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             sm.sv3[c] = s;
         }
         __syncthreads();
+        C.rowgemv(U, n, k, sm.sv3);
         C.ph++;
         {
             double ss = 0.0;
-            for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
-                double s = 0.0;
-                for (int c = 0; c < k; ++c) s += U[(size_t)c * n + r] * sm.sv3[c];
-                double av = a.vx[r] - s;
+            for (int rl = C.tid; rl < C.nr; rl += PNT) {
+                const int64_t r = C.rb0 + rl;
+                double av = sm.vloc[rl] - dyn[rl];
                 a.vx[r] = av;
+                if (r <= j0) A[(size_t)j0 * lda + r] = av;  // rows s+1:j of the updated column
                 if (r >= j0 + 2) ss += av * av;
+                sm.vloc[rl] = (r >= j0 + 2) ? av : 0.0;     // a_tail for U^T a_tail
             }
+            __syncthreads();
+            C.coltdot(U, n, k, 1);
             C.block_reduce_to_part(ss, 0);
         }
         grid.sync();
-        // ================= P2: left reflector ===============================
+        // ================= P2: left reflector (no barrier needed) ============
         double tau_u, scal_u, beta_u, alpha_u;
         {
-            C.gather(sm.sv1, 1, 0);
+            C.gather(sm.sv1, k + 1, 0);  // [||a_tail||^2, U^T a_tail]
             __syncthreads();
             const double ss = sm.sv1[0];
             alpha_u = __ldcg(&a.vx[j0 + 1]);
@@ -287,20 +460,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 scal_u = 1.0 / (alpha_u - beta_u);
             }
         }
-        __syncthreads();
-        for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
-            double u = (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : a.vx[r] * scal_u);
-            U[(size_t)k * n + r] = u;
-            if (r <= j0) A[(size_t)j0 * lda + r] = a.vx[r];  // rows s+1:j of the updated column (P1)
-            else if (r == j0 + 1) A[(size_t)j0 * lda + r] = beta_u;
-            else if (r >= j0 + 2) A[(size_t)j0 * lda + r] = 0.0;  // Set A(j+2:n, j) <- 0
-        }
-        C.ph++;
-        C.rows_tdot(U, n, k, [&](int64_t r) {
-            return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : a.vx[r] * scal_u);
-        }, 0);
-        grid.sync();
-        C.gather(sm.sv2, k, 0);  // U^T u
+        // U^T u = scal * U^T a_tail + U(j0+1, :)^T   (u(j0+1) = 1)
+        for (int c = C.tid; c < k; c += PNT) sm.sv2[c] = scal_u * sm.sv1[1 + c] + U[(size_t)c * n + j0 + 1];
         __syncthreads();
         for (int i = C.tid; i <= k; i += PNT) {
             double s = 0.0;
@@ -312,15 +473,22 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             }
             sm.snew[i] = s;
         }
+        auto unew = [&](int64_t r) -> double {
+            return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_u);
+        };
+        for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            const int64_t r = C.rb0 + rl;
+            U[(size_t)k * n + r] = unew(r);
+            if (r == j0 + 1) A[(size_t)j0 * lda + r] = beta_u;
+            else if (r >= j0 + 2) A[(size_t)j0 * lda + r] = 0.0;  // Set A(j+2:n, j) <- 0
+        }
         __syncthreads();
         if (C.bid == 0)
             for (int i = C.tid; i <= k; i += PNT) S[(size_t)k * nb + i] = sm.snew[i];
-        // S_{k+1}(i, c): c < k from global S, c == k from snew
         auto Sget = [&](int i, int c) -> double { return c == k ? sm.snew[i] : S[(size_t)c * nb + i]; };
 
-        // ================= P3: solve, P4: residual + IR ======================
-        // z2 = S_{k+1} w, w(c) = U(j0+1, c)
-        for (int i = C.tid; i < ku; i += PNT) {
+        // ================= P3: factored solve ==================================
+        for (int i = C.tid; i < ku; i += PNT) {  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
             double s = 0.0;
             for (int c = i; c < ku; ++c) {
                 double wc = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
@@ -330,56 +498,56 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         }
         __syncthreads();
         ++epoch;
-        trsv_scaled(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, ku, sm.sv3, epoch);
+        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, sm.sv3, epoch);
         grid.sync();
         int emax = trsv_emax(C);
         if (emax > 0) ++rescales;
-        // normalise y~ and form V^T y~
         C.ph++;
-        for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
+        for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            const int64_t r = C.rb0 + rl;
             int eb = __ldcg(&a.bexp[(r - p0) / TB]);
-            a.vy[r] = ldexp(__ldcg(&a.vy[r]), eb - emax);
+            sm.vloc[rl] = ldexp(__ldcg(&a.vy[r]), eb - emax);
         }
         __syncthreads();
-        C.rows_tdot(V, n, k, [&](int64_t r) { return a.vy[r]; }, 0);
+        C.coltdot(V, n, k, 0);
         grid.sync();
-        // x = (y~ - V T^T V^T y~)(j0+1:)
         C.gather(sm.sv1, k, 0);
         __syncthreads();
-        for (int c = C.tid; c < k; c += PNT) {
+        for (int c = C.tid; c < k; c += PNT) {  // sv2 = T^T (V^T y~)
             double s = 0.0;
             for (int i = 0; i <= c; ++i) s += T[(size_t)c * nb + i] * sm.sv1[i];
             sm.sv2[c] = s;
         }
         __syncthreads();
+        C.rowgemv(V, n, k, sm.sv2);
         C.ph++;
         {
             double sx = 0.0, st = 0.0;
-            for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
+            for (int rl = C.tid; rl < C.nr; rl += PNT) {
+                const int64_t r = C.rb0 + rl;
                 double xv = 0.0;
                 if (r >= j0 + 1) {
-                    double s = 0.0;
-                    for (int c = 0; c < k; ++c) s += V[(size_t)c * n + r] * sm.sv2[c];
-                    xv = a.vy[r] - s;
+                    xv = sm.vloc[rl] - dyn[rl];
                     sx += xv * xv;
                     if (r >= j0 + 2) st += xv * xv;
                 }
                 a.vx[r] = xv;
+                sm.vloc[rl] = xv;
             }
             __syncthreads();
-            C.rows_tdot(V, n, k, [&](int64_t r) { return a.vx[r]; }, 2);
+            C.coltdot(V, n, k, 2);
             C.block_reduce_to_part(sx, 0);
             C.block_reduce_to_part(st, 1);
         }
         grid.sync();
         double xnorm2 = 0.0, xtail2 = 0.0;
-        {
-            C.gather(sm.sv1, 2, 0);
-            __syncthreads();
-            xnorm2 = sm.sv1[0];
-            xtail2 = sm.sv1[1];
-            __syncthreads();
-        }
+        C.gather(sm.sv1, 2, 0);
+        __syncthreads();
+        xnorm2 = sm.sv1[0];
+        xtail2 = sm.sv1[1];
+        __syncthreads();
+
+        // ================= P4: residual + iterative refinement ================
         bool accepted = (k == 0);  // k = 0: stable solve, no test (reading R-Z4)
         bool forced = false;
         while (ffi < a.n_force_fail && a.force_fail[ffi] < j0) ++ffi;
@@ -387,8 +555,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         int ir = 0;
         bool this_col_ir = false;
         while (!accepted) {
-            // ---- P4 residual: w = (I - V T V^T)[0; x] ----
-            C.gather(sm.sv1, k, 2);  // V^T x (from the phase that produced x)
+            // w = (I - V T V^T)[0; x]
+            C.gather(sm.sv1, k, 2);  // V^T x
             __syncthreads();
             for (int i = C.tid; i < k; i += PNT) {  // sv2 = T t
                 double s = 0.0;
@@ -396,51 +564,33 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 sm.sv2[i] = s;
             }
             __syncthreads();
-            for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
-                double s = 0.0;
-                for (int c = 0; c < k; ++c) s += V[(size_t)c * n + r] * sm.sv2[c];
-                a.vw[r] = a.vx[r] - s;
+            C.rowgemv(V, n, k, sm.sv2);
+            for (int rl = C.tid; rl < C.nr; rl += PNT) {
+                const int64_t r = C.rb0 + rl;
+                a.vw[r] = __ldcg(&a.vx[r]) - dyn[rl];
             }
             grid.sync();
-            // ---- w2 = B w (area-balanced row slabs of the upper triangle) ----
+            // w2 = B w over area-balanced slabs, + partial U^T w2
             C.ph++;
-            int64_t tr0, tr1;
-            {
-                double f0 = 1.0 - (double)C.bid / C.G, f1 = 1.0 - (double)(C.bid + 1) / C.G;
-                tr0 = n - (int64_t)llround((double)C.M * sqrt(f0));
-                tr1 = n - (int64_t)llround((double)C.M * sqrt(f1 > 0.0 ? f1 : 0.0));
-                if (C.bid == 0) tr0 = p0;
-                if (C.bid == C.G - 1) tr1 = n;
-                if (tr0 < p0) tr0 = p0;
-                if (tr1 > n) tr1 = n;
-            }
-            for (int64_t rc = tr0; rc < tr1; rc += 32) {
-                const int64_t row = rc + C.lane;
-                double s = 0.0;
-                if (row < tr1)
-                    for (int64_t c = rc + C.warp; c < n; c += NWP)
-                        if (row <= c) s += a.B[(size_t)c * a.ldb + row] * a.vw[c];
-                sm.accg[C.warp & 7][C.lane + 32 * (C.warp >> 3)] = s;
-                __syncthreads();
-                if (C.tid < 32 && rc + C.tid < tr1) {
-                    double t2 = 0.0;
-                    for (int g = 0; g < 8; ++g) t2 += sm.accg[g][C.tid] + sm.accg[g][C.tid + 32];
-                    a.vw2[rc + C.tid] = t2;
-                }
-                __syncthreads();
-            }
-            // partial U^T w2 over [tr0, tr1)
+            slab_sweep<true>(C, a.B, a.ldb, tr0, tr1, 0, [&](int64_t c) { return __ldcg(&a.vw[c]); }, a.vw2);
             {
                 double *out = C.mypart();
+                double *stg = dyn;
                 for (int c = C.warp; c < ku; c += NWP) {
                     double s = 0.0;
+#pragma unroll 4
                     for (int64_t r = tr0 + C.lane; r < tr1; r += 32) s += U[(size_t)c * n + r] * a.vw2[r];
-                    s = warp_sum(s);
-                    if (C.lane == 0) out[c] = s;
+                    stg[c * 33 + C.lane] = s;
+                }
+                __syncthreads();
+                for (int c = C.tid; c < ku; c += PNT) {
+                    double t = 0.0;
+                    for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
+                    out[c] = t;
                 }
             }
             grid.sync();
-            // ---- r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:) ----
+            // r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:)
             C.gather(sm.sv1, ku, 0);
             __syncthreads();
             for (int c = C.tid; c < ku; c += PNT) {  // sv2 = S^T t
@@ -449,22 +599,23 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 sm.sv2[c] = s;
             }
             __syncthreads();
+            C.rowgemv(U, n, ku, sm.sv2);
             C.ph++;
             const double sigma = ldexp(1.0, -emax);
             {
                 double sr = 0.0;
-                for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
+                for (int rl = C.tid; rl < C.nr; rl += PNT) {
+                    const int64_t r = C.rb0 + rl;
                     double rv = 0.0;
                     if (r >= j0 + 1) {
-                        double s = 0.0;
-                        for (int c = 0; c < ku; ++c) s += U[(size_t)c * n + r] * sm.sv2[c];
-                        rv = (r == j0 + 1 ? sigma : 0.0) - (a.vw2[r] - s);
+                        rv = (r == j0 + 1 ? sigma : 0.0) - (__ldcg(&a.vw2[r]) - dyn[rl]);
                         sr += rv * rv;
                     }
                     a.vr[r] = rv;
+                    sm.vloc[rl] = rv;
                 }
                 __syncthreads();
-                C.rows_tdot(U, n, ku, [&](int64_t r) { return a.vr[r]; }, 1);
+                C.coltdot(U, n, ku, 1);
                 C.block_reduce_to_part(sr, 0);
             }
             grid.sync();
@@ -472,6 +623,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             __syncthreads();
             const double rn = sqrt(sm.sv1[0]), xn = sqrt(xnorm2);
             __syncthreads();
+            if (a.dbg && C.bid == 0 && C.tid == 0 && ir < 12) a.dbg[j0 * 12 + ir] = rn / (a.tol * xn);
             if (!forced && rn <= a.tol * xn && isfinite(rn)) {
                 accepted = true;
                 break;
@@ -490,17 +642,16 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             }
             __syncthreads();
             ++epoch;
-            trsv_scaled(C, [&](int64_t r) { return __ldcg(&a.vr[r]); }, ku, sm.sv3, epoch);
+            // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
+            trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
+                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, sm.sv3, epoch);
             grid.sync();
             const int ec = trsv_emax(C);
-            if (ec > 0) { ++rescales; break; }  // a rescaled correction counts as IR failure (C.8)
+            if (ec > 0) { ++rescales; break; }  // a rescaled correction counts as IR failure
             C.ph++;
-            for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
-                int eb = __ldcg(&a.bexp[(r - p0) / TB]);
-                a.vy[r] = ldexp(__ldcg(&a.vy[r]), eb);
-            }
+            for (int rl = C.tid; rl < C.nr; rl += PNT) sm.vloc[rl] = __ldcg(&a.vy[C.rb0 + rl]);
             __syncthreads();
-            C.rows_tdot(V, n, k, [&](int64_t r) { return a.vy[r]; }, 0);
+            C.coltdot(V, n, k, 0);
             grid.sync();
             C.gather(sm.sv1, k, 0);
             __syncthreads();
@@ -510,22 +661,23 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 sm.sv2[c] = s;
             }
             __syncthreads();
+            C.rowgemv(V, n, k, sm.sv2);
             C.ph++;
             {
                 double sx = 0.0, st = 0.0;
-                for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
+                for (int rl = C.tid; rl < C.nr; rl += PNT) {
+                    const int64_t r = C.rb0 + rl;
                     double xv = 0.0;
                     if (r >= j0 + 1) {
-                        double s = 0.0;
-                        for (int c = 0; c < k; ++c) s += V[(size_t)c * n + r] * sm.sv2[c];
-                        xv = a.vx[r] + (a.vy[r] - s);
+                        xv = __ldcg(&a.vx[r]) + (sm.vloc[rl] - dyn[rl]);
                         sx += xv * xv;
                         if (r >= j0 + 2) st += xv * xv;
                     }
                     a.vx[r] = xv;
+                    sm.vloc[rl] = xv;
                 }
                 __syncthreads();
-                C.rows_tdot(V, n, k, [&](int64_t r) { return a.vx[r]; }, 2);
+                C.coltdot(V, n, k, 2);
                 C.block_reduce_to_part(sx, 0);
                 C.block_reduce_to_part(st, 1);
             }
@@ -537,10 +689,11 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             __syncthreads();
         }
         if (this_col_ir) ++ir_cols;
-        if (C.bid == 0 && C.tid == 0) a.irtrace[j0] = (accepted ? 0 : 1000) + (a.irtrace[j0] >= 1000 ? 1000 : 0) + ir;
+        if (C.bid == 0 && C.tid == 0)
+            a.irtrace[j0] = (accepted ? 0 : 1000) + (a.irtrace[j0] >= 1000 ? 1000 : 0) + ir;
         if (!accepted) {
             // undo the left reflector: restore column j of A (Algorithm 1)
-            for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) A[(size_t)j0 * lda + r] = a.vsave[r];
+            for (int rl = C.tid; rl < C.nr; rl += PNT) A[(size_t)j0 * lda + C.rb0 + rl] = a.vsave[C.rb0 + rl];
             failed = 1;
             break;
         }
@@ -561,23 +714,16 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_v);
         };
         C.ph++;
-        for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) V[(size_t)k * n + r] = vget(r);
-        C.rows_tdot(V, n, k, vget, 0);
-        // A(p0:n, j0+1:n) v over own rows: lanes over rows, warps over columns
-        for (int64_t rc = C.rb0; rc < C.rb1; rc += 32) {
-            const int64_t row = rc + C.lane;
-            double s = 0.0;
-            if (row < C.rb1)
-                for (int64_t c = j0 + 1 + C.warp; c < n; c += NWP) s += A[(size_t)c * lda + row] * vget(c);
-            sm.accg[C.warp & 7][C.lane + 32 * (C.warp >> 3)] = s;
-            __syncthreads();
-            if (C.tid < 32 && rc + C.tid < C.rb1) {
-                double t2 = 0.0;
-                for (int g = 0; g < 8; ++g) t2 += sm.accg[g][C.tid] + sm.accg[g][C.tid + 32];
-                a.vw2[rc + C.tid] = t2;
-            }
-            __syncthreads();
+        for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            const int64_t r = C.rb0 + rl;
+            double v = vget(r);
+            V[(size_t)k * n + r] = v;
+            sm.vloc[rl] = v;
         }
+        __syncthreads();
+        C.coltdot(V, n, k, 0);
+        // A(p0:n, j0+1:n) v over own rows
+        slab_sweep<false>(C, A, lda, C.rb0, C.rb1, j0 + 1, vget, a.vw2);
         grid.sync();
         C.gather(sm.sv1, k, 0);  // z = V^T v
         __syncthreads();
@@ -592,10 +738,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 }
                 T[(size_t)k * nb + i] = s;
             }
-        for (int64_t r = C.rb0 + C.tid; r < C.rb1; r += PNT) {
-            double s = 0.0;
-            for (int c = 0; c < k; ++c) s += Y[(size_t)c * n + r] * sm.sv1[c];
-            Y[(size_t)k * n + r] = gam * (a.vw2[r] - s);
+        C.rowgemv(Y, n, k, sm.sv1);
+        for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            const int64_t r = C.rb0 + rl;
+            Y[(size_t)k * n + r] = gam * (a.vw2[r] - dyn[rl]);
         }
         ++k;
         __syncthreads();
@@ -611,6 +757,57 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
     }
 }
 
+// Inverse of each TB x TB diagonal block of B(p0:n, p0:n) (column-major, ld TB) and a
+// safety flag: finite, max|inv| <= 2^200, and max|inv| * max|D| <= 1e12 (else the
+// panel uses the overflow-safe sequential substitution for that block).
+__global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
+                                                      double *Dinv, int *dsafe)
+{
+    extern __shared__ __align__(16) double X[];  // TB x TB, column j = thread j
+    __shared__ double smax[2][TB / 32];
+    const int b = blockIdx.x, j = threadIdx.x;
+    const int64_t r0 = p0 + (int64_t)b * TB;
+    const int h = (int)(n - r0 < TB ? n - r0 : TB);
+    const double *D = B + r0 + r0 * ldb;
+    for (int i = 0; i < TB; ++i) X[j * TB + i] = (i == j && j < h) ? 1.0 : 0.0;
+    double dmax = 0.0;
+    if (j < h) {
+        for (int i = 0; i <= j; ++i) dmax = fmax(dmax, fabs(D[(size_t)j * ldb + i]));
+        // column j of D^{-1}: column-oriented back substitution on e_j
+        double *x = X + j * TB;
+        for (int l = j; l >= 0; --l) {
+            const double xl = x[l] / D[(size_t)l * ldb + l];
+            x[l] = xl;
+            if (xl != 0.0)
+                for (int i = 0; i < l; ++i) x[i] -= D[(size_t)l * ldb + i] * xl;
+        }
+    }
+    double imax = 0.0;
+    bool fin = true;
+    for (int i = 0; i < TB; ++i) {
+        double v = X[j * TB + i];
+        if (!isfinite(v)) fin = false;
+        imax = fmax(imax, fabs(v));
+    }
+    if (!fin) imax = INFINITY;
+    double a1 = warp_max(imax), a2 = warp_max(dmax);
+    if ((j & 31) == 0) {
+        smax[0][j >> 5] = a1;
+        smax[1][j >> 5] = a2;
+    }
+    __syncthreads();
+    double *out = Dinv + (size_t)b * TB * TB;
+    for (int i = 0; i < TB; ++i) out[j * TB + i] = X[j * TB + i];
+    if (j == 0) {
+        double im = 0.0, dm = 0.0;
+        for (int w = 0; w < TB / 32; ++w) {
+            im = fmax(im, smax[0][w]);
+            dm = fmax(dm, smax[1][w]);
+        }
+        dsafe[b] = (isfinite(im) && im <= 0x1p200 && im * dm <= 1e12) ? 1 : 0;
+    }
+}
+
 }  // namespace
 
 int ht_panel_max_blocks(int *nblocks_out)
@@ -618,15 +815,25 @@ int ht_panel_max_blocks(int *nblocks_out)
     int dev = 0, nsm = 0, per = 0;
     HT_CUDA_TRY(cudaGetDevice(&dev));
     HT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    HT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, panel_kernel, PNT, 0));
+    HT_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     DYN_DOUBLES * (int)sizeof(double)));
+    HT_CUDA_TRY(cudaFuncSetAttribute(inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TB * TB * (int)sizeof(double)));
+    HT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, panel_kernel, PNT,
+                                                              DYN_DOUBLES * sizeof(double)));
     if (per < 1) return 4;
-    *nblocks_out = nsm * (per > 1 ? 1 : per);
+    *nblocks_out = nsm;
     return 0;
 }
 
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
 {
+    const int64_t M = a->n - a->s0 - 1;
+    const int Nb = (int)((M + TB - 1) / TB);
+    inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
+    HT_CUDA_TRY(cudaGetLastError());
     void *args[] = {(void *)a};
-    HT_CUDA_TRY(cudaLaunchCooperativeKernel((void *)panel_kernel, dim3(nblocks), dim3(PNT), args, 0, st));
+    HT_CUDA_TRY(cudaLaunchCooperativeKernel((void *)panel_kernel, dim3(nblocks), dim3(PNT), args,
+                                            DYN_DOUBLES * sizeof(double), st));
     return 0;
 }
