@@ -709,6 +709,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
         HT_CUDA_TRY(cudaMemsetAsync(w->d_irtrace, 0, (size_t)n * sizeof(int), st));
         double *dbg = nullptr;
         const bool dbg_on = getenv("HT_DEBUG_IR") != nullptr;
+        double *ptime = nullptr;
+        const bool prof_on = getenv("HT_PROFILE") != nullptr;
+        if (prof_on) {
+            HT_CUDA_TRY(cudaMalloc((void **)&ptime, 16 * sizeof(double)));
+            HT_CUDA_TRY(cudaMemset(ptime, 0, 16 * sizeof(double)));
+        }
         if (dbg_on) {
             HT_CUDA_TRY(cudaMalloc((void **)&dbg, (size_t)n * 12 * sizeof(double)));
             HT_CUDA_TRY(cudaMemset(dbg, 0, (size_t)n * 12 * sizeof(double)));
@@ -736,6 +742,7 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.out = w->d_out;
             pa.irtrace = w->d_irtrace;
             pa.dbg = dbg;
+            pa.ptime = ptime;
             const int64_t M = n - s0 - 1;
             int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 31) / 32));
             R.tm.begin(st, 0);
@@ -761,6 +768,16 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             if (opt && opt->max_panels > 0 && R.rep.panels >= opt->max_panels) break;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (prof_on) {
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            double hp[16];
+            HT_CUDA_TRY(cudaMemcpy(hp, ptime, sizeof(hp), cudaMemcpyDeviceToHost));
+            const char *names[8] = {"P1", "P2+trsv", "P3 rest", "P4 r+IR", "P5 A*v", "P5 Y", "P4 w", "P4 B*w"};
+            fprintf(stderr, "[ht profile] panel phases (s):");
+            for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.3f", names[i], hp[i]);
+            fprintf(stderr, "\n");
+            cudaFree(ptime);
+        }
         if (dbg_on) {
             HT_CUDA_TRY(cudaStreamSynchronize(st));
             std::vector<double> hd((size_t)n * 12);

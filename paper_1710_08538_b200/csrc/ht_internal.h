@@ -50,6 +50,7 @@ struct PanelArgs {
     int max_ir;         // 10
     const int64_t *force_fail;  // sorted list of columns whose IR is forced to fail (test hook)
     int n_force_fail;
+    double *ptime;      // optional (HT_PROFILE): per-phase seconds, CTA 0 (globaltimer)
     double *dbg;        // optional (HT_DEBUG_IR): dbg[j*12 + it] = ||r||/(tol ||x||) per IR iteration
     int *irtrace;       // per-column IR count (+1000 after a failed attempt)
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used

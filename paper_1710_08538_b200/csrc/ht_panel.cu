@@ -61,6 +61,12 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void prefetch_l2(const void *p)
 {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -143,15 +149,54 @@ struct Ctx {
         }
         __syncthreads();
     }
-    // after a grid sync: dst[c] = sum_b part[b][off + c]  (fixed order: deterministic)
+    // after a grid sync: dst[c] = sum_b part[b][off + c]  (fixed order: deterministic).
+    // Lanes split the CTA partials, warps split the columns; per-lane sums are staged
+    // in shared memory so the L2 loads of all columns are in flight together.
     __device__ void gather(double *dst, int ncols, int off)
     {
-        const double *pp = curpart();
-        for (int c = tid; c < ncols; c += PNT) {
+        const double *pp = curpart() + off;
+        double *stg = dyn + TB * TB;  // reuse the tail of the dynamic buffer: ncols x 33 doubles
+        if (ncols * 33 > 4 * TB) stg = dyn;
+#pragma unroll 4
+        for (int c = warp; c < ncols; c += NWP) {
             double s = 0.0;
-            for (int b = 0; b < G; ++b) s += pp[(size_t)b * a.pw + off + c];
-            dst[c] = s;
+            for (int b = lane; b < G; b += 32) s += pp[(size_t)b * a.pw + c];
+            stg[c * 33 + lane] = s;
         }
+        __syncthreads();
+        for (int c = tid; c < ncols; c += PNT) {
+            double t = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
+            dst[c] = t;
+        }
+        __syncthreads();
+    }
+    // Upper-triangular k x k mat-vec with the matrix in global memory (L2):
+    //   !TR: out[i] = sum_{c >= i} M(i,c) v[c];   TR: out[c] = sum_{i <= c} M(i,c) v[i]
+    // scale multiplies the result.  All warps; per-lane partials staged in smem.
+    template <bool TR, class MF>
+    __device__ void trimv(MF Mget, int m, const double *v, double *out, double scale = 1.0)
+    {
+        double *stg = dyn;  // m x 33
+#pragma unroll 2
+        for (int o = warp; o < m; o += NWP) {
+            double s = 0.0;
+            if (!TR) {
+                for (int c = o + lane; c < m; c += 32) s += Mget(o, c) * v[c];
+            } else {
+                for (int i = lane; i <= o; i += 32) s += Mget(i, o) * v[i];
+            }
+            stg[o * 33 + lane] = s;
+        }
+        __syncthreads();
+        for (int o = tid; o < m; o += PNT) {
+            double t = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < 32; ++l) t += stg[o * 33 + l];
+            out[o] = scale * t;
+        }
+        __syncthreads();
     }
     __device__ double block_reduce_to_part(double v, int off)
     {
@@ -189,6 +234,28 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                 int i = idx & (TB - 1), j = idx >> 7;
                 Dsm[idx] = (i < h && j < h && i <= j) ? a.B[(size_t)(r0 + j) * a.ldb + r0 + i] : 0.0;
             }
+        }
+        // rhs part that does not depend on the solution (off the critical path):
+        // rb(i) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k), all 512 threads
+        {
+            const int64_t r = r0 + ri;
+            double u = 0.0;
+            if (ri < h) {
+#pragma unroll 4
+                for (int c = grp; c < k; c += 4) u += a.U[(size_t)c * n + r] * z2[c];
+            }
+            accg[grp * TB + ri] = u;
+            __syncthreads();
+            if (C.tid < TB) {
+                double rb = 0.0;
+                if (C.tid < h) {
+                    const int64_t rr = r0 + C.tid;
+                    rb = base(rr) - ((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]))
+                         - unew(rr) * z2[k];
+                }
+                sm.rhs[C.tid] = rb;
+            }
+            __syncthreads();
         }
         // warm L2 with the critical-path tile (b, b+1)
         if (b + 1 < Nb) {
@@ -234,12 +301,8 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         if (C.tid < TB) {
             double rv = 0.0;
             if (C.tid < h) {
-                const int64_t r = r0 + C.tid;
                 double s = accg[C.tid] + accg[TB + C.tid] + accg[2 * TB + C.tid] + accg[3 * TB + C.tid];
-                double u = 0.0;
-                for (int c = 0; c < k; ++c) u += a.U[(size_t)c * n + r] * z2[c];
-                u += unew(r) * z2[k];
-                rv = ldexp(base(r) - u, -Eacc) - s;
+                rv = ldexp(sm.rhs[C.tid], -Eacc) - s;
             }
             sm.rhs[C.tid] = rv;
         }
@@ -333,42 +396,59 @@ template <bool TRI, class VecF>
 __device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int64_t r1, int64_t cfirst, VecF vec,
                            double *out)
 {
-    double *stg = C.dyn;  // NWP x 32
+    double *stg = C.dyn;  // NWP x 64
     const int64_t n = C.n;
-    for (int64_t rc = r0; rc < r1; rc += 32) {
-        const int64_t row = rc + C.lane;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (row < r1) {
+    for (int64_t rc = r0; rc < r1; rc += 64) {
+        const int64_t rowA = rc + C.lane, rowB = rc + 32 + C.lane;
+        const bool okA = rowA < r1, okB = rowB < r1;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        if (okA) {
             const int64_t cb = TRI ? rc : cfirst;
-            const double *xp = X + row;
+            const double *xa = X + rowA;
+            const double *xb = X + (okB ? rowB : rowA);
             int64_t c = cb + C.warp;
             for (; c + 3 * NWP < n; c += 4 * NWP) {
-                double x0 = xp[(size_t)c * ldx], x1 = xp[(size_t)(c + NWP) * ldx];
-                double x2 = xp[(size_t)(c + 2 * NWP) * ldx], x3 = xp[(size_t)(c + 3 * NWP) * ldx];
-                double v0 = vec(c), v1 = vec(c + NWP), v2 = vec(c + 2 * NWP), v3 = vec(c + 3 * NWP);
-                if (TRI) {
-                    if (row > c) x0 = 0.0;
-                    if (row > c + NWP) x1 = 0.0;
-                    if (row > c + 2 * NWP) x2 = 0.0;
-                    if (row > c + 3 * NWP) x3 = 0.0;
+                double xa_[4], xb_[4], v_[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    xa_[q] = xa[(size_t)(c + q * NWP) * ldx];
+                    xb_[q] = xb[(size_t)(c + q * NWP) * ldx];
                 }
-                s0 += x0 * v0;
-                s1 += x1 * v1;
-                s2 += x2 * v2;
-                s3 += x3 * v3;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v_[q] = vec(c + q * NWP);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (TRI) {
+                        if (rowA > c + q * NWP) xa_[q] = 0.0;
+                        if (rowB > c + q * NWP) xb_[q] = 0.0;
+                    }
+                    if (q & 1) {
+                        a1 += xa_[q] * v_[q];
+                        b1 += xb_[q] * v_[q];
+                    } else {
+                        a0 += xa_[q] * v_[q];
+                        b0 += xb_[q] * v_[q];
+                    }
+                }
             }
             for (; c < n; c += NWP) {
-                double x0 = xp[(size_t)c * ldx];
-                if (TRI && row > c) x0 = 0.0;
-                s0 += x0 * vec(c);
+                const double v0 = vec(c);
+                double xa0 = xa[(size_t)c * ldx], xb0 = xb[(size_t)c * ldx];
+                if (TRI) {
+                    if (rowA > c) xa0 = 0.0;
+                    if (rowB > c) xb0 = 0.0;
+                }
+                a0 += xa0 * v0;
+                b0 += xb0 * v0;
             }
         }
-        stg[C.warp * 32 + C.lane] = (s0 + s1) + (s2 + s3);
+        stg[C.warp * 64 + C.lane] = a0 + a1;
+        stg[C.warp * 64 + 32 + C.lane] = okB ? b0 + b1 : 0.0;
         __syncthreads();
-        if (C.tid < 32 && rc + C.tid < r1) {
+        if (C.tid < 64 && rc + C.tid < r1) {
             double t = 0.0;
 #pragma unroll
-            for (int w = 0; w < NWP; ++w) t += stg[w * 32 + C.tid];
+            for (int w = 0; w < NWP; ++w) t += stg[w * 64 + C.tid];
             out[rc + C.tid] = t;
         }
         __syncthreads();
@@ -401,6 +481,15 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         if (tr1 > n) tr1 = n;
     }
 
+    const bool prof = a.ptime && C.bid == 0 && C.tid == 0;
+    unsigned long long tp = prof ? gtime() : 0ull;
+    auto mark = [&](int bin) {
+        if (prof) {
+            unsigned long long t = gtime();
+            a.ptime[bin] += (double)(t - tp) * 1e-9;
+            tp = t;
+        }
+    };
     while (k < a.kmax) {
         const int64_t j0 = s0 + k;
         const int ku = k + 1;  // U columns incl. the new u
@@ -420,12 +509,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         grid.sync();
         C.gather(sm.sv2, k, 0);
         __syncthreads();
-        for (int c = C.tid; c < k; c += PNT) {  // sv3 = S^T t
-            double s = 0.0;
-            for (int i = 0; i <= c; ++i) s += S[(size_t)c * nb + i] * sm.sv2[i];
-            sm.sv3[c] = s;
-        }
-        __syncthreads();
+        C.trimv<true>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, sm.sv2, sm.sv3);  // sv3 = S^T t
         C.rowgemv(U, n, k, sm.sv3);
         C.ph++;
         {
@@ -443,6 +527,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             C.block_reduce_to_part(ss, 0);
         }
         grid.sync();
+        mark(0);
         // ================= P2: left reflector (no barrier needed) ============
         double tau_u, scal_u, beta_u, alpha_u;
         {
@@ -463,16 +548,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         // U^T u = scal * U^T a_tail + U(j0+1, :)^T   (u(j0+1) = 1)
         for (int c = C.tid; c < k; c += PNT) sm.sv2[c] = scal_u * sm.sv1[1 + c] + U[(size_t)c * n + j0 + 1];
         __syncthreads();
-        for (int i = C.tid; i <= k; i += PNT) {
-            double s = 0.0;
-            if (i < k) {
-                for (int l = i; l < k; ++l) s += S[(size_t)l * nb + i] * sm.sv2[l];
-                s *= -tau_u;
-            } else {
-                s = tau_u;
-            }
-            sm.snew[i] = s;
-        }
+        C.trimv<false>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, sm.sv2, sm.snew, -tau_u);
+        if (C.tid == 0) sm.snew[k] = tau_u;
         auto unew = [&](int64_t r) -> double {
             return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_u);
         };
@@ -488,18 +565,13 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         auto Sget = [&](int i, int c) -> double { return c == k ? sm.snew[i] : S[(size_t)c * nb + i]; };
 
         // ================= P3: factored solve ==================================
-        for (int i = C.tid; i < ku; i += PNT) {  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
-            double s = 0.0;
-            for (int c = i; c < ku; ++c) {
-                double wc = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
-                s += Sget(i, c) * wc;
-            }
-            sm.sv3[i] = s;
-        }
+        for (int c = C.tid; c < ku; c += PNT) sm.sv1[c] = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
         __syncthreads();
+        C.trimv<false>(Sget, ku, sm.sv1, sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
         trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, sm.sv3, epoch);
         grid.sync();
+        mark(1);
         int emax = trsv_emax(C);
         if (emax > 0) ++rescales;
         C.ph++;
@@ -513,12 +585,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         grid.sync();
         C.gather(sm.sv1, k, 0);
         __syncthreads();
-        for (int c = C.tid; c < k; c += PNT) {  // sv2 = T^T (V^T y~)
-            double s = 0.0;
-            for (int i = 0; i <= c; ++i) s += T[(size_t)c * nb + i] * sm.sv1[i];
-            sm.sv2[c] = s;
-        }
-        __syncthreads();
+        C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);  // T^T (V^T y~)
         C.rowgemv(V, n, k, sm.sv2);
         C.ph++;
         {
@@ -540,6 +607,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             C.block_reduce_to_part(st, 1);
         }
         grid.sync();
+        mark(2);
         double xnorm2 = 0.0, xtail2 = 0.0;
         C.gather(sm.sv1, 2, 0);
         __syncthreads();
@@ -558,12 +626,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             // w = (I - V T V^T)[0; x]
             C.gather(sm.sv1, k, 2);  // V^T x
             __syncthreads();
-            for (int i = C.tid; i < k; i += PNT) {  // sv2 = T t
-                double s = 0.0;
-                for (int c = i; c < k; ++c) s += T[(size_t)c * nb + i] * sm.sv1[c];
-                sm.sv2[i] = s;
-            }
-            __syncthreads();
+            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);  // T t
             C.rowgemv(V, n, k, sm.sv2);
             for (int rl = C.tid; rl < C.nr; rl += PNT) {
                 const int64_t r = C.rb0 + rl;
@@ -572,6 +635,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             grid.sync();
             // w2 = B w over area-balanced slabs, + partial U^T w2
             C.ph++;
+            mark(6);
             slab_sweep<true>(C, a.B, a.ldb, tr0, tr1, 0, [&](int64_t c) { return __ldcg(&a.vw[c]); }, a.vw2);
             {
                 double *out = C.mypart();
@@ -590,15 +654,11 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 }
             }
             grid.sync();
+            mark(7);
             // r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:)
             C.gather(sm.sv1, ku, 0);
             __syncthreads();
-            for (int c = C.tid; c < ku; c += PNT) {  // sv2 = S^T t
-                double s = 0.0;
-                for (int i = 0; i <= c; ++i) s += Sget(i, c) * sm.sv1[i];
-                sm.sv2[c] = s;
-            }
-            __syncthreads();
+            C.trimv<true>(Sget, ku, sm.sv1, sm.sv2);  // S_{k+1}^T t
             C.rowgemv(U, n, ku, sm.sv2);
             C.ph++;
             const double sigma = ldexp(1.0, -emax);
@@ -635,12 +695,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             this_col_ir = true;
             C.gather(sm.sv1, ku, 1);  // U^T r_ext
             __syncthreads();
-            for (int i = C.tid; i < ku; i += PNT) {  // sv3 = S_{k+1} (U^T r)
-                double s = 0.0;
-                for (int c = i; c < ku; ++c) s += Sget(i, c) * sm.sv1[c];
-                sm.sv3[i] = s;
-            }
-            __syncthreads();
+            C.trimv<false>(Sget, ku, sm.sv1, sm.sv3);  // S_{k+1} (U^T r)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
             trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
@@ -655,12 +710,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             grid.sync();
             C.gather(sm.sv1, k, 0);
             __syncthreads();
-            for (int c = C.tid; c < k; c += PNT) {
-                double s = 0.0;
-                for (int i = 0; i <= c; ++i) s += T[(size_t)c * nb + i] * sm.sv1[i];
-                sm.sv2[c] = s;
-            }
-            __syncthreads();
+            C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);
             C.rowgemv(V, n, k, sm.sv2);
             C.ph++;
             {
@@ -688,6 +738,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             xtail2 = sm.sv1[1];
             __syncthreads();
         }
+        mark(3);
         if (this_col_ir) ++ir_cols;
         if (C.bid == 0 && C.tid == 0)
             a.irtrace[j0] = (accepted ? 0 : 1000) + (a.irtrace[j0] >= 1000 ? 1000 : 0) + ir;
@@ -725,19 +776,14 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         // A(p0:n, j0+1:n) v over own rows
         slab_sweep<false>(C, A, lda, C.rb0, C.rb1, j0 + 1, vget, a.vw2);
         grid.sync();
+        mark(4);
         C.gather(sm.sv1, k, 0);  // z = V^T v
         __syncthreads();
-        if (C.bid == 0)
-            for (int i = C.tid; i <= k; i += PNT) {
-                double s = 0.0;
-                if (i < k) {
-                    for (int l = i; l < k; ++l) s += T[(size_t)l * nb + i] * sm.sv1[l];
-                    s *= -gam;
-                } else {
-                    s = gam;
-                }
-                T[(size_t)k * nb + i] = s;
-            }
+        if (C.bid == 0) {
+            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2, -gam);
+            for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = sm.sv2[i];
+            if (C.tid == 0) T[(size_t)k * nb + k] = gam;
+        }
         C.rowgemv(Y, n, k, sm.sv1);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
@@ -745,6 +791,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         }
         ++k;
         __syncthreads();
+        mark(5);
     }
     grid.sync();
     if (C.bid == 0 && C.tid == 0) {
