@@ -40,7 +40,7 @@ struct Work {
     cudaStream_t own_stream = nullptr;
     double *U = nullptr, *V = nullptr, *Y = nullptr, *S = nullptr, *T = nullptr;
     double *vec = nullptr, *part = nullptr;
-    unsigned *flags = nullptr;
+    unsigned long long *flags = nullptr;
     int *bexp = nullptr;
     unsigned epoch = 0;
     int64_t *d_out = nullptr, *h_out = nullptr;
@@ -51,7 +51,7 @@ struct Work {
     double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
-    double *Dinv = nullptr;
+    double *Dinv = nullptr, *Mb = nullptr;
     int *dsafe = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
@@ -123,6 +123,8 @@ void work_free(Work &w)
     if (w.d_irtrace) cudaFree(w.d_irtrace);
     w.d_irtrace = nullptr;
     if (w.Dinv) cudaFree(w.Dinv);
+    if (w.Mb) cudaFree(w.Mb);
+    w.Mb = nullptr;
     if (w.dsafe) cudaFree(w.dsafe);
     w.Dinv = nullptr;
     w.dsafe = nullptr;
@@ -165,9 +167,9 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.vec, 8 * (size_t)N));
     TRY(dalloc(&w.part, 2 * (size_t)w.gmax * (NB + 8)));
     const size_t nblk = (size_t)(N / 64 + 4);
-    if (cudaMalloc((void **)&w.flags, nblk * sizeof(unsigned)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.flags, nblk * sizeof(unsigned long long)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.bexp, nblk * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
-    cudaMemset(w.flags, 0, nblk * sizeof(unsigned));
+    cudaMemset(w.flags, 0, nblk * sizeof(unsigned long long));
     w.epoch = 1;
     if (cudaMalloc((void **)&w.d_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
@@ -189,6 +191,7 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
+    TRY(dalloc(&w.Mb, (size_t)(N / 128 + 2) * 128 * 128));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -736,7 +739,7 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.vw = vv + 4 * N; pa.vw2 = vv + 5 * N; pa.vr = vv + 6 * N;
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.flags = w->flags; pa.bexp = w->bexp; pa.epoch = w->epoch;
-            pa.Dinv = w->Dinv; pa.dsafe = w->dsafe;
+            pa.Dinv = w->Dinv; pa.Mb = w->Mb; pa.dsafe = w->dsafe;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;

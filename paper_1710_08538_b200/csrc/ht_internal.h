@@ -41,8 +41,9 @@ struct PanelArgs {
     double *vsave, *vrhs, *vy, *vx, *vw, *vw2, *vr;  // n-vectors, absolute row index
     double *part;       // gridDim x PW partial sums
     int pw;
-    unsigned *flags;    // trsv flags (per 128-row block)
+    unsigned long long *flags;  // trsv publish words (epoch << 32 | exponent), per 128-row block
     double *Dinv;       // inverted 128x128 diagonal blocks of B(s+1:n, s+1:n)
+    double *Mb;         // Dinv_b * B(block b, block b+1) (look-ahead coupling blocks)
     int *dsafe;         // per block: 1 = use Dinv, 0 = sequential scaled substitution
     int *bexp;          // trsv block exponents
     unsigned epoch;     // trsv flag epoch base

@@ -48,30 +48,16 @@ struct __align__(16) PanelSmem {
     double vloc[RBMAX];      // own-row vector cache
     double red[32];
     double rhs[TB];
+    double cbv[TB];
     int ival[4];
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
-{
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v)
-{
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long gtime()
 {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void prefetch_l2(const void *p)
-{
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 struct Ctx {
     const PanelArgs &a;
     PanelSmem &sm;
@@ -209,14 +195,43 @@ struct Ctx {
 // ---------------------------------------------------------------------------
 // Block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs  (flag chain, 128-row blocks).
 // rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k).
-// Block b is owned by CTA (Nb-1-b) mod G; published through flags[b] = epoch,
-// exponent bexp[b]: true y~ = 2^bexp[b] * vy.
+// Block b is owned by CTA (Nb-1-b) mod G and published through the 64-bit word
+// flags[b] = (epoch << 32) | exponent, where true y~_b = 2^exponent * vy_b.
+// Safe blocks use the look-ahead form  y~_b = c_b - M_b y~_{b+1}  with
+// c_b = Dinv_b (rhs_b - sum_{c > b+1} B_bc y~_c) computed before y~_{b+1} is known
+// and M_b = Dinv_b B_{b,b+1} precomputed per panel, so the chain's critical path
+// is one shared-memory 128x128 mat-vec per block.  Unsafe blocks (tiny pivots)
+// use the overflow-safe sequential substitution.
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// thread 0 spins until block cb is published for `epoch`; returns its exponent (all threads)
+__device__ __forceinline__ int wait_block(Ctx &C, int cb, unsigned epoch, int slot)
+{
+    if (C.tid == 0) {
+        unsigned long long v;
+        do {
+            v = ld_acquire64(&C.a.flags[cb]);
+        } while ((unsigned)(v >> 32) != epoch);
+        C.sm.ival[slot] = (int)(unsigned)(v & 0xffffffffull);
+    }
+    __syncthreads();
+    return C.sm.ival[slot];
+}
+
 template <class BaseF, class UnewF>
 __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, unsigned epoch)
 {
     const PanelArgs &a = C.a;
     PanelSmem &sm = C.sm;
-    double *Dsm = C.dyn;             // TB x TB (Dinv, or D for the sequential path)
+    double *Dsm = C.dyn;             // TB x TB: M_b (safe) or D (unsafe)
     double *accg = C.dyn + TB * TB;  // 4 x TB
     const int64_t n = C.n, p0 = C.p0, M = C.M;
     const int Nb = (int)((M + TB - 1) / TB);
@@ -225,18 +240,9 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         const int64_t r0 = p0 + (int64_t)b * TB;
         const int h = (int)(n - r0 < TB ? n - r0 : TB);
         const bool safe = a.dsafe[b] != 0;
-        // stage Dinv (safe) or D (unsafe) of this block in shared memory
-        if (safe) {
-            const double *src = a.Dinv + (size_t)b * TB * TB;
-            for (int idx = C.tid; idx < TB * TB; idx += PNT) Dsm[idx] = src[idx];
-        } else {
-            for (int idx = C.tid; idx < TB * TB; idx += PNT) {
-                int i = idx & (TB - 1), j = idx >> 7;
-                Dsm[idx] = (i < h && j < h && i <= j) ? a.B[(size_t)(r0 + j) * a.ldb + r0 + i] : 0.0;
-            }
-        }
-        // rhs part that does not depend on the solution (off the critical path):
-        // rb(i) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k), all 512 threads
+        const bool last = (b == Nb - 1);
+        const int hn = last ? 0 : (int)(n - (r0 + TB) < TB ? n - (r0 + TB) : TB);  // rows of block b+1
+        // (1) rhs part that does not depend on the solution, all 512 threads
         {
             const int64_t r = r0 + ri;
             double u = 0.0;
@@ -257,27 +263,26 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             }
             __syncthreads();
         }
-        // warm L2 with the critical-path tile (b, b+1)
-        if (b + 1 < Nb) {
-            const int64_t c0 = p0 + (int64_t)(b + 1) * TB;
-            for (int idx = C.tid; idx < TB * 2; idx += PNT) {
-                int col = idx >> 1, half = idx & 1;
-                if (c0 + col < n) prefetch_l2(a.B + (size_t)(c0 + col) * a.ldb + r0 + half * 64);
+        // (2) stage M_b (safe) or D (unsafe) in shared memory
+        if (safe) {
+            if (!last) {
+                const double *src = a.Mb + (size_t)b * TB * TB;
+                for (int idx = C.tid; idx < TB * TB; idx += PNT) Dsm[idx] = src[idx];
+            }
+        } else {
+            for (int idx = C.tid; idx < TB * TB; idx += PNT) {
+                int i = idx & (TB - 1), j = idx >> 7;
+                Dsm[idx] = (i < h && j < h && i <= j) ? a.B[(size_t)(r0 + j) * a.ldb + r0 + i] : 0.0;
             }
         }
+        // (3) off-diagonal tiles c > b+1 (safe) or c > b (unsafe), as their solutions arrive
         double acc = 0.0;
         int Eacc = 0;
-        for (int cb = Nb - 1; cb > b; --cb) {
+        const int cstop = safe ? b + 1 : b;
+        for (int cb = Nb - 1; cb > cstop; --cb) {
             const int64_t c0 = p0 + (int64_t)cb * TB;
             const int w = (int)(n - c0 < TB ? n - c0 : TB);
-            if (C.tid == 0) {
-                while (ld_acquire(&a.flags[cb]) != epoch) {
-                }
-                __threadfence();
-                sm.ival[cb & 1] = __ldcg(&a.bexp[cb]);
-            }
-            __syncthreads();
-            const int ecb = sm.ival[cb & 1];
+            const int ecb = wait_block(C, cb, epoch, cb & 1);
             if (ecb > Eacc) {
                 acc = ldexp(acc, Eacc - ecb);
                 Eacc = ecb;
@@ -309,15 +314,37 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         __syncthreads();
         int e = Eacc;
         if (safe) {
-            // x = Dinv * rhs   (Dinv column-major TB x TB)
-            double s = 0.0;
+            // (4) c_b = Dinv_b * t   (Dinv from global; off the critical path)
+            {
+                const double *Di = a.Dinv + (size_t)b * TB * TB;
+                double s = 0.0;
 #pragma unroll 8
-            for (int l = grp; l < TB; l += 4) s += Dsm[l * TB + ri] * sm.rhs[l];
-            accg[grp * TB + ri] = s;
-            __syncthreads();
+                for (int l = grp; l < TB; l += 4) s += Di[l * TB + ri] * sm.rhs[l];
+                accg[grp * TB + ri] = s;
+                __syncthreads();
+                if (C.tid < TB)
+                    sm.cbv[C.tid] = (accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]);
+                __syncthreads();
+            }
+            // (5) critical path: y~_b = c_b 2^(Eacc-E) - M_b y~_{b+1} 2^(e1-E)
             double xv = 0.0;
-            if (C.tid < TB) xv = accg[C.tid] + accg[TB + C.tid] + accg[2 * TB + C.tid] + accg[3 * TB + C.tid];
-            // post-hoc power-of-two rescale if the block solution is too large
+            if (!last) {
+                const int e1 = wait_block(C, b + 1, epoch, 2);
+                const int E = e1 > Eacc ? e1 : Eacc;
+                const double *yp = a.vy + r0 + TB;
+                double s = 0.0;
+#pragma unroll 8
+                for (int l = grp; l < TB; l += 4) s += (l < hn ? Dsm[l * TB + ri] * __ldcg(yp + l) : 0.0);
+                accg[grp * TB + ri] = s;
+                __syncthreads();
+                if (C.tid < TB)
+                    xv = ldexp(sm.cbv[C.tid], Eacc - E) -
+                         ldexp((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]), e1 - E);
+                e = E;
+            } else if (C.tid < TB) {
+                xv = sm.cbv[C.tid];
+            }
+            // (6) post-hoc power-of-two rescale if the block solution is too large
             double mx = (C.tid < h) ? fabs(xv) : 0.0;
             mx = warp_max(mx);
             if (C.tid < TB && C.lane == 0) sm.red[C.warp] = mx;
@@ -364,20 +391,19 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (l + 32 * q < h) a.vy[r0 + l + 32 * q] = v[q];
-                if (l == 0) sm.ival[2] = e;
+                if (l == 0) sm.ival[3] = e;
             }
             __syncthreads();
-            e = sm.ival[2];
+            e = sm.ival[3];
         }
-        __threadfence();
+        // publish: block-wide barrier orders the vy stores before thread 0's release
         __syncthreads();
         if (C.tid == 0) {
             a.bexp[b] = e;
-            __threadfence();
-            st_release(&a.flags[b], epoch);
+            st_release64(&a.flags[b], ((unsigned long long)epoch << 32) | (unsigned)e);
         }
-        __syncthreads();
     }
+    __syncthreads();
 }
 
 // After a completed solve (grid synced): Emax over all blocks.
@@ -805,7 +831,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
 }
 
 // Inverse of each TB x TB diagonal block of B(p0:n, p0:n) (column-major, ld TB) and a
-// safety flag: finite, max|inv| <= 2^200, and max|inv| * max|D| <= 1e12 (else the
+// safety flag: finite, max|inv| <= 2^200, and max|inv| * max|D| <= 4e3 (well-conditioned, so the
+// look-ahead block solve stays backward stable to ~4e3 u) (else the
 // panel uses the overflow-safe sequential substitution for that block).
 __global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
                                                       double *Dinv, int *dsafe)
@@ -851,7 +878,7 @@ __global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t l
             im = fmax(im, smax[0][w]);
             dm = fmax(dm, smax[1][w]);
         }
-        dsafe[b] = (isfinite(im) && im <= 0x1p200 && im * dm <= 1e12) ? 1 : 0;
+        dsafe[b] = (isfinite(im) && im <= 0x1p200 && im * dm <= 4e3) ? 1 : 0;
     }
 }
 
@@ -879,6 +906,19 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb = (int)((M + TB - 1) / TB);
     inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
     HT_CUDA_TRY(cudaGetLastError());
+    // M_b = Dinv_b * B(block b, block b+1) for the look-ahead solve
+    if (Nb > 1) {
+        GemmBatchItem it[1024];
+        int cnt = 0;
+        for (int b = 0; b + 1 < Nb && cnt < 1024; ++b) {
+            const int64_t r0 = a->s0 + 1 + (int64_t)b * TB, c0 = r0 + TB;
+            const int w = (int)(a->n - c0 < TB ? a->n - c0 : TB);
+            it[cnt++] = GemmBatchItem{a->Dinv + (size_t)b * TB * TB, a->B + r0 + c0 * a->ldb, a->Mb + (size_t)b * TB * TB,
+                                      TB, a->ldb, TB, TB, w, TB, 1.0, 0.0, 0.0};
+        }
+        int rc = ht_gemm_multi(st, 'N', 'N', it, cnt);
+        if (rc) return rc;
+    }
     void *args[] = {(void *)a};
     HT_CUDA_TRY(cudaLaunchCooperativeKernel((void *)panel_kernel, dim3(nblocks), dim3(PNT), args,
                                             DYN_DOUBLES * sizeof(double), st));
