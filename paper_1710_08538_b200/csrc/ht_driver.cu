@@ -55,7 +55,8 @@ struct Work {
     int *dsafe = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
-    int64_t ndesc = 0, fd_cur = 0, ld_cur = 0;
+    ChainWin *d_cw = nullptr, *h_cw = nullptr;
+    int64_t ndesc = 0, fd_cur = 0, ld_cur = 0, cw_cur = 0;
 };
 
 std::mutex g_mu;
@@ -135,6 +136,9 @@ void work_free(Work &w)
     if (w.h_iflags) cudaFreeHost(w.h_iflags);
     if (w.h_fd) cudaFreeHost(w.h_fd);
     if (w.h_ld) cudaFreeHost(w.h_ld);
+    if (w.d_cw) cudaFree(w.d_cw);
+    if (w.h_cw) cudaFreeHost(w.h_cw);
+    w.d_cw = nullptr; w.h_cw = nullptr;
     w.flags = nullptr; w.bexp = nullptr; w.d_out = nullptr; w.d_iflags = nullptr; w.d_force = nullptr;
     w.d_fd = nullptr; w.d_ld = nullptr; w.h_out = nullptr; w.h_scal = nullptr; w.h_iflags = nullptr;
     w.h_fd = nullptr; w.h_ld = nullptr;
@@ -184,10 +188,9 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.Gm, nnb + 2 * nb2));
     TRY(dalloc(&w.Tm, nnb + 2 * nb2));
     TRY(dalloc(&w.Qw, 4 * nnb + 8 * nb2));
-    TRY(dalloc(&w.tmp, 3 * (size_t)N * 2 * NB));
     TRY(dalloc(&w.W1, nnb + 4 * nb2)); TRY(dalloc(&w.W2, nnb + 4 * nb2));
     TRY(dalloc(&w.UR, 2 * nb2));
-    TRY(dalloc(&w.fscr, 4 * nb2 + 64));
+    TRY(dalloc(&w.fscr, 4 * nb2 + 16384 + 64));
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
@@ -198,6 +201,8 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.d_cw, w.ndesc * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_cw, w.ndesc * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
     w.ncap = N;
     w.nbcap = NB;
     *out = &w;
@@ -298,31 +303,20 @@ struct Run {
         if (nd == 0) return 0;
         if (w->fd_cur + nd > w->ndesc || w->ld_cur + nd > w->ndesc) return HT_ENUMERIC;
         FactorDesc *hf = w->h_fd + w->fd_cur;
-        LarftDesc *hl = w->h_ld + w->ld_cur;
-        int maxpq = 0;
+        int maxp = 0;
         for (int i = 0; i < nd; ++i) {
-            hf[i] = fds[i];
-            maxpq = std::max(maxpq, fds[i].p * fds[i].q);
             const Win &x = wins[i0 + i];
-            hl[i] = LarftDesc{w->Gm + x.og, x.q, w->tau + x.ot, w->Tm + x.og, x.q, x.q};
+            hf[i] = fds[i];
+            hf[i].T = w->Tm + x.og;  // q x q compact-WY T, formed inside the factor kernel
+            hf[i].ldt = x.q;
+            maxp = std::max(maxp, fds[i].p);
             extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, st));
-        HT_CUDA_TRY(cudaMemcpyAsync(w->d_ld + w->ld_cur, hl, nd * sizeof(LarftDesc), cudaMemcpyHostToDevice, st));
         tm.begin(st, 2);
-        TRY(ht_factor_run(st, w->d_fd + w->fd_cur, nd, w->fscr, maxpq));
+        TRY(ht_factor_run(st, w->d_fd + w->fd_cur, nd, w->fscr, maxp));
         tm.end(st);
-        // G = V^T V
         std::vector<GemmBatchItem> it(nd);
-        for (int i = 0; i < nd; ++i) {
-            const Win &x = wins[i0 + i];
-            it[i] = GemmBatchItem{w->Vhat + x.ov, w->Vhat + x.ov, w->Gm + x.og, x.p, x.p, x.q,
-                                  x.q, x.q, x.p, 1.0, 0.0, 0.0};
-        }
-        TRY(gemm_multi('T', 'N', it));
-        tm.begin(st, 2);
-        TRY(ht_larft_run(st, w->d_ld + w->ld_cur, nd));
-        tm.end(st);
         // Wt = V T
         for (int i = 0; i < nd; ++i) {
             const Win &x = wins[i0 + i];
@@ -342,45 +336,29 @@ struct Run {
         return 0;
     }
 
-    struct Tgt {
-        double *X;
-        int64_t ldx, r0, rows, c0, cols;  // right: rows r0..r0+rows, cols c0..c0+p ; left: rows r0..r0+p, cols c0..
-    };
-    // X(r0:, c0:c0+p) <- X(...) Qw  for each target
-    int apply_right(const std::vector<Tgt> &tg, const double *Qwp, int p)
+    // Chained window applies (ht_chain.cu): every matrix in `mats` takes the windows of
+    // `wl` in order; lo/hi of a window are indexed by the matrix position in `mats`.
+    int chain(const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl)
     {
-        std::vector<GemmBatchItem> it;
-        for (size_t i = 0; i < tg.size(); ++i) {
-            if (tg[i].rows <= 0) continue;
-            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            it.push_back(GemmBatchItem{tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, Qwp, tmp, tg[i].ldx, p, tg[i].rows,
-                                       (int)tg[i].rows, p, p, 1.0, 0.0, 0.0});
+        if (wl.empty() || mats.empty()) return 0;
+        const int nw = (int)wl.size();
+        if (w->cw_cur + nw > w->ndesc) return HT_ENUMERIC;
+        ChainWin *hc = w->h_cw + w->cw_cur;
+        int pmax = 0;
+        for (int i = 0; i < nw; ++i) {
+            hc[i] = wl[i];
+            pmax = std::max(pmax, wl[i].p);
+            for (size_t m = 0; m < mats.size(); ++m) {
+                const int64_t a = std::max(wl[i].lo[m], mats[m].s_begin), b = std::min(wl[i].hi[m], mats[m].s_end);
+                if (b > a) g_ht_flops += 2.0 * (double)(b - a) * wl[i].p * (double)wl[i].p;
+            }
         }
-        TRY(gemm_multi('N', 'N', it));
-        for (size_t i = 0; i < tg.size(); ++i) {
-            if (tg[i].rows <= 0) continue;
-            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            TRY(copy2d(tg[i].rows, p, tmp, tg[i].rows, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
-        }
-        return 0;
-    }
-    // X(r0:r0+p, c0:c0+cols) <- Qw^T X(...)
-    int apply_left(const std::vector<Tgt> &tg, const double *Qwp, int p)
-    {
-        std::vector<GemmBatchItem> it;
-        for (size_t i = 0; i < tg.size(); ++i) {
-            if (tg[i].cols <= 0) continue;
-            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            it.push_back(GemmBatchItem{Qwp, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tmp, p, tg[i].ldx, p, p,
-                                       (int)tg[i].cols, p, 1.0, 0.0, 0.0});
-        }
-        TRY(gemm_multi('T', 'N', it));
-        for (size_t i = 0; i < tg.size(); ++i) {
-            if (tg[i].cols <= 0) continue;
-            double *tmp = w->tmp + i * (size_t)n * 2 * nb;
-            TRY(copy2d(p, tg[i].cols, tmp, p, tg[i].X + tg[i].r0 + tg[i].c0 * tg[i].ldx, tg[i].ldx));
-        }
-        return 0;
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, st));
+        tm.begin(st, 1);
+        int rc = ht_chain_apply(st, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax);
+        tm.end(st);
+        w->cw_cur += nw;
+        return rc;
     }
 
     // ---------------- absorption (sec. 3.3) ---------------------------------
@@ -388,7 +366,7 @@ struct Run {
     {
         const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
         double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
-        w->fd_cur = w->ld_cur = 0;
+        w->fd_cur = w->ld_cur = w->cw_cur = 0;
         // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns
         TRY(gemm('N', 'N', p0, k, n - p0, 1.0, A + p0 * lda, lda, V + p0, n, 0.0, w->W1, n));
         TRY(gemm('N', 'N', p0, k, k, 1.0, w->W1, n, T, nb, 0.0, Y, n));
@@ -419,14 +397,15 @@ struct Run {
         }
         TRY(factor_and_form(fds, 0));
         // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e) =====
-        for (int i = 0; i < r; ++i) {
-            const Win &x = wins[i];
-            const int64_t c0 = J + 1 + rb[i];
-            std::vector<Tgt> tg;
-            tg.push_back(Tgt{B, ldb, 0, J + 1 + rb[i + 2], c0, 0});
-            tg.push_back(Tgt{A, lda, 0, n, c0, 0});
-            if (wz) tg.push_back(Tgt{Z, ldz, 0, n, c0, 0});
-            TRY(apply_right(tg, w->Qw + x.oq, x.p));
+        {
+            std::vector<ChainWin> wl;
+            for (int i = 0; i < r; ++i) {
+                const Win &x = wins[i];
+                wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
+            }
+            std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, n}, ChainMat{A, lda, 0, 0, n}};
+            if (wz) mats.push_back(ChainMat{Z, ldz, 0, 0, n});
+            TRY(chain(mats, wl));
         }
         const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
         {
@@ -465,11 +444,9 @@ struct Run {
             std::vector<FactorDesc> f1{FactorDesc{B + (R0 + h - 1) + (C0 + wdt - 1) * ldb, -ldb, -1, (int)wdt, (int)h,
                                                   1, w->Vhat + x.ov, wdt, w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
-            std::vector<Tgt> tg;
-            tg.push_back(Tgt{B, ldb, 0, R0, C0, 0});
-            tg.push_back(Tgt{A, lda, 0, n, C0, 0});
-            if (wz) tg.push_back(Tgt{Z, ldz, 0, n, C0, 0});
-            TRY(apply_right(tg, w->Qw + x.oq, (int)wdt));
+            std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, R0}, ChainMat{A, lda, 0, 0, n}};
+            if (wz) mats.push_back(ChainMat{Z, ldz, 0, 0, n});
+            TRY(chain(mats, {ChainWin{w->Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}}}));
         }
         // ===== L1: QR staircase of U2, bottom -> top (sec. 3.3.2b) =====
         wins_reset();
@@ -486,17 +463,16 @@ struct Run {
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
         TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
         TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));
-        for (int i = 0; i < r; ++i) {
-            const Win &x = wins[i];
-            const int64_t R0 = J + 1 + lb[r - 1 - i];
-            std::vector<Tgt> tg;
-            tg.push_back(Tgt{B, ldb, R0, 0, R0, n - R0});
-            tg.push_back(Tgt{A, lda, R0, 0, J, n - J});
-            TRY(apply_left(tg, w->Qw + x.oq, x.p));
-            if (wq) {
-                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
-                TRY(apply_right(tq, w->Qw + x.oq, x.p));
+        {
+            std::vector<ChainWin> wl;
+            for (int i = 0; i < r; ++i) {
+                const Win &x = wins[i];
+                const int64_t R0 = J + 1 + lb[r - 1 - i];
+                wl.push_back(ChainWin{w->Qw + x.oq, R0, x.p, {R0, J, 0}, {n, n, n}});
             }
+            std::vector<ChainMat> mats{ChainMat{B, ldb, 1, J + 1, n}, ChainMat{A, lda, 1, J, n}};
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            TRY(chain(mats, wl));
         }
         // UR = [U1; R~1]  (2k x k)
         const int64_t ldur = 2 * k;
@@ -531,14 +507,9 @@ struct Run {
             std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)p, (int)q, 0, w->Vhat + x.ov, p,
                                                   w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
-            std::vector<Tgt> tg;
-            tg.push_back(Tgt{B, ldb, R0, 0, R0 + q, n - (R0 + q)});
-            tg.push_back(Tgt{A, lda, R0, 0, J, n - J});
-            TRY(apply_left(tg, w->Qw + x.oq, (int)p));
-            if (wq) {
-                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
-                TRY(apply_right(tq, w->Qw + x.oq, (int)p));
-            }
+            std::vector<ChainMat> mats{ChainMat{B, ldb, 1, R0 + q, n}, ChainMat{A, lda, 1, J, n}};
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            TRY(chain(mats, {ChainWin{w->Qw + x.oq, R0, (int)p, {R0 + q, J, 0}, {n, n, n}}}));
         }
         return 0;
     }
@@ -564,12 +535,9 @@ struct Run {
             std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)m, (int)m, 0, w->Vhat + x.ov, m,
                                                   w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
-            std::vector<Tgt> tg{Tgt{A, lda, R0, 0, J, n - J}};
-            TRY(apply_left(tg, w->Qw + x.oq, (int)m));
-            if (wq) {
-                std::vector<Tgt> tq{Tgt{Q, ldq, 0, n, R0, 0}};
-                TRY(apply_right(tq, w->Qw + x.oq, (int)m));
-            }
+            std::vector<ChainMat> mats{ChainMat{A, lda, 1, J, n}};
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            TRY(chain(mats, {ChainWin{w->Qw + x.oq, R0, (int)m, {J, 0, 0}, {n, n, n}}}));
         }
         return 0;
     }

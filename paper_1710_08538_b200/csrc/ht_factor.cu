@@ -10,134 +10,586 @@
 // whose rows/columns are reversed (and, for RQ, transposed); the reflector
 // vectors are written back in the natural order, so every window transform is
 //   Qw = I - Vnat T Vnat^T   (compact WY, eq. compactWY)
-// which is then formed explicitly (2k x 2k) and applied with the DMMA GEMM.
+// with T formed here as well; the driver forms Qw explicitly and applies it.
+//
+// B200 design: one CTA of 512 threads per
+// chain; the window is factored in 32-column panels (left-looking, DMMA), each
+// panel in four 8-column leaves held in registers (lane = (column, row group)),
+// so that one Householder column step is ~100 instructions per warp and ONE
+// block barrier; a finished leaf updates the rest of its panel as a blocked (WY)
+// update.
 #include "ht_common.cuh"
 #include "ht_internal.h"
 
 namespace {
 
-constexpr int FNT = 512;  // threads of the factor CTA
+constexpr int FNT = 512;  // threads of the factor CTA (16 warps)
+constexpr int FNW = FNT / 32;
+constexpr int PBW = 32;   // panel width (left-looking granularity)
+constexpr int LW = 8;     // leaf width (columns factored one by one)
+constexpr int NLF = PBW / LW;
+constexpr int VRC = 256;  // rows per staged chunk of a previous panel's V
+constexpr int LDX = 40;   // ld of the 32x32 X buffer (== 8 mod 32: conflict-free B fragments)
+constexpr int LDT = 33;
 
-__global__ void __launch_bounds__(FNT) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch,
-                                                         int smem_doubles)
+// Optional phase profile (micro-benchmarks only): when non-null, thread 0 accumulates
+// globaltimer nanoseconds per phase into g_fprof[phase].
+__device__ unsigned long long *g_fprof = nullptr;
+__device__ __forceinline__ unsigned long long fclock()
 {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FPROF(ph)                                                          \
+    do {                                                                   \
+        if (fprof && threadIdx.x == 0) {                                   \
+            const unsigned long long _t = fclock();                        \
+            fprof[ph] += _t - fprof_t;                                     \
+            fprof_t = _t;                                                  \
+        }                                                                  \
+    } while (0)
+
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// 1/sqrt(x) and 1/x by a single-precision seed + Newton steps (each step doubles the
+// correct bits: 23 -> 46 -> 92), ~1 ulp; exact library path outside the float range.
+__device__ __forceinline__ double fast_rsqrt(double x)
+{
+    if (!(x > 1e-36 && x < 1e36)) return 1.0 / sqrt(x);
+    double y = (double)rsqrtf((float)x);
+    y = y * fma(-0.5 * x * y, y, 1.5);
+    y = y * fma(-0.5 * x * y, y, 1.5);
+    return y;
+}
+__device__ __forceinline__ double fast_rcp(double x)
+{
+    if (!(fabs(x) > 1e-36 && fabs(x) < 1e36)) return 1.0 / x;
+    double y = (double)(1.0f / (float)x);
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return y;
+}
+// Householder scalars of x = [alpha; tail], ||tail||^2 = ss > 0 (dlarfg convention, R-Z1):
+// beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||,
+// scal = 1 / (alpha - beta) (so that v = [1; tail * scal]).
+__device__ __forceinline__ void house_scalars(double alpha, double ss, double &beta, double &tau, double &scal)
+{
+    const double N = fma(alpha, alpha, ss);
+    const double r = fast_rsqrt(N);
+    const double nrm = N * r;
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = fma(fabs(alpha), r, 1.0);
+    const double den = fast_rcp(fabs(alpha) + nrm);
+    scal = alpha >= 0.0 ? den : -den;
+}
+
+// RPT: rows per thread per leaf; a warp holds 4 row groups x 8 leaf columns, so the
+// CTA covers MAXP = 16 warps * 4 * RPT rows.
+template <int RPT>
+struct FactorSmem {
+    static constexpr int MAXP = FNW * 4 * RPT;
+    static constexpr int LDP = MAXP + 4;                       // == 4 mod 32
+    static constexpr int RC = MAXP < VRC ? MAXP : VRC;
+    static constexpr int LDV = RC + 4;                         // == 4 mod 32
+    static constexpr int VSZ = (PBW * LDV > FNW * LW * PBW) ? PBW * LDV : FNW * LW * PBW;
+    static constexpr int DOUBLES = PBW * LDP + VSZ + PBW * LDX + PBW * LDT + 2 * FNW * LW + 2 * LW + PBW + 2 * 64;
+};
+
+// Vs[c][rr] = V(r0 + rr, col0 + c) (view row order), rr < RC, zero beyond `rows`.
+// All loads of a thread are issued before any store (memory-level parallelism).
+template <int RPT>
+__device__ __forceinline__ void stage_v(const FactorDesc &d, int col0, int r0, int rows, double *Vs)
+{
+    using L = FactorSmem<RPT>;
+    constexpr int PER = (PBW * L::RC + FNT - 1) / FNT;
+    const int tid = threadIdx.x, p = d.p;
+    double t[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+        const int idx = tid + e * FNT;
+        const int c = idx / L::RC, rr = idx % L::RC, r = r0 + rr;
+        t[e] = (c < PBW && rr < rows) ? d.V[(int64_t)(col0 + c) * d.ldv + (d.rev ? p - 1 - r : r)] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+        const int idx = tid + e * FNT;
+        const int c = idx / L::RC, rr = idx % L::RC;
+        if (c < PBW) Vs[c * L::LDV + rr] = t[e];
+    }
+}
+
+// X(32 x 32) = V_i(r_beg:p, :)^T * Ps(r_beg:p, :) by DMMA (K = rows), V_i = columns
+// 32i..32i+31 of the window's V (view row order).  Warp w computes the 8x8 tile
+// (w/4, w%4) and returns it in (o0, o1) = X(8tm+g, 8tn+2t4 + {0,1}).
+template <int RPT>
+__device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r_beg, const double *Ps, double *Vs,
+                                               double &o0, double &o1)
+{
+    using L = FactorSmem<RPT>;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+    const int p = d.p;
+    const int tm = warp >> 2, tn = warp & 3;
+    double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+    for (int r0 = r_beg; r0 < p; r0 += L::RC) {
+        const int rows = min(L::RC, p - r0);
+        __syncthreads();
+        stage_v<RPT>(d, i * PBW, r0, rows, Vs);
+        __syncthreads();
+        const double *va = Vs + (8 * tm + g) * L::LDV + t4;
+        const double *pb = Ps + (8 * tn + g) * L::LDP + r0 + t4;
+        int kk = 0;
+        for (; kk + 8 <= rows; kk += 8) {
+            dmma884(x0, x1, va[kk], pb[kk]);
+            dmma884(y0, y1, va[kk + 4], pb[kk + 4]);
+        }
+        for (; kk < rows; kk += 4) dmma884(x0, x1, va[kk], pb[kk]);  // padded rows are 0
+    }
+    o0 = x0 + y0;
+    o1 = x1 + y1;
+}
+
+// Blocked, left-looking Householder QR of one p x q window view (p <= MAXP), PAPER.md
+// sec. 2.1 reflectors (dlarfg convention, reading R-Z1) accumulated in compact WY form
+// (eq. compactWY):
+//   for each 32-column panel b:  P <- Q_{b-1}^T ... Q_0^T P     (Q_i = I - V_i T_i V_i^T, DMMA)
+//     for each 8-column leaf:    column steps (one block reduction per column gives the
+//                                tail norm and the leaf's dot products), then the leaf's
+//                                8 reflectors update the rest of the panel (WY, T_leaf)
+//   T_b from G = V_b^T V_b (DMMA) by the dlarft recurrence;
+//   T(0:c0, panel b) = -T(0:c0, 0:c0) (V(:, 0:c0)^T V_b) T_b.
+// Outputs: R (upper trapezoid, exact zeros below) back through the view, V in natural
+// row order, tau, and the q x q T of Q = H_0 ... H_{q-1} = I - V T V^T.
+// gscratch: >= 64 * q doubles.
+template <int RPT>
+__global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch)
+{
+    using L = FactorSmem<RPT>;
     extern __shared__ __align__(16) double fsm[];
-    __shared__ double red[32];
-    __shared__ double sc[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = FNT / 32;
+    double *Ps = fsm;                         // [PBW][LDP]   panel, column-major
+    double *Vs = Ps + PBW * L::LDP;           // [PBW][LDV]   staged V_i chunk / leaf partials
+    double *Xs = Vs + L::VSZ;                 // [PBW][LDX]   X = T^T V^T P (row-major) / G_b
+    double *Ts = Xs + PBW * LDX;              // [PBW][LDT]   T_i (left-looking) / leaf W
+    double *part = Ts + PBW * LDT;            // [2][FNW][LW]
+    double *rowc = part + 2 * FNW * LW;       // [2][LW]
+    double *taus = rowc + 2 * LW;             // [PBW]
+    double *Zl = taus + PBW;                  // [LW][LW] leaf Z
+    double *Tl = Zl + 64;                     // [LW][LW] leaf T
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int c8 = lane & 7, rq = lane >> 3;    // leaf column / row group of this lane
+    const int rw0 = warp * 4 * RPT + rq * RPT;  // first of this thread's RPT rows
+    unsigned long long *fprof = g_fprof;
+    unsigned long long fprof_t = fprof ? fclock() : 0ull;
+
     for (int di = 0; di < nd; ++di) {
         const FactorDesc d = descs[di];
         const int p = d.p, q = d.q;
-        double *Wk = (p * q <= smem_doubles) ? fsm : gscratch;
-        // load the view
-        for (int idx = tid; idx < p * q; idx += FNT) {
-            int i = idx % p, j = idx / p;
-            Wk[idx] = d.W[(int64_t)i * d.rs + (int64_t)j * d.cs];
-        }
-        __syncthreads();
-        for (int c = 0; c < q; ++c) {
-            // Householder reflector of Wk(c:p, c) (dlarfg convention, reading R1)
-            double ss = 0.0;
-            for (int i = c + 1 + tid; i < p; i += FNT) {
-                double v = Wk[c * p + i];
-                ss += v * v;
-            }
-            ss = block_sum(ss, red);
-            if (tid == 0) {
-                double alpha = (c < p) ? Wk[c * p + c] : 0.0;
-                double tau = 0.0, scal = 0.0, beta = alpha;
-                if (ss > 0.0) {
-                    double nrm = sqrt(alpha * alpha + ss);
-                    beta = (alpha >= 0.0) ? -nrm : nrm;
-                    tau = (beta - alpha) / beta;
-                    scal = 1.0 / (alpha - beta);
+        const int64_t rs = d.rs, cs = d.cs;
+        auto nat = [&](int r) -> int64_t { return d.rev ? (int64_t)(p - 1 - r) : (int64_t)r; };
+        auto Tout = [&](int a, int c) -> double & { return d.T[(int64_t)c * d.ldt + a]; };
+        const int nblk = (q + PBW - 1) / PBW;
+        for (int b = 0; b < nblk; ++b) {
+            const int c0 = b * PBW, nc = min(PBW, q - c0);
+            // ---- load panel columns c0 .. c0+nc of the view (zero padding) ----
+            {
+                constexpr int PER = (PBW * L::LDP + FNT - 1) / FNT;
+                const bool rowfast = (rs == 1 || rs == -1);  // contiguous along the view's rows
+                double t[PER];
+#pragma unroll
+                for (int e = 0; e < PER; ++e) {
+                    const int idx = tid + e * FNT;
+                    const int j = rowfast ? idx / L::LDP : idx % PBW, r = rowfast ? idx % L::LDP : idx / PBW;
+                    t[e] = (j < nc && r < p) ? d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] : 0.0;
                 }
-                sc[0] = tau;
-                sc[1] = scal;
-                sc[2] = beta;
-                d.tau[c] = tau;
+#pragma unroll
+                for (int e = 0; e < PER; ++e) {
+                    const int idx = tid + e * FNT;
+                    const int j = rowfast ? idx / L::LDP : idx % PBW, r = rowfast ? idx % L::LDP : idx / PBW;
+                    if (j < PBW && r < L::LDP) Ps[j * L::LDP + r] = t[e];
+                }
             }
-            __syncthreads();
-            const double tau = sc[0], scal = sc[1];
-            if (tau != 0.0) {
-                for (int i = c + 1 + tid; i < p; i += FNT) Wk[c * p + i] *= scal;
+            FPROF(0);
+            // ---- left-looking: P <- (I - V_i T_i^T V_i^T) P for i < b ----
+            for (int i = 0; i < b; ++i) {
+                const int r_lo = i * PBW;  // V_i is zero above row r_lo
                 __syncthreads();
-                // apply (I - tau v v^T) to columns j > c
-                for (int j = c + 1 + warp; j < q; j += nw) {
-                    double w = 0.0;
-                    for (int i = c + lane; i < p; i += 32) {
-                        double vi = (i == c) ? 1.0 : Wk[c * p + i];
-                        w += vi * Wk[j * p + i];
+                for (int idx = tid; idx < PBW * PBW; idx += FNT) {
+                    const int a = idx / PBW, c = idx % PBW;
+                    Ts[a * LDT + c] = Tout(r_lo + a, r_lo + c);  // diagonal block T_i
+                }
+                double o0, o1;
+                vt_times_panel<RPT>(d, i, r_lo, Ps, Vs, o0, o1);
+                {
+                    const int tm = warp >> 2, tn = warp & 3;
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = o0;
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = o1;
+                }
+                __syncthreads();
+                // X <- T_i^T X  (T_i upper triangular): X'(a, c) = sum_{l <= a} T(l, a) X(l, c)
+                double xv[2];
+                for (int e = 0; e < 2; ++e) {
+                    const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
+                    double s = 0.0;
+                    for (int l = 0; l <= a; ++l) s += Ts[l * LDT + a] * Xs[l * LDX + c];
+                    xv[e] = s;
+                }
+                __syncthreads();
+                for (int e = 0; e < 2; ++e) {
+                    const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
+                    Xs[a * LDX + c] = -xv[e];
+                }
+                __syncthreads();
+                // P -= V_i X : per chunk, warp w owns row tiles {2w, 2w+1} x 4 column tiles
+                for (int r0 = r_lo; r0 < p; r0 += L::RC) {
+                    const int rows = min(L::RC, p - r0);
+                    if (p - r_lo > L::RC) {  // multi-chunk: Vs holds the last chunk -> re-stage
+                        __syncthreads();
+                        stage_v<RPT>(d, r_lo, r0, rows, Vs);
+                        __syncthreads();
                     }
-                    w = warp_sum(w) * tau;
-                    for (int i = c + lane; i < p; i += 32) {
-                        double vi = (i == c) ? 1.0 : Wk[c * p + i];
-                        Wk[j * p + i] -= w * vi;
+                    for (int tr = 2 * warp; tr < 2 * warp + 2; ++tr) {
+                        if (8 * tr >= rows) break;
+                        double acc[4][2];
+#pragma unroll
+                        for (int tn2 = 0; tn2 < 4; ++tn2) {
+                            acc[tn2][0] = Ps[(8 * tn2 + 2 * t4) * L::LDP + r0 + 8 * tr + g];
+                            acc[tn2][1] = Ps[(8 * tn2 + 2 * t4 + 1) * L::LDP + r0 + 8 * tr + g];
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < PBW; kk += 4) {
+                            const double av = Vs[(kk + t4) * L::LDV + 8 * tr + g];
+#pragma unroll
+                            for (int tn2 = 0; tn2 < 4; ++tn2)
+                                dmma884(acc[tn2][0], acc[tn2][1], av, Xs[(kk + t4) * LDX + 8 * tn2 + g]);
+                        }
+#pragma unroll
+                        for (int tn2 = 0; tn2 < 4; ++tn2) {
+                            Ps[(8 * tn2 + 2 * t4) * L::LDP + r0 + 8 * tr + g] = acc[tn2][0];
+                            Ps[(8 * tn2 + 2 * t4 + 1) * L::LDP + r0 + 8 * tr + g] = acc[tn2][1];
+                        }
                     }
                 }
             }
             __syncthreads();
-            if (tid == 0 && c < p) Wk[c * p + c] = sc[2];
+            FPROF(1);
+            // ---- the panel in registers: val[l][e] = P(rw0 + e, 8l + c8) ----
+            double val[NLF][RPT];
+#pragma unroll
+            for (int l = 0; l < NLF; ++l)
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) val[l][e] = Ps[(LW * l + c8) * L::LDP + rw0 + e];
+            int buf = 0;
+#pragma unroll
+            for (int lf = 0; lf < NLF; ++lf) {
+                const int jbeg = LW * lf;
+                if (jbeg >= nc) break;
+                const int jend = min(nc, jbeg + LW);
+                // -------- column steps inside the leaf --------
+                for (int jj = jbeg; jj < jend; ++jj) {
+                    const int jc = jj - jbeg;
+                    const int dr = c0 + jj;                             // diagonal row of this column
+                    const bool active = warp * 4 * RPT + 4 * RPT > dr;  // warp-uniform: rows >= dr here
+                    const int src = (rq << 3) | jc;
+                    double xr[RPT];
+                    double s = 0.0;
+                    if (active) {
+                        double sa[2] = {0.0, 0.0};
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e) {
+                            xr[e] = __shfl_sync(0xffffffffu, val[lf][e], src);
+                            const double vm = (rw0 + e > dr) ? val[lf][e] : 0.0;
+                            sa[e & 1] = fma(vm, xr[e], sa[e & 1]);
+                        }
+                        s = sa[0] + sa[1];
+                        s += __shfl_xor_sync(0xffffffffu, s, 8);
+                        s += __shfl_xor_sync(0xffffffffu, s, 16);
+                    }
+                    if (rq == 0) part[(buf * FNW + warp) * LW + c8] = s;
+                    if (dr >= rw0 && dr < rw0 + RPT) {  // this thread holds row dr
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e)
+                            if (rw0 + e == dr) rowc[buf * LW + c8] = val[lf][e];
+                    }
+                    __syncthreads();
+                    double pr[FNW];
+#pragma unroll
+                    for (int w = 0; w < FNW; ++w) pr[w] = part[(buf * FNW + w) * LW + c8];
+#pragma unroll
+                    for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
+#pragma unroll
+                        for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
+                    const double S = pr[0];
+                    const double ss = __shfl_sync(0xffffffffu, S, jc);  // lane jc: column jj
+                    const double alpha = rowc[buf * LW + jc];
+                    double tau = 0.0, scal = 0.0, beta = alpha;
+                    if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
+                    const double myrow = rowc[buf * LW + c8];
+                    const double wj = tau * (myrow + scal * S);
+                    // rows > dr: val += mx * x  (lane jc: x = own value -> val = scal * x)
+                    const double mx = (c8 > jc) ? -wj * scal : (c8 == jc ? scal - 1.0 : 0.0);
+                    if (active) {
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e)
+                            if (rw0 + e > dr) val[lf][e] = fma(mx, xr[e], val[lf][e]);
+                    }
+                    if (dr >= rw0 && dr < rw0 + RPT) {  // row dr: beta on the diagonal, -w_j to its right
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e)
+                            if (rw0 + e == dr) val[lf][e] = (c8 > jc) ? val[lf][e] - wj : (c8 == jc ? beta : val[lf][e]);
+                    }
+                    if (tid == jc) taus[jj] = tau;
+                    if (tid < jc) Zl[tid * LW + jc] = myrow + scal * S;  // threads 0..7: c8 = tid
+                    buf ^= 1;
+                }
+                FPROF(2);
+                // -------- blocked update of the later leaves of this panel --------
+                if (jend < nc) {
+                    __syncthreads();  // taus, Zl of the leaf complete
+                    // leaf T (8x8): T(i,i) = tau_i, T(i,c) = -tau_c sum_{l=i}^{c-1} T(i,l) Z(l,c)
+                    if (tid < LW) {
+                        const int i = tid;
+                        double trow[LW];
+#pragma unroll
+                        for (int c = 0; c < LW; ++c) {
+                            double tv = 0.0;
+                            if (c == i) tv = taus[jbeg + i];
+                            else if (c > i) {
+                                double sacc = 0.0;
+#pragma unroll
+                                for (int l = 0; l < c; ++l)
+                                    if (l >= i) sacc += trow[l] * Zl[l * LW + c];
+                                tv = -taus[jbeg + c] * sacc;
+                            }
+                            trow[c] = tv;
+                        }
+#pragma unroll
+                        for (int c = 0; c < LW; ++c) Tl[i * LW + c] = trow[c];
+                    }
+                    // W(i, (l', c)) = sum_r v_i(r) P_l'(r, c) for the leaf's reflectors i
+                    double *wpart = Vs;  // [FNW][LW][PBW]
+#pragma unroll
+                    for (int l2 = lf + 1; l2 < NLF; ++l2) {
+                        double acc[LW];
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) acc[i] = 0.0;
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) {
+                            const int di_ = c0 + jbeg + i;  // diagonal row of reflector i
+#pragma unroll
+                            for (int e = 0; e < RPT; ++e) {
+                                const double vr = __shfl_sync(0xffffffffu, val[lf][e], (rq << 3) | i);
+                                const int r = rw0 + e;
+                                const double v = (r > di_) ? vr : (r == di_ ? 1.0 : 0.0);
+                                acc[i] = fma(v, val[l2][e], acc[i]);
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) {
+                            acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+                            acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+                        }
+                        if (rq == 0)
+#pragma unroll
+                            for (int i = 0; i < LW; ++i) wpart[(warp * LW + i) * PBW + LW * l2 + c8] = acc[i];
+                    }
+                    __syncthreads();
+                    double *Wl = Ts;  // [LW][PBW]
+                    if (tid < LW * PBW) {
+                        const int i = tid / PBW, c = tid % PBW;
+                        double pr[FNW];
+#pragma unroll
+                        for (int w = 0; w < FNW; ++w) pr[w] = (c >= LW * (lf + 1)) ? wpart[(w * LW + i) * PBW + c] : 0.0;
+#pragma unroll
+                        for (int hh = FNW / 2; hh >= 1; hh >>= 1)
+#pragma unroll
+                            for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
+                        Wl[i * PBW + c] = pr[0];
+                    }
+                    __syncthreads();
+                    // W' = T_leaf^T W  (reflectors with jbeg + i >= jend have tau = 0 -> zero rows)
+                    double wp = 0.0;
+                    if (tid < LW * PBW) {
+                        const int a = tid / PBW, c = tid % PBW;
+                        for (int l = 0; l <= a; ++l) wp += Tl[l * LW + a] * Wl[l * PBW + c];
+                    }
+                    __syncthreads();
+                    if (tid < LW * PBW) Wl[tid] = wp;
+                    __syncthreads();
+                    // P_l' -= V_leaf W'
+#pragma unroll
+                    for (int l2 = lf + 1; l2 < NLF; ++l2) {
+                        double wv[LW];
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) wv[i] = Wl[i * PBW + LW * l2 + c8];
+#pragma unroll
+                        for (int i = 0; i < LW; ++i) {
+                            const int di_ = c0 + jbeg + i;
+#pragma unroll
+                            for (int e = 0; e < RPT; ++e) {
+                                const double vr = __shfl_sync(0xffffffffu, val[lf][e], (rq << 3) | i);
+                                const int r = rw0 + e;
+                                const double v = (r > di_) ? vr : (r == di_ ? 1.0 : 0.0);
+                                val[l2][e] = fma(-v, wv[i], val[l2][e]);
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+                FPROF(3);
+            }
             __syncthreads();
-        }
-        // write back R (upper trapezoid of the view, exact zeros below) and Vnat
-        for (int idx = tid; idx < p * q; idx += FNT) {
-            int i = idx % p, j = idx / p;
-            double r = (i <= j) ? Wk[idx] : 0.0;
-            d.W[(int64_t)i * d.rs + (int64_t)j * d.cs] = r;
-            double v = (i < j) ? 0.0 : (i == j ? 1.0 : Wk[idx]);
-            if (i > j && d.tau[j] == 0.0) v = 0.0;
-            int inat = d.rev ? (p - 1 - i) : i;
-            d.V[(int64_t)j * d.ldv + inat] = v;
+            // ---- write R (through the view), V (natural order), tau; V_b stays in Ps ----
+            // R (upper trapezoid of the panel columns) goes through Ps first so that the
+            // global stores are coalesced along the view's contiguous direction.
+#pragma unroll
+            for (int l = 0; l < NLF; ++l)
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = rw0 + e, jl = LW * l + c8, col = c0 + jl;
+                    Ps[jl * L::LDP + r] = (r <= col && r < p && jl < nc) ? val[l][e] : 0.0;
+                }
+            __syncthreads();
+            {
+                const bool rowfast = (rs == 1 || rs == -1);
+                for (int idx = tid; idx < PBW * p; idx += FNT) {
+                    const int j = rowfast ? idx / p : idx % PBW, r = rowfast ? idx % p : idx / PBW;
+                    if (j < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = Ps[j * L::LDP + r];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int l = 0; l < NLF; ++l)
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = rw0 + e, jl = LW * l + c8, col = c0 + jl;
+                    const double tv = taus[jl < nc ? jl : 0];
+                    const double v = (jl >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[l][e]));
+                    Ps[jl * L::LDP + r] = (r < p) ? v : 0.0;
+                }
+            __syncthreads();
+            for (int idx = tid; idx < nc * p; idx += FNT) {
+                const int j = idx / p, r = idx % p;
+                d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = Ps[j * L::LDP + r];
+            }
+            if (tid < nc) d.tau[c0 + tid] = taus[tid];
+            __threadfence_block();
+            FPROF(4);
+            // ---- G_b = V_b^T V_b (DMMA) and T_b by the dlarft recurrence (row i per lane) ----
+            __syncthreads();
+            {
+                const int tm = warp >> 2, tn = warp & 3;
+                const double *pa = Ps + (8 * tm + g) * L::LDP + t4, *pb = Ps + (8 * tn + g) * L::LDP + t4;
+                double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+                int kk = c0;
+                for (; kk + 8 <= p; kk += 8) {
+                    dmma884(x0, x1, pa[kk], pb[kk]);
+                    dmma884(y0, y1, pa[kk + 4], pb[kk + 4]);
+                }
+                for (; kk < p; kk += 4) dmma884(x0, x1, pa[kk], pb[kk]);
+                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = x0 + y0;
+                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = x1 + y1;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                double *trow = Ts + lane * LDT;
+                const int i = lane;
+                for (int c = 0; c < PBW; ++c) trow[c] = (c == i && i < nc) ? taus[i] : 0.0;
+                for (int c = i + 1; c < nc; ++c) {
+                    double sacc = 0.0;
+                    for (int l = i; l < c; ++l) sacc += trow[l] * Xs[l * LDX + c];
+                    trow[c] = -taus[c] * sacc;
+                }
+                if (i < nc)
+                    for (int c = 0; c < nc; ++c) Tout(c0 + i, c0 + c) = trow[c];
+            }
+            __threadfence_block();
+            __syncthreads();
+            FPROF(5);
+            // ---- off-diagonal T blocks: T(0:c0, c0:c0+nc) = -T(0:c0,0:c0) G T_b,  G = V(:,0:c0)^T V_b ----
+            if (b > 0) {
+                for (int i = 0; i < b; ++i) {
+                    double o0, o1;
+                    vt_times_panel<RPT>(d, i, c0, Ps, Vs, o0, o1);  // V_i^T V_b (V_b = 0 above row c0)
+                    const int tm = warp >> 2, tn = warp & 3;
+                    gscratch[(size_t)(i * PBW + 8 * tm + g) * PBW + 8 * tn + 2 * t4] = o0;
+                    gscratch[(size_t)(i * PBW + 8 * tm + g) * PBW + 8 * tn + 2 * t4 + 1] = o1;
+                }
+                __threadfence_block();
+                __syncthreads();
+                // Y = G T_b (c0 x 32; T_b upper, zero beyond nc): 8x8 tiles over warps
+                double *Yg = gscratch + (size_t)c0 * PBW;
+                for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
+                    const int tr = tile >> 2, tn = tile & 3;
+                    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < PBW; kk += 4) {
+                        const double av = gscratch[(size_t)(8 * tr + g) * PBW + kk + t4];
+                        const int kr = kk + t4, cc = 8 * tn + g;
+                        const double bv = (kr <= cc && cc < nc) ? Tout(c0 + kr, c0 + cc) : 0.0;
+                        dmma884(a0, a1, av, bv);
+                    }
+                    Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4] = a0;
+                    Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4 + 1] = a1;
+                }
+                __threadfence_block();
+                __syncthreads();
+                // T(0:c0, c0:c0+nc) = -T(0:c0, 0:c0) Y  (T upper: k from the tile's first row)
+                for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
+                    const int tr = tile >> 2, tn = tile & 3;
+                    double a0 = 0.0, a1 = 0.0;
+                    for (int kk = 8 * tr; kk < c0; kk += 4) {
+                        const int row = 8 * tr + g, kr = kk + t4;
+                        const double av = (kr >= row) ? Tout(row, kr) : 0.0;
+                        const double bv = Yg[(size_t)kr * PBW + 8 * tn + g];
+                        dmma884(a0, a1, av, bv);
+                    }
+                    const int row = 8 * tr + g, cc = 8 * tn + 2 * t4;
+                    if (cc < nc) Tout(row, c0 + cc) = -a0;
+                    if (cc + 1 < nc) Tout(row, c0 + cc + 1) = -a1;
+                }
+            }
+            FPROF(6);
+            // zeros below the diagonal block
+            for (int idx = tid; idx < nc * (q - c0); idx += FNT) {
+                const int c = idx / (q - c0), a = c0 + idx % (q - c0);
+                if (a > c0 + c) Tout(a, c0 + c) = 0.0;
+            }
+            __threadfence_block();
+            __syncthreads();
+            FPROF(7);
         }
         __threadfence();
         __syncthreads();
     }
 }
 
-// T from G = V^T V by the dlarft forward recurrence:
-// T(c,c) = tau_c, T(0:c,c) = -tau_c T(0:c,0:c) G(0:c,c).  One CTA per window.
-__global__ void larft_kernel(const LarftDesc *descs)
+template <int RPT>
+int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch)
 {
-    const LarftDesc d = descs[blockIdx.x];
-    const int q = d.q;
-    for (int c = 0; c < q; ++c) {
-        const double tc = d.tau[c];
-        for (int i = threadIdx.x; i < c; i += blockDim.x) {
-            double s = 0.0;
-            for (int l = i; l < c; ++l) s += d.T[(int64_t)l * d.ldt + i] * d.G[(int64_t)c * d.ldg + l];
-            d.T[(int64_t)c * d.ldt + i] = -tc * s;
-        }
-        if (threadIdx.x == 0) d.T[(int64_t)c * d.ldt + c] = tc;
-        for (int i = c + 1 + threadIdx.x; i < q; i += blockDim.x) d.T[(int64_t)c * d.ldt + i] = 0.0;
-        __syncthreads();
+    const int smem = FactorSmem<RPT>::DOUBLES * (int)sizeof(double);
+    static bool init = false;
+    if (!init) {
+        HT_CUDA_TRY(cudaFuncSetAttribute(factor_qr_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        init = true;
     }
+    factor_qr_kernel<RPT><<<1, FNT, smem, st>>>(d_descs, nd, gscratch);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
 }
 
 }  // namespace
 
-int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxpq)
+int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp)
 {
     if (nd <= 0) return 0;
-    static int smem_max = -1;
-    if (smem_max < 0) {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        smem_max = v - 4096;
-        cudaFuncSetAttribute(factor_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    }
-    int want = maxpq * 8;
-    int smem = want <= smem_max ? want : 0;
-    factor_qr_kernel<<<1, FNT, smem, st>>>(d_descs, nd, gscratch, smem / 8);
-    HT_CUDA_TRY(cudaGetLastError());
-    return 0;
-}
-
-int ht_larft_run(cudaStream_t st, const LarftDesc *d_descs, int nd)
-{
-    if (nd <= 0) return 0;
-    larft_kernel<<<nd, 256, 0, st>>>(d_descs);
-    HT_CUDA_TRY(cudaGetLastError());
-    return 0;
+    if (maxp <= FactorSmem<2>::MAXP) return launch_factor<2>(st, d_descs, nd, gscratch);
+    if (maxp <= FactorSmem<4>::MAXP) return launch_factor<4>(st, d_descs, nd, gscratch);
+    if (maxp <= FactorSmem<8>::MAXP) return launch_factor<8>(st, d_descs, nd, gscratch);
+    return 4;  // HT_ENUMERIC: window taller than 512 rows (nb <= 256 guarantees p <= 512)
 }

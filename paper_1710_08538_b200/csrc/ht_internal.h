@@ -15,6 +15,8 @@ struct FactorDesc {
     double *V;
     int64_t ldv;
     double *tau;
+    double *T;     // q x q upper-triangular compact-WY factor of Q = H_0 H_1 ... H_{q-1}
+    int64_t ldt;
 };
 struct LarftDesc {
     const double *G;  // V^T V (q x q)
@@ -25,7 +27,25 @@ struct LarftDesc {
     int q;
 };
 
-int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxpq);
+// chained window applies (ht_chain.cu): per matrix, slab dimension s in [s_begin, s_end)
+// (rows if !left, columns if left), window dimension c; element (s, c) is X[s + c*ld]
+// (right apply, X <- X Qhat) or X[c + s*ld] (left apply, X <- Qhat^T X).
+struct ChainMat {
+    double *X;
+    int64_t ld;
+    int left;
+    int64_t s_begin, s_end;
+};
+// one window: columns (rows) [o, o+p) <- . * Qw (p x p, ld p); applied to slabs s in [lo[m], hi[m])
+struct ChainWin {
+    const double *Qw;
+    int64_t o;
+    int p;
+    int64_t lo[3], hi[3];
+};
+int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax);
+
+int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp);
 int ht_larft_run(cudaStream_t st, const LarftDesc *d_descs, int nd);
 
 // panel kernel (ht_panel.cu)

@@ -1,0 +1,84 @@
+// Micro-benchmark + self-check of the window factorization kernel (development tool).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_1710_08538_b200/csrc
+//        factor_bench.cu -o factor_bench
+// Usage: ./factor_bench p q [reps] [rev] [transposed]
+#include "../../paper_1710_08538_b200/csrc/ht_factor.cu"
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+int ht_cuda_fail(cudaError_t e, const char *what, const char *file, int line)
+{
+    fprintf(stderr, "CUDA error %s at %s:%d (%s)\n", cudaGetErrorString(e), file, line, what);
+    return 2;
+}
+int main(int argc, char **argv)
+{
+    const int p = argc > 1 ? atoi(argv[1]) : 256, q = argc > 2 ? atoi(argv[2]) : 128;
+    const int reps = argc > 3 ? atoi(argv[3]) : 10;
+    const int rev = argc > 4 ? atoi(argv[4]) : 0;
+    std::vector<double> W0((size_t)p * q);
+    srand(1);
+    for (auto &x : W0) x = (double)rand() / RAND_MAX - 0.5;
+    double *dW, *dV, *dtau, *dT, *dg;
+    cudaMalloc(&dW, W0.size() * 8); cudaMalloc(&dV, (size_t)p * q * 8); cudaMalloc(&dtau, q * 8);
+    cudaMalloc(&dT, (size_t)q * q * 8); cudaMalloc(&dg, 64 * 1024 * 8);
+    FactorDesc hd;
+    // view: rev -> reversed rows and columns (QL-type); W(i, j) = base[i*rs + j*cs]
+    if (rev) hd = FactorDesc{dW + (p - 1) + (size_t)(q - 1) * p, -1, -(int64_t)p, p, q, 1, dV, p, dtau, dT, q};
+    else hd = FactorDesc{dW, 1, p, p, q, 0, dV, p, dtau, dT, q};
+    FactorDesc *dd; cudaMalloc(&dd, sizeof(FactorDesc));
+    cudaMemcpy(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice);
+    unsigned long long *dprof; cudaMalloc(&dprof, 16 * 8); cudaMemset(dprof, 0, 16 * 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int it = 0; it < reps + 1; ++it) {
+        cudaMemcpy(dW, W0.data(), W0.size() * 8, cudaMemcpyHostToDevice);
+        if (it == reps) cudaMemcpyToSymbol(g_fprof, &dprof, sizeof(dprof));
+        cudaEventRecord(e0);
+        int rc = ht_factor_run(0, dd, 1, dg, p);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        if (rc || cudaGetLastError() != cudaSuccess) { printf("launch failed\n"); return 1; }
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (it < reps) best = ms < best ? ms : best;
+    }
+    unsigned long long hp[16]; cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost);
+    printf("p=%d q=%d rev=%d: best %.1f us | phases(us): load %.1f left %.1f leafsteps %.1f leafupd %.1f write %.1f GT %.1f offT %.1f zero %.1f\n",
+           p, q, rev, best * 1e3, hp[0] * 1e-3, hp[1] * 1e-3, hp[2] * 1e-3, hp[3] * 1e-3, hp[4] * 1e-3, hp[5] * 1e-3,
+           hp[6] * 1e-3, hp[7] * 1e-3);
+    // check: with the view W (p x q, view coordinates), Q = I - V T V^T (V in natural order);
+    // natural-order window Wn0 = Q * Rn where Rn is the R written back through the view.
+    std::vector<double> Wf(W0.size()), V((size_t)p * q), T((size_t)q * q);
+    cudaMemcpy(Wf.data(), dW, Wf.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(V.data(), dV, V.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(T.data(), dT, T.size() * 8, cudaMemcpyDeviceToHost);
+    // view accessors on host (natural storage index)
+    auto vidx = [&](int i, int j) -> size_t { return rev ? (size_t)(p - 1 - i) + (size_t)(q - 1 - j) * p : (size_t)i + (size_t)j * p; };
+    // Qv = I - Vv T Vv^T in view row order (Vv(i,j) = V(nat(i), j))
+    double maxres = 0, nrm = 0, maxlow = 0;
+    std::vector<double> VT((size_t)p * q, 0.0);  // Vv * T
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < q; ++j) {
+            double s = 0;
+            for (int l = 0; l <= j; ++l) s += V[(size_t)l * p + (rev ? p - 1 - i : i)] * T[(size_t)j * q + l];
+            VT[(size_t)j * p + i] = s;
+        }
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < q; ++j) {
+            // (Qv R)(i, j) = R(i,j) - sum_l VT(i,l) * (Vv^T R)(l, j)
+            double r = 0;
+            double acc = (i <= j) ? Wf[vidx(i, j)] : 0.0;
+            if (i > j && Wf[vidx(i, j)] != 0.0) maxlow = fmax(maxlow, fabs(Wf[vidx(i, j)]));
+            for (int l = 0; l < q; ++l) {
+                double vr = 0;
+                for (int m = 0; m <= j && m < p; ++m) vr += V[(size_t)l * p + (rev ? p - 1 - m : m)] * Wf[vidx(m, j)] * (m <= j);
+                acc -= VT[(size_t)l * p + i] * vr;
+            }
+            (void)r;
+            maxres = fmax(maxres, fabs(acc - W0[vidx(i, j)]));
+            nrm = fmax(nrm, fabs(W0[vidx(i, j)]));
+        }
+    printf("check: max |Q R - W0| / max|W0| = %.2e, nonzero below diag = %.2e\n", maxres / nrm, maxlow);
+    return 0;
+}
