@@ -32,15 +32,17 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 struct ChainParams {
     ChainMat m[3];
     int nm;
-    int h, cap, kc;      // slab height, ring capacity (columns), Qhat rows per chunk
+    int h, cap;          // slab height, ring capacity (columns); both powers of two
     const ChainWin *wins;
     int nw;
 };
 
+template <int KC>
 __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P)
 {
     extern __shared__ __align__(16) double csm[];
-    const int h = P.h, cap = P.cap, kc = P.kc;
+    const int h = P.h, cap = P.cap;
+    constexpr int kc = KC;
     const int ldh = h + 8;          // == 8 mod 32: conflict-free A fragments
     const int ldq = cap + 8;        // == 8 mod 32: conflict-free B fragments
     double *Xs = csm;               // [cap][ldh]  ring of slab columns
@@ -62,49 +64,45 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P
     auto gaddr = [&](int s, int64_t c) -> double * {
         return M.left ? M.X + c + (s0 + s) * M.ld : M.X + (s0 + s) + c * M.ld;
     };
-    auto slot = [&](int64_t c) -> int { return (int)(c % cap); };
-    // move columns [c_lo, c_hi) between HBM and the ring
+    const int capm = cap - 1;
+    auto slot = [&](int64_t c) -> int { return (int)c & capm; };
+    // move columns [c_lo, c_hi) between HBM and the ring (coalesced along the contiguous
+    // direction: rows of a column for right applies, columns of a row for left applies)
     auto load_cols = [&](int64_t c_lo, int64_t c_hi) {
-        const int64_t nc = c_hi - c_lo;
+        const int nc = (int)(c_hi - c_lo);
         if (nc <= 0) return;
-        if (M.left) {  // contiguous along c
-            for (int64_t idx = tid; idx < nc * h; idx += CNT) {
-                const int64_t c = c_lo + idx % nc;
-                const int s = (int)(idx / nc);
-                Xs[slot(c) * ldh + s] = (s < hs) ? *gaddr(s, c) : 0.0;
-            }
-        } else {       // contiguous along s
-            for (int64_t idx = tid; idx < nc * h; idx += CNT) {
-                const int s = (int)(idx % h);
-                const int64_t c = c_lo + idx / h;
-                Xs[slot(c) * ldh + s] = (s < hs) ? *gaddr(s, c) : 0.0;
-            }
+        if (M.left) {
+            for (int s = warp; s < h; s += CNT / 32)
+                for (int c = lane; c < nc; c += 32)
+                    Xs[slot(c_lo + c) * ldh + s] = (s < hs) ? *gaddr(s, c_lo + c) : 0.0;
+        } else {
+            for (int c = warp; c < nc; c += CNT / 32)
+                for (int s = lane; s < h; s += 32)
+                    Xs[slot(c_lo + c) * ldh + s] = (s < hs) ? *gaddr(s, c_lo + c) : 0.0;
         }
     };
     auto store_cols = [&](int64_t c_lo, int64_t c_hi) {
-        const int64_t nc = c_hi - c_lo;
+        const int nc = (int)(c_hi - c_lo);
         if (nc <= 0) return;
         if (M.left) {
-            for (int64_t idx = tid; idx < nc * h; idx += CNT) {
-                const int64_t c = c_lo + idx % nc;
-                const int s = (int)(idx / nc);
-                if (s < hs) *gaddr(s, c) = Xs[slot(c) * ldh + s];
-            }
+            for (int s = warp; s < hs; s += CNT / 32)
+                for (int c = lane; c < nc; c += 32) *gaddr(s, c_lo + c) = Xs[slot(c_lo + c) * ldh + s];
         } else {
-            for (int64_t idx = tid; idx < nc * h; idx += CNT) {
-                const int s = (int)(idx % h);
-                const int64_t c = c_lo + idx / h;
-                if (s < hs) *gaddr(s, c) = Xs[slot(c) * ldh + s];
-            }
+            for (int c = warp; c < nc; c += CNT / 32)
+                for (int s = lane; s < hs; s += 32) *gaddr(s, c_lo + c) = Xs[slot(c_lo + c) * ldh + s];
         }
     };
+    // padding columns [o + p, o + pp) of a window must read as zeros (their Qhat rows are 0,
+    // but 0 * NaN would not be): they are dead ring slots, zeroed before the window runs
+    auto zero_pad = [&](int64_t o, int p) {
+        const int pp = (p + 31) & ~31;
+        for (int idx = tid; idx < (pp - p) * ldh; idx += CNT) Xs[slot(o + p + idx / ldh) * ldh + idx % ldh] = 0.0;
+    };
 
-    // zero the ring once (padding columns must hold finite values)
-    for (int idx = tid; idx < cap * ldh; idx += CNT) Xs[idx] = 0.0;
-    __syncthreads();
     {
         const ChainWin w0 = P.wins[0];
         load_cols(w0.o, (int64_t)w0.o + w0.p);
+        zero_pad(w0.o, w0.p);
     }
     for (int wi = 0; wi < P.nw; ++wi) {
         const ChainWin W = P.wins[wi];
@@ -128,7 +126,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P
                 for (int e = 0; e < 8; ++e) {
                     if (e >= per) break;
                     const int idx = tid + e * CNT;
-                    const int kr = idx % kc, c = idx / kc;
+                    const int kr = idx % KC, c = idx / KC;
                     double v = 0.0;
                     if (c < p && k0 + kr < p) v = W.Qw[(size_t)(k0 + kr) + (size_t)c * p];
                     rq[e] = v;
@@ -139,7 +137,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P
                 for (int e = 0; e < 8; ++e) {
                     if (e >= per) break;
                     const int idx = tid + e * CNT;
-                    const int kr = idx % kc, c = idx / kc;
+                    const int kr = idx % KC, c = idx / KC;
                     if (c < pp) Qs[(size_t)buf * kc * ldq + kr * ldq + c] = rq[e];
                 }
             };
@@ -152,7 +150,8 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P
                 if (kt + 1 < nk) fetch((kt + 1) * kc);
                 if (wact) {
                     const double *qb = Qs + (size_t)buf * kc * ldq;
-                    for (int kk = 0; kk < kc; kk += 4) {
+#pragma unroll
+                    for (int kk = 0; kk < KC; kk += 4) {
                         const int64_t cA = (int64_t)W.o + kt * kc + kk + t4;  // window column of A frag
                         const double *xa = Xs + slot(cA) * ldh + wr * 32 + g;
                         double af[4], bf[4];
@@ -197,6 +196,8 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P
             __syncthreads();
             load_cols(b0, b1 < a0 ? b1 : a0);
             load_cols(b0 > a1 ? b0 : a1, b1);
+            __syncthreads();
+            zero_pad(N.o, N.p);
         } else {
             store_cols(a0, a1);
         }
@@ -217,21 +218,23 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
     P.cap = pp <= 256 ? 256 : 512;
     P.h = SLAB_ELEMS / P.cap;          // 64 (p <= 256) or 32 (p <= 512)
     if (pp <= 128) { P.cap = 128; P.h = 128; }
-    P.kc = P.cap <= 256 ? 16 : 8;
     P.wins = d_wins;
     P.nw = nw;
     int64_t nblk = 0;
     for (int i = 0; i < nm; ++i)
         if (mats[i].s_end > mats[i].s_begin) nblk += (mats[i].s_end - mats[i].s_begin + P.h - 1) / P.h;
     if (nblk == 0) return 0;
-    const size_t smem = ((size_t)P.cap * (P.h + 8) + 2 * (size_t)P.kc * (P.cap + 8)) * sizeof(double);
+    const int kc = P.cap <= 256 ? 16 : 8;
+    const size_t smem = ((size_t)P.cap * (P.h + 8) + 2 * (size_t)kc * (P.cap + 8)) * sizeof(double);
     static bool init = false;
     if (!init) {
-        HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(SLAB_ELEMS + 8 * 512 + 2 * 16 * 264) * 8));
+        const int mx = (int)(SLAB_ELEMS + 8 * 512 + 2 * 16 * 264) * 8;
+        HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         init = true;
     }
-    chain_apply_kernel<<<(unsigned)nblk, CNT, smem, st>>>(P);
+    if (kc == 16) chain_apply_kernel<16><<<(unsigned)nblk, CNT, smem, st>>>(P);
+    else chain_apply_kernel<8><<<(unsigned)nblk, CNT, smem, st>>>(P);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -51,7 +51,7 @@ struct Work {
     double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
-    double *Dinv = nullptr, *Mb = nullptr;
+    double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
     int *dsafe = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
@@ -124,8 +124,10 @@ void work_free(Work &w)
     if (w.d_irtrace) cudaFree(w.d_irtrace);
     w.d_irtrace = nullptr;
     if (w.Dinv) cudaFree(w.Dinv);
-    if (w.Mb) cudaFree(w.Mb);
-    w.Mb = nullptr;
+    if (w.Bt) cudaFree(w.Bt);
+    w.Bt = nullptr;
+    if (w.ypart) cudaFree(w.ypart);
+    w.ypart = nullptr;
     if (w.dsafe) cudaFree(w.dsafe);
     w.Dinv = nullptr;
     w.dsafe = nullptr;
@@ -194,7 +196,8 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
-    TRY(dalloc(&w.Mb, (size_t)(N / 128 + 2) * 128 * 128));
+    TRY(dalloc(&w.Bt, (size_t)N * (size_t)N));
+    TRY(dalloc(&w.ypart, (size_t)(N / 256 + 2) * (size_t)N));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -690,6 +693,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             HT_CUDA_TRY(cudaMalloc((void **)&dbg, (size_t)n * 12 * sizeof(double)));
             HT_CUDA_TRY(cudaMemset(dbg, 0, (size_t)n * 12 * sizeof(double)));
         }
+        unsigned long long *ttr = nullptr;
+        const int64_t tcol = getenv("HT_TRACE_COL") ? atoll(getenv("HT_TRACE_COL")) : -1;
+        if (tcol >= 0) {
+            HT_CUDA_TRY(cudaMalloc((void **)&ttr, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+            HT_CUDA_TRY(cudaMemset(ttr, 0, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+        }
         int64_t s0 = 0;
         while (s0 <= n - 3) {
             const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
@@ -707,12 +716,14 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.vw = vv + 4 * N; pa.vw2 = vv + 5 * N; pa.vr = vv + 6 * N;
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.flags = w->flags; pa.bexp = w->bexp; pa.epoch = w->epoch;
-            pa.Dinv = w->Dinv; pa.Mb = w->Mb; pa.dsafe = w->dsafe;
+            pa.Dinv = w->Dinv; pa.Bt = w->Bt; pa.ldbt = n; pa.dsafe = w->dsafe; pa.ypart = w->ypart;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;
             pa.irtrace = w->d_irtrace;
             pa.dbg = dbg;
+            pa.ttrace = ttr;
+            pa.tcol = tcol;
             pa.ptime = ptime;
             const int64_t M = n - s0 - 1;
             int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 31) / 32));
@@ -748,6 +759,21 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.3f", names[i], hp[i]);
             fprintf(stderr, "\n");
             cudaFree(ptime);
+        }
+        if (ttr) {
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            const int nbk = (int)((n - 1 + 127) / 128) + 2;
+            std::vector<unsigned long long> h((size_t)nbk * 4);
+            HT_CUDA_TRY(cudaMemcpy(h.data(), ttr, h.size() * 8, cudaMemcpyDeviceToHost));
+            unsigned long long t0 = ~0ull;
+            for (auto v : h)
+                if (v && v < t0) t0 = v;
+            fprintf(stderr, "[ht trace] col %lld: block: tiles_done wait_done publish (us from first event)\n", (long long)tcol);
+            for (int b = nbk - 1; b >= 0; --b)
+                if (h[4 * b + 2])
+                    fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f\n", b, h[4 * b] ? (h[4 * b] - t0) * 1e-3 : -1.0,
+                            h[4 * b + 1] ? (h[4 * b + 1] - t0) * 1e-3 : -1.0, (h[4 * b + 2] - t0) * 1e-3);
+            cudaFree(ttr);
         }
         if (dbg_on) {
             HT_CUDA_TRY(cudaStreamSynchronize(st));

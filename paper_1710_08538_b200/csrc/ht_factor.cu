@@ -219,9 +219,11 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
             for (int i = 0; i < b; ++i) {
                 const int r_lo = i * PBW;  // V_i is zero above row r_lo
                 __syncthreads();
-                for (int idx = tid; idx < PBW * PBW; idx += FNT) {
-                    const int a = idx / PBW, c = idx % PBW;
-                    Ts[a * LDT + c] = Tout(r_lo + a, r_lo + c);  // diagonal block T_i
+                {
+                    const int c = tid / PBW, a = tid % PBW;  // 2 elements per thread, both loads first
+                    const double t0 = Tout(r_lo + a, r_lo + c), t1 = Tout(r_lo + a, r_lo + c + FNT / PBW);
+                    Ts[a * LDT + c] = t0;
+                    Ts[a * LDT + c + FNT / PBW] = t1;  // diagonal block T_i
                 }
                 double o0, o1;
                 vt_times_panel<RPT>(d, i, r_lo, Ps, Vs, o0, o1);
@@ -235,9 +237,14 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 double xv[2];
                 for (int e = 0; e < 2; ++e) {
                     const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
-                    double s = 0.0;
-                    for (int l = 0; l <= a; ++l) s += Ts[l * LDT + a] * Xs[l * LDX + c];
-                    xv[e] = s;
+                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
+                    int l = 0;
+                    for (; l + 4 <= a + 1; l += 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) sa[u] = fma(Ts[(l + u) * LDT + a], Xs[(l + u) * LDX + c], sa[u]);
+                    }
+                    for (; l <= a; ++l) sa[0] = fma(Ts[l * LDT + a], Xs[l * LDX + c], sa[0]);
+                    xv[e] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
                 }
                 __syncthreads();
                 for (int e = 0; e < 2; ++e) {
@@ -455,12 +462,12 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     Ps[jl * L::LDP + r] = (r <= col && r < p && jl < nc) ? val[l][e] : 0.0;
                 }
             __syncthreads();
-            {
-                const bool rowfast = (rs == 1 || rs == -1);
-                for (int idx = tid; idx < PBW * p; idx += FNT) {
-                    const int j = rowfast ? idx / p : idx % PBW, r = rowfast ? idx % p : idx / PBW;
-                    if (j < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = Ps[j * L::LDP + r];
-                }
+            if (rs == 1 || rs == -1) {  // contiguous along rows: lanes over rows
+                for (int j = warp; j < nc; j += FNW)
+                    for (int r = lane; r < p; r += 32) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = Ps[j * L::LDP + r];
+            } else {                     // contiguous along columns: lanes over columns
+                for (int r = warp; r < p; r += FNW)
+                    if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = Ps[lane * L::LDP + r];
             }
             __syncthreads();
 #pragma unroll
@@ -473,10 +480,8 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     Ps[jl * L::LDP + r] = (r < p) ? v : 0.0;
                 }
             __syncthreads();
-            for (int idx = tid; idx < nc * p; idx += FNT) {
-                const int j = idx / p, r = idx % p;
-                d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = Ps[j * L::LDP + r];
-            }
+            for (int j = warp; j < nc; j += FNW)
+                for (int r = lane; r < p; r += 32) d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = Ps[j * L::LDP + r];
             if (tid < nc) d.tau[c0 + tid] = taus[tid];
             __threadfence_block();
             FPROF(4);
@@ -501,9 +506,14 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 const int i = lane;
                 for (int c = 0; c < PBW; ++c) trow[c] = (c == i && i < nc) ? taus[i] : 0.0;
                 for (int c = i + 1; c < nc; ++c) {
-                    double sacc = 0.0;
-                    for (int l = i; l < c; ++l) sacc += trow[l] * Xs[l * LDX + c];
-                    trow[c] = -taus[c] * sacc;
+                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
+                    int l = i;
+                    for (; l + 4 <= c; l += 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) sa[u] = fma(trow[l + u], Xs[(l + u) * LDX + c], sa[u]);
+                    }
+                    for (; l < c; ++l) sa[0] = fma(trow[l], Xs[l * LDX + c], sa[0]);
+                    trow[c] = -taus[c] * ((sa[0] + sa[1]) + (sa[2] + sa[3]));
                 }
                 if (i < nc)
                     for (int c = 0; c < nc; ++c) Tout(c0 + i, c0 + c) = trow[c];

@@ -63,7 +63,8 @@ struct PanelArgs {
     int pw;
     unsigned long long *flags;  // trsv publish words (epoch << 32 | exponent), per 128-row block
     double *Dinv;       // inverted 128x128 diagonal blocks of B(s+1:n, s+1:n)
-    double *Mb;         // Dinv_b * B(block b, block b+1) (look-ahead coupling blocks)
+    double *Bt;         // Dinv_b * B(block b, blocks > b): pre-scaled block rows
+    int64_t ldbt;
     int *dsafe;         // per block: 1 = use Dinv, 0 = sequential scaled substitution
     int *bexp;          // trsv block exponents
     unsigned epoch;     // trsv flag epoch base
@@ -74,6 +75,9 @@ struct PanelArgs {
     double *ptime;      // optional (HT_PROFILE): per-phase seconds, CTA 0 (globaltimer)
     double *dbg;        // optional (HT_DEBUG_IR): dbg[j*12 + it] = ||r||/(tol ||x||) per IR iteration
     int *irtrace;       // per-column IR count (+1000 after a failed attempt)
+    unsigned long long *ttrace;  // optional (HT_TRACE_COL): per-block trsv timestamps of one column
+    int64_t tcol;
+    double *ypart;      // tiled mat-vec partial sums: [column chunk][row], ld = n
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
 };
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);

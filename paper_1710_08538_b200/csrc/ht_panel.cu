@@ -25,6 +25,7 @@
 // (reading R-Z8), so y~ never overflows.  HBM-bound sweeps (B w, A v, the
 // off-diagonal solve tiles) are issued with many independent loads per thread.
 #include <cooperative_groups.h>
+#include <vector>
 #include "ht_common.cuh"
 #include "ht_internal.h"
 
@@ -38,7 +39,7 @@ constexpr int TB = 128;    // triangular-solve block size
 constexpr int NBMAX = 256; // max panel width supported
 constexpr int RBMAX = 256; // max own rows per CTA (uniform slabs)
 constexpr double BIG = 0x1p256;
-constexpr int DYN_DOUBLES = TB * TB + 4 * TB;  // Dinv / staging + trsv group partials
+constexpr int DYN_DOUBLES = TB * TB + 8 * TB;  // M tile / staging + trsv group partials (8 x TB)
 
 struct __align__(16) PanelSmem {
     double sv1[NBMAX + 2];
@@ -90,17 +91,26 @@ struct Ctx {
     __device__ double *curpart() { return part[ph & 1]; }
 
     // out[c] = sum over own rows of X(r,c) * vloc[r - rb0], c < ncols -> mypart()[off + c].
-    // Per-lane partials go through shared staging so that every warp keeps many
-    // independent loads in flight (no shuffle per column).
+    // Warps take 4 columns at a time and issue all their loads before summing
+    // (memory-level parallelism); lane partials go through shared staging.
     __device__ void coltdot(const double *X, int64_t ldx, int ncols, int off)
     {
         double *stg = dyn;  // ncols x 33
-        for (int c = warp; c < ncols; c += NWP) {
-            double s = 0.0;
-            const double *xp = X + (size_t)c * ldx + rb0;
-#pragma unroll 4
-            for (int rl = lane; rl < nr; rl += 32) s += xp[rl] * sm.vloc[rl];
-            stg[c * 33 + lane] = s;
+        for (int c0 = warp * 4; c0 < ncols; c0 += NWP * 4) {
+            double acc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = 0.0;
+            for (int rl = lane; rl < nr; rl += 32) {
+                double xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = (c0 + u < ncols) ? X[(size_t)(c0 + u) * ldx + rb0 + rl] : 0.0;
+                const double vv = sm.vloc[rl];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[u] = fma(xv[u], vv, acc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + u < ncols) stg[(c0 + u) * 33 + lane] = acc[u];
         }
         __syncthreads();
         double *out = mypart() + off;
@@ -136,25 +146,29 @@ struct Ctx {
         __syncthreads();
     }
     // after a grid sync: dst[c] = sum_b part[b][off + c]  (fixed order: deterministic).
-    // Lanes split the CTA partials, warps split the columns; per-lane sums are staged
-    // in shared memory so the L2 loads of all columns are in flight together.
+    // Warps take 2 columns at a time, lanes split the CTA partials; all loads of a lane
+    // are issued before the sums (the partials live in L2: latency, not bandwidth, bound).
     __device__ void gather(double *dst, int ncols, int off)
     {
         const double *pp = curpart() + off;
-        double *stg = dyn + TB * TB;  // reuse the tail of the dynamic buffer: ncols x 33 doubles
-        if (ncols * 33 > 4 * TB) stg = dyn;
-#pragma unroll 4
-        for (int c = warp; c < ncols; c += NWP) {
-            double s = 0.0;
-            for (int b = lane; b < G; b += 32) s += pp[(size_t)b * a.pw + c];
-            stg[c * 33 + lane] = s;
-        }
-        __syncthreads();
-        for (int c = tid; c < ncols; c += PNT) {
-            double t = 0.0;
-#pragma unroll 8
-            for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
-            dst[c] = t;
+        constexpr int MAXB = 8;  // G <= 256 CTAs
+        for (int c0 = warp * 2; c0 < ncols; c0 += NWP * 2) {
+            double v[2][MAXB];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int q = 0; q < MAXB; ++q) {
+                    const int b = lane + 32 * q;
+                    v[u][q] = (b < G && c0 + u < ncols) ? __ldcg(pp + (size_t)b * a.pw + c0 + u) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < MAXB; ++q) t += v[u][q];
+                t = warp_sum(t);
+                if (lane == 0 && c0 + u < ncols) dst[c0 + u] = t;
+            }
         }
         __syncthreads();
     }
@@ -193,15 +207,13 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------------------
-// Block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs  (flag chain, 128-row blocks).
-// rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k).
-// Block b is owned by CTA (Nb-1-b) mod G and published through the 64-bit word
-// flags[b] = (epoch << 32) | exponent, where true y~_b = 2^exponent * vy_b.
-// Safe blocks use the look-ahead form  y~_b = c_b - M_b y~_{b+1}  with
-// c_b = Dinv_b (rhs_b - sum_{c > b+1} B_bc y~_c) computed before y~_{b+1} is known
-// and M_b = Dinv_b B_{b,b+1} precomputed per panel, so the chain's critical path
-// is one shared-memory 128x128 mat-vec per block.  Unsafe blocks (tiny pivots)
-// use the overflow-safe sequential substitution.
+// Flag-chained block back-substitution (see trsv_blocked below).
+// 2^e as a double for |e| <= 1000 (exact; bit construction instead of ldexp's special cases)
+__device__ __forceinline__ double pow2i(int e)
+{
+    e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
 __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p)
 {
     unsigned long long v;
@@ -226,13 +238,61 @@ __device__ __forceinline__ int wait_block(Ctx &C, int cb, unsigned epoch, int sl
     return C.sm.ival[slot];
 }
 
-template <class BaseF, class UnewF>
-__device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, unsigned epoch)
+// acc(ri) += sum_{l < w} Xt(ri, l) * y(l) over one 128 x 128 tile (column-major, ld ldx)
+// for the 128 rows of a block; y from global (L2).  Thread (rp, grp): rows 2rp, 2rp+1,
+// columns grp, grp+8, ...: 16-byte loads, all 16 issued before any FMA.  The 8 column
+// groups are folded through shared memory by the caller (acc8).
+__device__ __forceinline__ void tile_mv(const double *Xt, int64_t ldx, const double *y, int w, int h, int tid,
+                                        double &a0, double &a1)
 {
+    const int rp = tid & 63, grp = tid >> 6;  // 64 row pairs x 8 column groups
+    const bool vec = ((ldx & 1) == 0) && ((((uintptr_t)Xt) & 15) == 0);
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        double2 xv[8];
+        double yv[8];
+        if (vec) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int l = grp + 8 * (q + 8 * half);
+                if (l < w && 2 * rp + 1 < h) xv[q] = *reinterpret_cast<const double2 *>(Xt + (size_t)l * ldx + 2 * rp);
+                else xv[q] = make_double2((l < w && 2 * rp < h) ? Xt[(size_t)l * ldx + 2 * rp] : 0.0, 0.0);
+                yv[q] = (l < w) ? __ldcg(y + l) : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int l = grp + 8 * (q + 8 * half);
+                xv[q].x = (l < w && 2 * rp < h) ? Xt[(size_t)l * ldx + 2 * rp] : 0.0;
+                xv[q].y = (l < w && 2 * rp + 1 < h) ? Xt[(size_t)l * ldx + 2 * rp + 1] : 0.0;
+                yv[q] = (l < w) ? __ldcg(y + l) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            a0 = fma(xv[q].x, yv[q], a0);
+            a1 = fma(xv[q].y, yv[q], a1);
+        }
+    }
+}
+
+// Block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs  (flag chain, 128-row blocks).
+// rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k).
+// Block b is owned by CTA (Nb-1-b) mod G and published through the 64-bit word
+// flags[b] = (epoch << 32) | exponent, where true y~_b = 2^exponent * vy_b.
+// Safe blocks use the pre-scaled block rows  Bt_bc = Dinv_b B_bc  (c > b, formed per
+// panel by ht_panel_run):  y~_b = Dinv_b rhs_b - sum_{c > b} Bt_bc y~_c, the terms
+// accumulated as the y~_c arrive; the chain's critical path is the last term
+// Bt_{b,b+1} y~_{b+1}, staged in shared memory.  Unsafe blocks (tiny pivots) use the
+// original B and the overflow-safe sequential substitution.
+template <class BaseF, class UnewF>
+__device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, unsigned epoch, int64_t jcol)
+{
+    unsigned long long *tt = (C.a.ttrace && jcol == C.a.tcol && C.tid == 0) ? C.a.ttrace : nullptr;
     const PanelArgs &a = C.a;
     PanelSmem &sm = C.sm;
-    double *Dsm = C.dyn;             // TB x TB: M_b (safe) or D (unsafe)
-    double *accg = C.dyn + TB * TB;  // 4 x TB
+    double *Dsm = C.dyn;             // TB x TB: Bt_{b,b+1} (safe) or D (unsafe)
+    double *accg = C.dyn + TB * TB;  // 4 x TB (reused as 8 x 64 pairs)
     const int64_t n = C.n, p0 = C.p0, M = C.M;
     const int Nb = (int)((M + TB - 1) / TB);
     const int ri = C.tid & (TB - 1), grp = C.tid >> 7;  // 128 rows x 4 column groups
@@ -242,13 +302,24 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         const bool safe = a.dsafe[b] != 0;
         const bool last = (b == Nb - 1);
         const int hn = last ? 0 : (int)(n - (r0 + TB) < TB ? n - (r0 + TB) : TB);  // rows of block b+1
-        // (1) rhs part that does not depend on the solution, all 512 threads
+        const double *Bsrc = safe ? a.Bt : a.B;  // off-diagonal tiles
+        const int64_t ldsrc = safe ? a.ldbt : a.ldb;
+        // (1) rhs_b (all loads of a thread first)
         {
             const int64_t r = r0 + ri;
             double u = 0.0;
             if (ri < h) {
-#pragma unroll 4
-                for (int c = grp; c < k; c += 4) u += a.U[(size_t)c * n + r] * z2[c];
+                double uv[8], zv[8];
+                for (int c0 = grp; c0 < k; c0 += 32) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int c = c0 + 4 * q;
+                        uv[q] = (c < k) ? a.U[(size_t)c * n + r] : 0.0;
+                        zv[q] = (c < k) ? z2[c] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) u = fma(uv[q], zv[q], u);
+                }
             }
             accg[grp * TB + ri] = u;
             __syncthreads();
@@ -263,12 +334,38 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             }
             __syncthreads();
         }
-        // (2) stage M_b (safe) or D (unsafe) in shared memory
+        // (2) stage Bt_{b,b+1} (safe) or D (unsafe) in shared memory; c_b = Dinv_b rhs_b (safe)
         if (safe) {
             if (!last) {
-                const double *src = a.Mb + (size_t)b * TB * TB;
-                for (int idx = C.tid; idx < TB * TB; idx += PNT) Dsm[idx] = src[idx];
+                const double *src = a.Bt + (size_t)(r0 + TB) * a.ldbt + r0;
+                for (int l0 = 0; l0 < TB; l0 += 32) {  // 32 columns per round, 8 loads per thread
+                    double t[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int idx = C.tid + q * PNT, l = l0 + idx / TB, i = idx % TB;
+                        t[q] = (l < hn && i < h) ? src[(size_t)l * a.ldbt + i] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int idx = C.tid + q * PNT;
+                        Dsm[(l0 + idx / TB) * TB + idx % TB] = t[q];
+                    }
+                }
             }
+            const double *Di = a.Dinv + (size_t)b * TB * TB;
+            double s = 0.0;
+            double dv[8];
+            for (int l0 = grp; l0 < TB; l0 += 32) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dv[q] = Di[(l0 + 4 * q) * TB + ri];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s = fma(dv[q], sm.rhs[l0 + 4 * q], s);
+            }
+            accg[grp * TB + ri] = s;
+            __syncthreads();
+            if (C.tid < TB)
+                sm.cbv[C.tid] = (accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]);
+            __syncthreads();
         } else {
             for (int idx = C.tid; idx < TB * TB; idx += PNT) {
                 int i = idx & (TB - 1), j = idx >> 7;
@@ -276,7 +373,7 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             }
         }
         // (3) off-diagonal tiles c > b+1 (safe) or c > b (unsafe), as their solutions arrive
-        double acc = 0.0;
+        double acc0 = 0.0, acc1 = 0.0;
         int Eacc = 0;
         const int cstop = safe ? b + 1 : b;
         for (int cb = Nb - 1; cb > cstop; --cb) {
@@ -284,77 +381,75 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             const int w = (int)(n - c0 < TB ? n - c0 : TB);
             const int ecb = wait_block(C, cb, epoch, cb & 1);
             if (ecb > Eacc) {
-                acc = ldexp(acc, Eacc - ecb);
+                acc0 *= pow2i(Eacc - ecb);
+                acc1 *= pow2i(Eacc - ecb);
                 Eacc = ecb;
             }
-            if (ri < h) {
-                const double *bp = a.B + (size_t)c0 * a.ldb + r0 + ri;
-                const double *yp = a.vy + c0;
-                double s0 = 0.0, s1 = 0.0;
-                int cc = grp;
-#pragma unroll 4
-                for (; cc + 4 < w; cc += 8) {
-                    s0 += bp[(size_t)cc * a.ldb] * __ldcg(yp + cc);
-                    s1 += bp[(size_t)(cc + 4) * a.ldb] * __ldcg(yp + cc + 4);
-                }
-                for (; cc < w; cc += 4) s0 += bp[(size_t)cc * a.ldb] * __ldcg(yp + cc);
-                acc += (s0 + s1) * ldexp(1.0, ecb - Eacc);
+            if (cb - 1 > cstop && C.tid < TB) {  // pull the next tile into L2 while this one is consumed
+                const double *nt = Bsrc + (size_t)(c0 - TB) * ldsrc + r0;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(nt + (size_t)C.tid * ldsrc));
+                if (h > 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(nt + (size_t)C.tid * ldsrc + 64));
             }
+            double t0 = 0.0, t1 = 0.0;
+            tile_mv(Bsrc + (size_t)c0 * ldsrc + r0, ldsrc, a.vy + c0, w, h, C.tid, t0, t1);
+            const double sc = pow2i(ecb - Eacc);
+            acc0 = fma(t0, sc, acc0);
+            acc1 = fma(t1, sc, acc1);
         }
-        accg[grp * TB + ri] = acc;
+        if (tt) tt[4 * b + 0] = gtime();
+        {   // fold the 8 column groups: rows 2rp, 2rp+1
+            const int rp = C.tid & 63, g8 = C.tid >> 6;
+            accg[g8 * TB + 2 * rp] = acc0;
+            accg[g8 * TB + 2 * rp + 1] = acc1;
+        }
         __syncthreads();
+        double s8 = 0.0;
         if (C.tid < TB) {
-            double rv = 0.0;
-            if (C.tid < h) {
-                double s = accg[C.tid] + accg[TB + C.tid] + accg[2 * TB + C.tid] + accg[3 * TB + C.tid];
-                rv = ldexp(sm.rhs[C.tid], -Eacc) - s;
-            }
-            sm.rhs[C.tid] = rv;
+#pragma unroll
+            for (int g8 = 0; g8 < 8; ++g8) s8 += accg[g8 * TB + C.tid];
         }
         __syncthreads();
         int e = Eacc;
         if (safe) {
-            // (4) c_b = Dinv_b * t   (Dinv from global; off the critical path)
-            {
-                const double *Di = a.Dinv + (size_t)b * TB * TB;
-                double s = 0.0;
-#pragma unroll 8
-                for (int l = grp; l < TB; l += 4) s += Di[l * TB + ri] * sm.rhs[l];
-                accg[grp * TB + ri] = s;
-                __syncthreads();
-                if (C.tid < TB)
-                    sm.cbv[C.tid] = (accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]);
-                __syncthreads();
-            }
-            // (5) critical path: y~_b = c_b 2^(Eacc-E) - M_b y~_{b+1} 2^(e1-E)
+            // (4) critical path: y~_b = c_b 2^(-E) - acc 2^(Eacc-E) - Bt_{b,b+1} y~_{b+1} 2^(e1-E)
             double xv = 0.0;
             if (!last) {
                 const int e1 = wait_block(C, b + 1, epoch, 2);
-                const int E = e1 > Eacc ? e1 : Eacc;
-                const double *yp = a.vy + r0 + TB;
-                double s = 0.0;
-#pragma unroll 8
-                for (int l = grp; l < TB; l += 4) s += (l < hn ? Dsm[l * TB + ri] * __ldcg(yp + l) : 0.0);
-                accg[grp * TB + ri] = s;
+                if (tt) tt[4 * b + 1] = gtime();
+                if (C.tid < TB) sm.rhs[C.tid] = (C.tid < hn) ? __ldcg(a.vy + r0 + TB + C.tid) : 0.0;
                 __syncthreads();
+                double sa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int l = grp; l < TB; l += 16)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) sa[u] = fma(Dsm[(l + 4 * u) * TB + ri], sm.rhs[l + 4 * u], sa[u]);
+                accg[grp * TB + ri] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+                __syncthreads();
+                const int E = max(e1, Eacc);
                 if (C.tid < TB)
-                    xv = ldexp(sm.cbv[C.tid], Eacc - E) -
-                         ldexp((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]), e1 - E);
+                    xv = sm.cbv[C.tid] * pow2i(-E) - s8 * pow2i(Eacc - E) -
+                         ((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid])) * pow2i(e1 - E);
                 e = E;
             } else if (C.tid < TB) {
-                xv = sm.cbv[C.tid];
+                xv = sm.cbv[C.tid] * pow2i(-Eacc) - s8;
             }
-            // (6) post-hoc power-of-two rescale if the block solution is too large
-            double mx = (C.tid < h) ? fabs(xv) : 0.0;
-            mx = warp_max(mx);
-            if (C.tid < TB && C.lane == 0) sm.red[C.warp] = mx;
-            __syncthreads();
-            mx = fmax(fmax(sm.red[0], sm.red[1]), fmax(sm.red[2], sm.red[3]));
+            // (5) post-hoc power-of-two rescale, only if some entry of the block is too large
+            const bool big = (C.tid < h) && !(fabs(xv) <= BIG);
             int ex = 0;
-            if (!(mx <= BIG)) frexp(mx, &ex);
-            if (C.tid < h) a.vy[r0 + C.tid] = ldexp(xv, -ex);
+            if (__syncthreads_or(big)) {
+                double mx = (C.tid < h) ? fabs(xv) : 0.0;
+                mx = warp_max(mx);
+                if (C.tid < TB && C.lane == 0) sm.red[C.warp] = mx;
+                __syncthreads();
+                mx = fmax(fmax(sm.red[0], sm.red[1]), fmax(sm.red[2], sm.red[3]));
+                if (!(mx <= BIG)) frexp(mx, &ex);
+                if (!isfinite(mx)) ex = 0;
+            }
+            if (C.tid < h) a.vy[r0 + C.tid] = ex ? ldexp(xv, -ex) : xv;
             e += ex;
         } else {
+            if (C.tid < TB) sm.rhs[C.tid] = (C.tid < h) ? ldexp(sm.rhs[C.tid], -Eacc) - s8 : 0.0;
+            __syncthreads();
             if (C.warp == 0) {
                 // overflow-safe sequential back-substitution (unsafe block, e.g. config 4)
                 const int l = C.lane;
@@ -401,6 +496,7 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         if (C.tid == 0) {
             a.bexp[b] = e;
             st_release64(&a.flags[b], ((unsigned long long)epoch << 32) | (unsigned)e);
+            if (tt) tt[4 * b + 2] = gtime();
         }
     }
     __syncthreads();
@@ -411,8 +507,16 @@ __device__ int trsv_emax(Ctx &C)
 {
     const int Nb = (int)((C.M + TB - 1) / TB);
     int e = INT_MIN;
-    for (int b = 0; b < Nb; ++b) e = max(e, __ldcg(&C.a.bexp[b]));
-    return e;
+    for (int b = C.tid; b < Nb; b += PNT) e = max(e, __ldcg(&C.a.bexp[b]));  // all loads in parallel
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (C.lane == 0) C.sm.ival[C.warp & 3] = INT_MIN;
+    __syncthreads();
+    if (C.lane == 0) atomicMax(&C.sm.ival[0], e);
+    __syncthreads();
+    const int r = C.sm.ival[0];
+    __syncthreads();
+    return r;
 }
 
 // Row-slab sweep  out(r) = sum_{c in [cbeg, n)} X(r,c) vec(c)  over rows [r0, r1)
@@ -481,6 +585,143 @@ __device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int
     }
 }
 
+// Tiled mat-vec  y = X(r_beg:r_end, c_beg:c_end) * vf  (TRI: only entries with c >= r,
+// i.e. an upper-triangular X), HBM-bound.  The matrix is cut into 256 x 256 items that
+// are dealt round-robin to the CTAs; inside an item every warp streams 16 columns with
+// 16-byte loads over all 256 rows (16 independent loads in flight per lane), so each
+// SM keeps ~128 KB of loads outstanding.  Item partial sums go to ypart[cc][r]
+// (cc = column chunk) and are added in a fixed order by tiled_sum() after a grid sync
+// (deterministic).
+constexpr int TRT = 256, TCW = 256;
+struct TileGeom {
+    int64_t r_al, r_end, c_beg, c_end;
+    int nrb, ncc;
+    bool tri;
+    __device__ TileGeom(int64_t rb_, int64_t re_, int64_t cb_, int64_t ce_, bool t)
+        : r_al(rb_ & ~(int64_t)1), r_end(re_), c_beg(cb_), c_end(ce_), tri(t)
+    {
+        nrb = (int)((r_end - r_al + TRT - 1) / TRT);
+        ncc = (int)((c_end - c_beg + TCW - 1) / TCW);
+    }
+    // first column chunk that meets row block rb (TRI), else 0
+    __device__ int cc_min(int rb) const
+    {
+        if (!tri) return 0;
+        const int64_t d = r_al + (int64_t)TRT * rb - c_beg;
+        return d <= 0 ? 0 : (int)(d / TCW);
+    }
+    __device__ int items() const
+    {
+        if (!tri) return nrb * ncc;
+        int t = 0;
+        for (int rb = 0; rb < nrb; ++rb) t += ncc - cc_min(rb);
+        return t;
+    }
+    __device__ void item(int i, int &rb, int &cc) const
+    {
+        if (!tri) { rb = i / ncc; cc = i % ncc; return; }
+        for (rb = 0; rb < nrb; ++rb) {
+            const int m = ncc - cc_min(rb);
+            if (i < m) { cc = cc_min(rb) + i; return; }
+            i -= m;
+        }
+    }
+};
+
+template <class VF>
+__device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf)
+{
+    double *red = C.dyn;               // [NWP][TRT]
+    double *vs = C.dyn + NWP * TRT;    // [TCW]
+    const bool vec = (ldx % 2) == 0;
+    const int nit = tg.items();
+    for (int it = C.bid; it < nit; it += C.G) {
+        int rb, cc;
+        tg.item(it, rb, cc);
+        const int64_t r0 = tg.r_al + (int64_t)TRT * rb, c0 = tg.c_beg + (int64_t)TCW * cc;
+        __syncthreads();
+        if (C.tid < TCW) {
+            const int64_t c = c0 + C.tid;
+            vs[C.tid] = (c < tg.c_end) ? vf(c) : 0.0;
+        }
+        __syncthreads();
+        double acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+        const int cw0 = C.warp * (TCW / NWP);  // 16 columns per warp
+        const bool diag = tg.tri && (r0 + TRT - 1 > c0);
+        const bool full = (r0 + TRT <= tg.r_end);
+        if (vec && full && !diag) {
+#pragma unroll 1
+            for (int u0 = 0; u0 < TCW / NWP; u0 += 4) {
+                double2 xv[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t c = c0 + cw0 + u0 + u;
+                    const double2 *col = reinterpret_cast<const double2 *>(X + (size_t)(c < tg.c_end ? c : c0) * ldx + r0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[u][i] = col[C.lane + 32 * i];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double v = vs[cw0 + u0 + u];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        acc[2 * i] = fma(xv[u][i].x, v, acc[2 * i]);
+                        acc[2 * i + 1] = fma(xv[u][i].y, v, acc[2 * i + 1]);
+                    }
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int u0 = 0; u0 < TCW / NWP; u0 += 2) {
+                double xv[2][8];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int64_t c = c0 + cw0 + u0 + u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int64_t r = r0 + 2 * C.lane + 64 * i + h;
+                            const bool ok = c < tg.c_end && r < tg.r_end && (!tg.tri || c >= r);
+                            xv[u][2 * i + h] = ok ? X[(size_t)c * ldx + r] : 0.0;
+                        }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const double v = vs[cw0 + u0 + u];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) acc[q] = fma(xv[u][q], v, acc[q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            red[C.warp * TRT + 2 * C.lane + 64 * i] = acc[2 * i];
+            red[C.warp * TRT + 2 * C.lane + 64 * i + 1] = acc[2 * i + 1];
+        }
+        __syncthreads();
+        if (C.tid < TRT) {
+            const int64_t r = r0 + C.tid;
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWP; ++w) t += red[w * TRT + C.tid];
+            if (r < tg.r_end) C.a.ypart[(size_t)cc * C.n + r] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// y(r) = sum of the item partials of row r (after a grid sync), fixed order.
+__device__ __forceinline__ double tiled_sum(const Ctx &C, const TileGeom &tg, int64_t r)
+{
+    const int rb = (int)((r - tg.r_al) / TRT);
+    double t = 0.0;
+    for (int cc = tg.cc_min(rb); cc < tg.ncc; ++cc) t += __ldcg(C.a.ypart + (size_t)cc * C.n + r);
+    return t;
+}
+
 __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -495,18 +736,6 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
     int k = 0, failed = 0;
     long long ir_steps = 0, ir_cols = 0, rescales = 0;
     int ffi = 0;  // cursor into the forced-failure list
-    // area-balanced row slabs of the trailing triangle (B w)
-    int64_t tr0, tr1;
-    {
-        double f0 = 1.0 - (double)C.bid / C.G, f1 = 1.0 - (double)(C.bid + 1) / C.G;
-        tr0 = n - (int64_t)llround((double)C.M * sqrt(f0));
-        tr1 = n - (int64_t)llround((double)C.M * sqrt(f1 > 0.0 ? f1 : 0.0));
-        if (C.bid == 0) tr0 = p0;
-        if (C.bid == C.G - 1) tr1 = n;
-        if (tr0 < p0) tr0 = p0;
-        if (tr1 > n) tr1 = n;
-    }
-
     const bool prof = a.ptime && C.bid == 0 && C.tid == 0;
     unsigned long long tp = prof ? gtime() : 0ull;
     auto mark = [&](int bin) {
@@ -595,7 +824,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         __syncthreads();
         C.trimv<false>(Sget, ku, sm.sv1, sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
-        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, sm.sv3, epoch);
+        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, sm.sv3, epoch, j0);
         grid.sync();
         mark(1);
         int emax = trsv_emax(C);
@@ -662,14 +891,18 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             // w2 = B w over area-balanced slabs, + partial U^T w2
             C.ph++;
             mark(6);
-            slab_sweep<true>(C, a.B, a.ldb, tr0, tr1, 0, [&](int64_t c) { return __ldcg(&a.vw[c]); }, a.vw2);
+            const TileGeom tgb(p0, n, p0, n, true);
+            tiled_matvec(C, tgb, a.B, a.ldb, [&](int64_t c) { return __ldcg(&a.vw[c]); });
+            grid.sync();
             {
+                for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tgb, C.rb0 + rl);
+                __syncthreads();
                 double *out = C.mypart();
                 double *stg = dyn;
                 for (int c = C.warp; c < ku; c += NWP) {
                     double s = 0.0;
 #pragma unroll 4
-                    for (int64_t r = tr0 + C.lane; r < tr1; r += 32) s += U[(size_t)c * n + r] * a.vw2[r];
+                    for (int64_t r = C.rb0 + C.lane; r < C.rb1; r += 32) s += U[(size_t)c * n + r] * a.vw2[r];
                     stg[c * 33 + C.lane] = s;
                 }
                 __syncthreads();
@@ -725,7 +958,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
             trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
-                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, sm.sv3, epoch);
+                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, sm.sv3, epoch, -1);
             grid.sync();
             const int ec = trsv_emax(C);
             if (ec > 0) { ++rescales; break; }  // a rescaled correction counts as IR failure
@@ -799,10 +1032,13 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         }
         __syncthreads();
         C.coltdot(V, n, k, 0);
-        // A(p0:n, j0+1:n) v over own rows
-        slab_sweep<false>(C, A, lda, C.rb0, C.rb1, j0 + 1, vget, a.vw2);
+        // A(p0:n, j0+1:n) v  (tiled, partials in ypart)
+        const TileGeom tga(p0, n, j0 + 1, n, false);
+        tiled_matvec(C, tga, A, lda, vget);
         grid.sync();
         mark(4);
+        for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tga, C.rb0 + rl);
+        __syncthreads();
         C.gather(sm.sv1, k, 0);  // z = V^T v
         __syncthreads();
         if (C.bid == 0) {
@@ -906,17 +1142,16 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb = (int)((M + TB - 1) / TB);
     inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
     HT_CUDA_TRY(cudaGetLastError());
-    // M_b = Dinv_b * B(block b, block b+1) for the look-ahead solve
+    // Bt(block b, blocks > b) = Dinv_b * B(block b, blocks > b): pre-scaled block rows
     if (Nb > 1) {
-        GemmBatchItem it[1024];
-        int cnt = 0;
-        for (int b = 0; b + 1 < Nb && cnt < 1024; ++b) {
+        std::vector<GemmBatchItem> it;
+        for (int b = 0; b + 1 < Nb; ++b) {
             const int64_t r0 = a->s0 + 1 + (int64_t)b * TB, c0 = r0 + TB;
-            const int w = (int)(a->n - c0 < TB ? a->n - c0 : TB);
-            it[cnt++] = GemmBatchItem{a->Dinv + (size_t)b * TB * TB, a->B + r0 + c0 * a->ldb, a->Mb + (size_t)b * TB * TB,
-                                      TB, a->ldb, TB, TB, w, TB, 1.0, 0.0, 0.0};
+            const int w = (int)(a->n - c0);
+            it.push_back(GemmBatchItem{a->Dinv + (size_t)b * TB * TB, a->B + r0 + c0 * a->ldb, a->Bt + r0 + c0 * a->ldbt,
+                                       TB, a->ldb, a->ldbt, TB, w, TB, 1.0, 0.0, 0.0});
         }
-        int rc = ht_gemm_multi(st, 'N', 'N', it, cnt);
+        int rc = ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size());
         if (rc) return rc;
     }
     void *args[] = {(void *)a};
