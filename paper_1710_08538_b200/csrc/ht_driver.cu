@@ -49,6 +49,10 @@ struct Work {
     double *VW = nullptr, *UW = nullptr;
     double *Vhat = nullptr, *tau = nullptr, *Gm = nullptr, *Tm = nullptr, *Wt = nullptr, *Qw = nullptr;
     double *tmp = nullptr, *W1 = nullptr, *W2 = nullptr, *UR = nullptr, *fscr = nullptr;
+    // second window store for the U2 staircase (L1), factored on side_stream concurrently
+    double *VhatL = nullptr, *QwL = nullptr, *TmL = nullptr, *tauL = nullptr, *WtL = nullptr, *fscrL = nullptr;
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
@@ -113,7 +117,8 @@ struct Timer {
 void work_free(Work &w)
 {
     double **dp[] = {&w.U, &w.V, &w.Y, &w.S, &w.T, &w.vec, &w.part, &w.VW, &w.UW, &w.Vhat, &w.tau,
-                     &w.Gm, &w.Tm, &w.Wt, &w.Qw, &w.tmp, &w.W1, &w.W2, &w.UR, &w.fscr, &w.d_scal};
+                     &w.Gm, &w.Tm, &w.Wt, &w.Qw, &w.tmp, &w.W1, &w.W2, &w.UR, &w.fscr, &w.d_scal,
+                     &w.VhatL, &w.QwL, &w.TmL, &w.tauL, &w.WtL, &w.fscrL};
     for (auto p : dp)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (w.flags) cudaFree(w.flags);
@@ -193,6 +198,13 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.W1, nnb + 4 * nb2)); TRY(dalloc(&w.W2, nnb + 4 * nb2));
     TRY(dalloc(&w.UR, 2 * nb2));
     TRY(dalloc(&w.fscr, 4 * nb2 + 16384 + 64));
+    TRY(dalloc(&w.VhatL, 2 * nnb + 4 * nb2)); TRY(dalloc(&w.WtL, 2 * nnb + 4 * nb2));
+    TRY(dalloc(&w.QwL, 4 * nnb + 8 * nb2)); TRY(dalloc(&w.TmL, nnb + 2 * nb2));
+    TRY(dalloc(&w.tauL, (size_t)N + 2 * NB)); TRY(dalloc(&w.fscrL, 4 * nb2 + 16384 + 64));
+    if (!w.side_stream && cudaStreamCreateWithFlags(&w.side_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return HT_ECUDA;
+    if (!w.ev_fork && cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
+    if (!w.ev_join && cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
@@ -234,12 +246,12 @@ struct Run {
         tm.end(st);
         return rc;
     }
-    int gemm_multi(char ta, char tb, const std::vector<GemmBatchItem> &it)
+    int gemm_multi_on(cudaStream_t s, char ta, char tb, const std::vector<GemmBatchItem> &it)
     {
         if (it.empty()) return 0;
-        tm.begin(st, 1, (int)((it.size() + 15) / 16));
-        int rc = ht_gemm_multi(st, ta, tb, it.data(), (int)it.size());
-        tm.end(st);
+        tm.begin(s, 1, (int)((it.size() + 15) / 16));
+        int rc = ht_gemm_multi(s, ta, tb, it.data(), (int)it.size());
+        tm.end(s);
         return rc;
     }
     int copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd)
@@ -278,65 +290,75 @@ struct Run {
         return 0;
     }
 
-    // Window bookkeeping for one chain: packed offsets into Vhat/Qw/Gm/Tm/tau.
+    // Window bookkeeping for one chain: packed offsets into a window store.
     struct Win {
         int p, q;
         size_t ov, oq, og, ot;
     };
-    std::vector<Win> wins;
+    struct Store {  // V-hat, explicit Q-hat, T, tau, V T, factor scratch
+        double *Vhat, *Qw, *Tm, *tau, *Wt, *fscr;
+    };
+    Store main_store() const { return Store{w->Vhat, w->Qw, w->Tm, w->tau, w->Wt, w->fscr}; }
+    Store side_store() const { return Store{w->VhatL, w->QwL, w->TmL, w->tauL, w->WtL, w->fscrL}; }
+    std::vector<Win> wins, winsL;
     void wins_reset() { wins.clear(); }
-    Win add_win(int p, int q)
+    static Win add_win(std::vector<Win> &ws, int p, int q)
     {
         Win x{p, q, 0, 0, 0, 0};
-        if (!wins.empty()) {
-            const Win &b = wins.back();
+        if (!ws.empty()) {
+            const Win &b = ws.back();
             x.ov = b.ov + (size_t)b.p * b.q;
             x.oq = b.oq + (size_t)b.p * b.p;
             x.og = b.og + (size_t)b.q * b.q;
             x.ot = b.ot + (size_t)b.q;
         }
-        wins.push_back(x);
+        ws.push_back(x);
         return x;
     }
+    Win add_win(int p, int q) { return add_win(wins, p, q); }
 
-    // Factor windows [i0, i1) of `wins` (descs in h_fd at fd_cur..), then form Qw for them.
-    int factor_and_form(const std::vector<FactorDesc> &fds, size_t i0)
+    // Factor the windows `ws` (descriptors `fds`, one per window) on stream `s` with the
+    // window store `sto`, then form Qw = I - V T V^T for each.
+    int factor_and_form(const std::vector<FactorDesc> &fds, const std::vector<Win> &ws, const Store &sto,
+                        cudaStream_t s)
     {
         const int nd = (int)fds.size();
         if (nd == 0) return 0;
-        if (w->fd_cur + nd > w->ndesc || w->ld_cur + nd > w->ndesc) return HT_ENUMERIC;
+        if (w->fd_cur + nd > w->ndesc) return HT_ENUMERIC;
         FactorDesc *hf = w->h_fd + w->fd_cur;
         int maxp = 0;
         for (int i = 0; i < nd; ++i) {
-            const Win &x = wins[i0 + i];
+            const Win &x = ws[i];
             hf[i] = fds[i];
-            hf[i].T = w->Tm + x.og;  // q x q compact-WY T, formed inside the factor kernel
+            hf[i].T = sto.Tm + x.og;  // q x q compact-WY T, formed inside the factor kernel
             hf[i].ldt = x.q;
             maxp = std::max(maxp, fds[i].p);
             extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
         }
-        HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, st));
-        tm.begin(st, 2);
-        TRY(ht_factor_run(st, w->d_fd + w->fd_cur, nd, w->fscr, maxp));
-        tm.end(st);
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
+        tm.begin(s, 2);
+        TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
+        tm.end(s);
         std::vector<GemmBatchItem> it(nd);
         // Wt = V T
         for (int i = 0; i < nd; ++i) {
-            const Win &x = wins[i0 + i];
-            it[i] = GemmBatchItem{w->Vhat + x.ov, w->Tm + x.og, w->Wt + x.ov, x.p, x.q, x.p,
-                                  x.p, x.q, x.q, 1.0, 0.0, 0.0};
+            const Win &x = ws[i];
+            it[i] = GemmBatchItem{sto.Vhat + x.ov, sto.Tm + x.og, sto.Wt + x.ov, x.p, x.q, x.p, x.p, x.q, x.q, 1.0, 0.0, 0.0};
         }
-        TRY(gemm_multi('N', 'N', it));
+        TRY(gemm_multi_on(s, 'N', 'N', it));
         // Qw = I - Wt V^T
         for (int i = 0; i < nd; ++i) {
-            const Win &x = wins[i0 + i];
-            it[i] = GemmBatchItem{w->Wt + x.ov, w->Vhat + x.ov, w->Qw + x.oq, x.p, x.p, x.p,
-                                  x.p, x.p, x.q, -1.0, 0.0, 1.0};
+            const Win &x = ws[i];
+            it[i] = GemmBatchItem{sto.Wt + x.ov, sto.Vhat + x.ov, sto.Qw + x.oq, x.p, x.p, x.p, x.p, x.p, x.q, -1.0, 0.0, 1.0};
         }
-        TRY(gemm_multi('N', 'T', it));
+        TRY(gemm_multi_on(s, 'N', 'T', it));
         w->fd_cur += nd;
-        w->ld_cur += nd;
         return 0;
+    }
+    int factor_and_form(const std::vector<FactorDesc> &fds, size_t i0)
+    {
+        std::vector<Win> ws(wins.begin() + i0, wins.begin() + i0 + fds.size());
+        return factor_and_form(fds, ws, main_store(), st);
     }
 
     // Chained window applies (ht_chain.cu): every matrix in `mats` takes the windows of
@@ -388,6 +410,24 @@ struct Run {
         TRY(copy2d(m, k, V + J + 1, n, w->VW, ldw));
         TRY(copy2d(m, k, U + J + 1, n, w->UW, ldw));
         const int K = (int)k;
+
+        // ===== L1: QR staircase of U2, bottom -> top (sec. 3.3.2b) =====
+        // It depends only on U2, so it is factored on the side stream while R1-R3 run.
+        winsL.clear();
+        {
+            std::vector<FactorDesc> fl;
+            const Store sl = side_store();
+            for (int i = 0; i < r; ++i) {
+                const int64_t top = lb[r - 1 - i], bot = lb[r + 1 - i];
+                const int p = (int)(bot - top);
+                Win x = add_win(winsL, p, K);
+                fl.push_back(FactorDesc{w->UW + top, 1, ldw, p, K, 0, sl.Vhat + x.ov, p, sl.tau + x.ot});
+            }
+            HT_CUDA_TRY(cudaEventRecord(w->ev_fork, st));
+            HT_CUDA_TRY(cudaStreamWaitEvent(w->side_stream, w->ev_fork, 0));
+            TRY(factor_and_form(fl, winsL, sl, w->side_stream));
+            HT_CUDA_TRY(cudaEventRecord(w->ev_join, w->side_stream));
+        }
 
         // ===== R1: QL staircase of V2, top -> bottom (sec. 3.3.1b) =====
         wins_reset();
@@ -451,16 +491,7 @@ struct Run {
             if (wz) mats.push_back(ChainMat{Z, ldz, 0, 0, n});
             TRY(chain(mats, {ChainWin{w->Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}}}));
         }
-        // ===== L1: QR staircase of U2, bottom -> top (sec. 3.3.2b) =====
-        wins_reset();
-        fds.clear();
-        for (int i = 0; i < r; ++i) {
-            const int64_t top = lb[r - 1 - i], bot = lb[r + 1 - i];
-            const int p = (int)(bot - top);
-            Win x = add_win(p, K);
-            fds.push_back(FactorDesc{w->UW + top, 1, ldw, p, K, 0, w->Vhat + x.ov, p, w->tau + x.ot});
-        }
-        TRY(factor_and_form(fds, 0));
+        HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
         // ===== L2: spike, chain on B, A, Q, W-updates =====
         TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
@@ -469,9 +500,9 @@ struct Run {
         {
             std::vector<ChainWin> wl;
             for (int i = 0; i < r; ++i) {
-                const Win &x = wins[i];
+                const Win &x = winsL[i];
                 const int64_t R0 = J + 1 + lb[r - 1 - i];
-                wl.push_back(ChainWin{w->Qw + x.oq, R0, x.p, {R0, J, 0}, {n, n, n}});
+                wl.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, J, 0}, {n, n, n}});
             }
             std::vector<ChainMat> mats{ChainMat{B, ldb, 1, J + 1, n}, ChainMat{A, lda, 1, J, n}};
             if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});

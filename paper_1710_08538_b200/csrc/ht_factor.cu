@@ -98,7 +98,7 @@ struct FactorSmem {
     static constexpr int RC = MAXP < VRC ? MAXP : VRC;
     static constexpr int LDV = RC + 4;                         // == 4 mod 32
     static constexpr int VSZ = (PBW * LDV > FNW * LW * PBW) ? PBW * LDV : FNW * LW * PBW;
-    static constexpr int DOUBLES = PBW * LDP + VSZ + PBW * LDX + PBW * LDT + 2 * FNW * LW + 2 * LW + PBW + 2 * 64;
+    static constexpr int DOUBLES = PBW * LDP + VSZ + PBW * LDX + PBW * LDT + 2 * FNW * LW + 2 * LW + PBW + 2 * 64 + 4 * LW;
 };
 
 // Vs[c][rr] = V(r0 + rr, col0 + c) (view row order), rr < RC, zero beyond `rows`.
@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
     double *taus = rowc + 2 * LW;             // [PBW]
     double *Zl = taus + PBW;                  // [LW][LW] leaf Z
     double *Tl = Zl + 64;                     // [LW][LW] leaf T
+    double *coef = Tl + 64;                   // [2][2][LW] column-step update coefficients
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int c8 = lane & 7, rq = lane >> 3;    // leaf column / row group of this lane
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = o1;
                 }
                 __syncthreads();
+                FPROF(8);
                 // X <- T_i^T X  (T_i upper triangular): X'(a, c) = sum_{l <= a} T(l, a) X(l, c)
                 double xv[2];
                 for (int e = 0; e < 2; ++e) {
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     Xs[a * LDX + c] = -xv[e];
                 }
                 __syncthreads();
+                FPROF(9);
                 // P -= V_i X : per chunk, warp w owns row tiles {2w, 2w+1} x 4 column tiles
                 for (int r0 = r_lo; r0 < p; r0 += L::RC) {
                     const int rows = min(L::RC, p - r0);
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 }
             }
             __syncthreads();
-            FPROF(1);
+            FPROF(10);
             // ---- the panel in registers: val[l][e] = P(rw0 + e, 8l + c8) ----
             double val[NLF][RPT];
 #pragma unroll
@@ -298,13 +301,19 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 if (jbeg >= nc) break;
                 const int jend = min(nc, jbeg + LW);
                 // -------- column steps inside the leaf --------
+                // A (all warps): partial dot products of the pivot column with the leaf's
+                //   columns over own rows -> part;  B (warp 0, lanes = columns): sums, the
+                //   reflector scalars and per-column update coefficients -> coef;
+                //   C (all warps): rank-1 update of own rows.  Two barriers per column.
                 for (int jj = jbeg; jj < jend; ++jj) {
+                    const bool cp = fprof && lane == 0 && (warp == 0 || warp == FNW - 1);
+                    const int cpo = 12 + (warp == 0 ? 0 : 5);
+                    long long ck0 = cp ? clock64() : 0;
                     const int jc = jj - jbeg;
                     const int dr = c0 + jj;                             // diagonal row of this column
                     const bool active = warp * 4 * RPT + 4 * RPT > dr;  // warp-uniform: rows >= dr here
                     const int src = (rq << 3) | jc;
                     double xr[RPT];
-                    double s = 0.0;
                     if (active) {
                         double sa[2] = {0.0, 0.0};
 #pragma unroll
@@ -313,45 +322,67 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                             const double vm = (rw0 + e > dr) ? val[lf][e] : 0.0;
                             sa[e & 1] = fma(vm, xr[e], sa[e & 1]);
                         }
-                        s = sa[0] + sa[1];
+                        double s = sa[0] + sa[1];
                         s += __shfl_xor_sync(0xffffffffu, s, 8);
                         s += __shfl_xor_sync(0xffffffffu, s, 16);
+                        if (rq == 0) part[(buf * FNW + warp) * LW + c8] = s;
+                    } else if (rq == 0) {
+                        part[(buf * FNW + warp) * LW + c8] = 0.0;
                     }
-                    if (rq == 0) part[(buf * FNW + warp) * LW + c8] = s;
                     if (dr >= rw0 && dr < rw0 + RPT) {  // this thread holds row dr
 #pragma unroll
                         for (int e = 0; e < RPT; ++e)
                             if (rw0 + e == dr) rowc[buf * LW + c8] = val[lf][e];
                     }
+                    long long ck1 = cp ? clock64() : 0;
                     __syncthreads();
-                    double pr[FNW];
+                    long long ck2 = cp ? clock64() : 0;
+                    if (warp == 0) {
+                        double pr[FNW];
 #pragma unroll
-                    for (int w = 0; w < FNW; ++w) pr[w] = part[(buf * FNW + w) * LW + c8];
+                        for (int w = 0; w < FNW; ++w) pr[w] = part[(buf * FNW + w) * LW + c8];
 #pragma unroll
-                    for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
+                        for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
 #pragma unroll
-                        for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
-                    const double S = pr[0];
-                    const double ss = __shfl_sync(0xffffffffu, S, jc);  // lane jc: column jj
-                    const double alpha = rowc[buf * LW + jc];
-                    double tau = 0.0, scal = 0.0, beta = alpha;
-                    if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
-                    const double myrow = rowc[buf * LW + c8];
-                    const double wj = tau * (myrow + scal * S);
-                    // rows > dr: val += mx * x  (lane jc: x = own value -> val = scal * x)
-                    const double mx = (c8 > jc) ? -wj * scal : (c8 == jc ? scal - 1.0 : 0.0);
+                            for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
+                        const double S = pr[0];
+                        const double ss = __shfl_sync(0xffffffffu, S, jc);  // lane jc: column jj
+                        const double alpha = rowc[buf * LW + jc];
+                        double tau = 0.0, scal = 0.0, beta = alpha;
+                        if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
+                        const double myrow = rowc[buf * LW + c8];
+                        const double wj = tau * (myrow + scal * S);
+                        if (lane < LW) {
+                            // rows > dr: val += mx * x  (column jc: x = own value -> val = scal * x)
+                            coef[(buf * 2) * LW + c8] = (c8 > jc) ? -wj * scal : (c8 == jc ? scal - 1.0 : 0.0);
+                            coef[(buf * 2 + 1) * LW + c8] = (c8 > jc) ? -wj : beta;  // row dr
+                            if (c8 < jc) Zl[c8 * LW + jc] = myrow + scal * S;  // Z(l, jj) = v_l^T v_jj
+                            if (c8 == jc) taus[jj] = tau;
+                        }
+                    }
+                    long long ck3 = cp ? clock64() : 0;
+                    __syncthreads();
+                    long long ck4 = cp ? clock64() : 0;
                     if (active) {
+                        const double mx = coef[(buf * 2) * LW + c8];
 #pragma unroll
                         for (int e = 0; e < RPT; ++e)
                             if (rw0 + e > dr) val[lf][e] = fma(mx, xr[e], val[lf][e]);
-                    }
-                    if (dr >= rw0 && dr < rw0 + RPT) {  // row dr: beta on the diagonal, -w_j to its right
+                        if (dr >= rw0 && dr < rw0 + RPT) {  // row dr: beta on the diagonal, -w_j to its right
+                            const double c2 = coef[(buf * 2 + 1) * LW + c8];
 #pragma unroll
-                        for (int e = 0; e < RPT; ++e)
-                            if (rw0 + e == dr) val[lf][e] = (c8 > jc) ? val[lf][e] - wj : (c8 == jc ? beta : val[lf][e]);
+                            for (int e = 0; e < RPT; ++e)
+                                if (rw0 + e == dr) val[lf][e] = (c8 > jc) ? val[lf][e] + c2 : (c8 == jc ? c2 : val[lf][e]);
+                        }
                     }
-                    if (tid == jc) taus[jj] = tau;
-                    if (tid < jc) Zl[tid * LW + jc] = myrow + scal * S;  // threads 0..7: c8 = tid
+                    if (cp) {
+                        long long ck5 = clock64();
+                        atomicAdd(&fprof[cpo + 0], (unsigned long long)(ck1 - ck0));
+                        atomicAdd(&fprof[cpo + 1], (unsigned long long)(ck2 - ck1));
+                        atomicAdd(&fprof[cpo + 2], (unsigned long long)(ck3 - ck2));
+                        atomicAdd(&fprof[cpo + 3], (unsigned long long)(ck4 - ck3));
+                        atomicAdd(&fprof[cpo + 4], (unsigned long long)(ck5 - ck4));
+                    }
                     buf ^= 1;
                 }
                 FPROF(2);
@@ -501,22 +532,29 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = x1 + y1;
             }
             __syncthreads();
+            FPROF(11);
             if (warp == 0) {
-                double *trow = Ts + lane * LDT;
+                // T_b by the dlarft forward recurrence, lane i = row i held in registers
+                // (T upper triangular: trow[l] = 0 for l < i, so the sums run over all l < c):
+                //   T(i,i) = tau_i,  T(i,c) = -tau_c sum_{l<c} T(i,l) G(l,c)   (G symmetric: G(c,l))
                 const int i = lane;
-                for (int c = 0; c < PBW; ++c) trow[c] = (c == i && i < nc) ? taus[i] : 0.0;
-                for (int c = i + 1; c < nc; ++c) {
-                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
-                    int l = i;
-                    for (; l + 4 <= c; l += 4) {
+                double trow[PBW];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) sa[u] = fma(trow[l + u], Xs[(l + u) * LDX + c], sa[u]);
-                    }
-                    for (; l < c; ++l) sa[0] = fma(trow[l], Xs[l * LDX + c], sa[0]);
-                    trow[c] = -taus[c] * ((sa[0] + sa[1]) + (sa[2] + sa[3]));
+                for (int c = 0; c < PBW; ++c) trow[c] = (c == i && i < nc) ? taus[i] : 0.0;
+#pragma unroll
+                for (int c = 1; c < PBW; ++c) {
+                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int l = 0; l < c; ++l) sa[l & 3] = fma(trow[l], Xs[c * LDX + l], sa[l & 3]);
+                    const double tv = -taus[c < nc ? c : 0] * ((sa[0] + sa[1]) + (sa[2] + sa[3]));
+                    if (c > i && c < nc) trow[c] = tv;
                 }
-                if (i < nc)
-                    for (int c = 0; c < nc; ++c) Tout(c0 + i, c0 + c) = trow[c];
+                if (i < nc) {
+                    // row i of T_b -> global T (columns c0..c0+nc) and the shared copy for the off-diagonal step
+#pragma unroll
+                    for (int c = 0; c < PBW; ++c)
+                        if (c < nc) Tout(c0 + i, c0 + c) = trow[c];
+                }
             }
             __threadfence_block();
             __syncthreads();

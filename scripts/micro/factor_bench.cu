@@ -29,7 +29,7 @@ int main(int argc, char **argv)
     else hd = FactorDesc{dW, 1, p, p, q, 0, dV, p, dtau, dT, q};
     FactorDesc *dd; cudaMalloc(&dd, sizeof(FactorDesc));
     cudaMemcpy(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice);
-    unsigned long long *dprof; cudaMalloc(&dprof, 16 * 8); cudaMemset(dprof, 0, 16 * 8);
+    unsigned long long *dprof; cudaMalloc(&dprof, 32 * 8); cudaMemset(dprof, 0, 32 * 8);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e30f;
     for (int it = 0; it < reps + 1; ++it) {
@@ -43,10 +43,13 @@ int main(int argc, char **argv)
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (it < reps) best = ms < best ? ms : best;
     }
-    unsigned long long hp[16]; cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost);
-    printf("p=%d q=%d rev=%d: best %.1f us | phases(us): load %.1f left %.1f leafsteps %.1f leafupd %.1f write %.1f GT %.1f offT %.1f zero %.1f\n",
-           p, q, rev, best * 1e3, hp[0] * 1e-3, hp[1] * 1e-3, hp[2] * 1e-3, hp[3] * 1e-3, hp[4] * 1e-3, hp[5] * 1e-3,
-           hp[6] * 1e-3, hp[7] * 1e-3);
+    unsigned long long hp[32]; cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost);
+    printf("column step cycles/col: warp0 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]  warp15 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]\n",
+           hp[12] / (double)q, hp[13] / (double)q, hp[14] / (double)q, hp[15] / (double)q, hp[16] / (double)q,
+           hp[17] / (double)q, hp[18] / (double)q, hp[19] / (double)q, hp[20] / (double)q, hp[21] / (double)q);
+    printf("p=%d q=%d rev=%d: best %.1f us | phases(us): load %.1f left[X %.1f TX %.1f upd %.1f] leafsteps %.1f leafupd %.1f write %.1f G %.1f T %.1f offT %.1f zero %.1f\n",
+           p, q, rev, best * 1e3, hp[0] * 1e-3, hp[8] * 1e-3, hp[9] * 1e-3, hp[10] * 1e-3, hp[2] * 1e-3, hp[3] * 1e-3, hp[4] * 1e-3,
+           hp[11] * 1e-3, hp[5] * 1e-3, hp[6] * 1e-3, hp[7] * 1e-3);
     // check: with the view W (p x q, view coordinates), Q = I - V T V^T (V in natural order);
     // natural-order window Wn0 = Q * Rn where Rn is the R written back through the view.
     std::vector<double> Wf(W0.size()), V((size_t)p * q), T((size_t)q * q);
