@@ -8,11 +8,12 @@ seed 2), with A, B restored from a pristine device copy at the start of each ste
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C] [--n N]
 
-N > 1 is launched with torch.distributed.run: every rank reduces its own pencil
-("replicas only", weak scaling; the sharded 1-D layout is DESIGN.md future work).
+N > 1 is launched with torch.distributed.run (one process per GPU, NCCL): all ranks
+reduce ONE pencil together (paper_1710_08538_b200/mg.py): A, B replicated, Q and Z split
+into row slabs and all-gathered at the end (strong scaling).
 Prints ONE JSON line on rank 0.  `value` is GFLOP/s counted with the fixed
 App.-A model flop count F_model(n, nb) (DESIGN.md), so both arms are comparable;
-`ms_per_step` is the wall time of one reduction.
+`ms_per_step` is the wall time of one reduction (max over ranks).
 """
 from __future__ import annotations
 
@@ -169,7 +170,7 @@ def run_reference(args, cfg, n, nb, rank, world):
     t = float(np.mean(tf))
     val = Fm / t / 1e9
     line = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
                        "n": n, "nb": nb},
@@ -220,10 +221,12 @@ def main():
     Q, Z = torch.empty_like(A0), torch.empty_like(A0)
     stream = torch.cuda.current_stream()
 
+    from paper_1710_08538_b200 import mg
+
     def step():
         A.copy_(A0)
         B.copy_(B0)
-        return ht.reduce_device(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+        return mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
 
     for _ in range(args.warmup):
         step()
@@ -251,7 +254,7 @@ def main():
         elapsed = float(t.item())
     t_step = elapsed / args.steps
     Fm = model_flops(n, nb)
-    value = Fm * world / t_step / 1e9
+    value = Fm / t_step / 1e9  # one pencil per step, whatever the number of GPUs
 
     agg = {k: float(np.sum([r[k] for r in reps])) for k in
            ("t_panel", "t_gemm", "t_factor", "t_other", "panel_bytes", "flops", "flops_level3", "launches")}
@@ -274,14 +277,30 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        ht.reduce_device  # noqa
+        # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host
         ts = []
         for _ in range(max(1, min(args.steps, 2))):
+            if dist:
+                dist.barrier()
             t0 = time.time()
-            ht.ht_reduce(A_h, B_h, nb=nb)
-            ts.append(time.time() - t0)
+            if world == 1:
+                ht.ht_reduce(A_h, B_h, nb=nb)
+            else:
+                hA = torch.from_numpy(np.ascontiguousarray(A_h.T)).pin_memory()
+                hB = torch.from_numpy(np.ascontiguousarray(B_h.T)).pin_memory()
+                A.copy_(hA, non_blocking=True)
+                B.copy_(hB, non_blocking=True)
+                mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+                outs = [M.cpu() for M in (A, B, Q, Z)]
+                torch.cuda.synchronize()
+            te_ = time.time() - t0
+            if dist:
+                tt = torch.tensor([te_], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te_ = float(tt.item())
+            ts.append(te_)
         te = float(np.mean(ts))
-        e2e = {"value": Fm * world / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
+        e2e = {"value": Fm / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
                "d2h_bytes_per_step": 4 * n * n * 8, "s_per_step": te}
 
     cpu = None
@@ -294,15 +313,15 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
                            "n": n, "nb": nb, "seed": ht_inputs.CONFIGS[cfg]["seed"],
                            "l2": "inputs larger than L2 (A,B,Q,Z = 4 x %.0f MB)" % (n * n * 8 / 1e6),
-                           "parallelism": "replicas" if world > 1 else "single"},
+                           "parallelism": (f"AB-replicated, QZ-rowslab{world}" if world > 1 else "single")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(agg["launches"]), "clocks": clk,
-                "detail": {"gflops_executed": agg["flops"] / elapsed / 1e9 * world, "model_flops": Fm,
+                "detail": {"gflops_executed": agg["flops"] / elapsed / 1e9, "model_flops": Fm,
                            "executed_flops_per_step": agg["flops"] / args.steps,
                            "t_panel_s": agg["t_panel"] / args.steps, "t_gemm_s": agg["t_gemm"] / args.steps,
                            "t_factor_s": agg["t_factor"] / args.steps, "t_other_s": agg["t_other"] / args.steps,

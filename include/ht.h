@@ -84,6 +84,13 @@ typedef struct {
                               column j failed and triggered a premature absorption)       */
     int64_t max_panels;    /* test hook: stop after this many panel+absorption steps (0 = all);
                               the output is then a partial reduction with A = Q^T A0 Z etc. */
+    /* Multi-GPU row slab: unless both are 0, only rows [row_begin, row_end) of Q and Z
+       are computed (Q and Z only receive right multiplications, so their rows are
+       independent).  A, B (H, T) are computed in
+       full on every caller.  Rows of Q, Z outside the slab are left unspecified.
+       0, 0 = all rows.  Requires 0 <= row_begin <= row_end <= n, else HT_EARG_OPT. */
+    int64_t row_begin;
+    int64_t row_end;
 } ht_options;
 
 /* Statistics of one reduction (the paper's Table 3/4 columns). */

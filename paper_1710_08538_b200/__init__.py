@@ -32,7 +32,8 @@ class HTOptions(ctypes.Structure):
     _fields_ = [("nb", ctypes.c_int64), ("max_ir", ctypes.c_int), ("tol_factor", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
                 ("force_ir_fail", ctypes.POINTER(ctypes.c_int64)), ("n_force_ir_fail", ctypes.c_int64),
-                ("ir_trace", ctypes.POINTER(ctypes.c_int32)), ("max_panels", ctypes.c_int64)]
+                ("ir_trace", ctypes.POINTER(ctypes.c_int32)), ("max_panels", ctypes.c_int64),
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64)]
 
 
 class HTReport(ctypes.Structure):
@@ -112,8 +113,11 @@ def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True):
     return H, T, Q, Z
 
 
-def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=(), ir_trace=None, max_panels=0):
+def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=(), ir_trace=None, max_panels=0,
+                 row_range=None):
     opt = HTOptions()
+    if row_range is not None:
+        opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
     opt.nb = int(nb)
     opt.max_ir = int(max_ir)
     opt.tol_factor = float(tol_factor)

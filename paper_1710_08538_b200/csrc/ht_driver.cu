@@ -233,6 +233,7 @@ struct Run {
     double *A, *B, *Q, *Z;
     int64_t lda, ldb, ldq, ldz;
     bool wq, wz;
+    int64_t qz0 = 0, qz1 = 0;  // rows of Q and Z this call computes (multi-GPU row slabs)
     ht_report rep;
     double extra_flops = 0.0;
 
@@ -447,22 +448,22 @@ struct Run {
                 wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
             }
             std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, n}, ChainMat{A, lda, 0, 0, n}};
-            if (wz) mats.push_back(ChainMat{Z, ldz, 0, 0, n});
+            if (wz) mats.push_back(ChainMat{Z, ldz, 0, qz0, qz1});
             TRY(chain(mats, wl));
         }
         const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
         {
-            double *Xs[2] = {B, wz ? Z : nullptr};
-            int64_t lds[2] = {ldb, ldz};
+            double *Xs[2] = {B, wz ? Z + qz0 : nullptr};  // Z: only this call's row slab
+            int64_t lds[2] = {ldb, ldz}, rows[2] = {n, qz1 - qz0};
             for (int q = 0; q < 2; ++q) {
                 double *X = Xs[q];
-                if (!X) continue;
-                const int64_t ldx = lds[q];
-                TRY(gemm('N', 'N', n, k, k, 1.0, X + p0 * ldx, ldx, V + p0, n, 0.0, w->W1, n));
-                TRY(gemm('N', 'N', n, k, k, 1.0, X + (n - k) * ldx, ldx, L1, ldw, 1.0, w->W1, n));
-                TRY(gemm('N', 'N', n, k, k, 1.0, w->W1, n, T, nb, 0.0, w->W2, n));
-                TRY(gemm('N', 'T', n, k, k, -1.0, w->W2, n, V + p0, n, 1.0, X + p0 * ldx, ldx));
-                TRY(gemm('N', 'T', n, k, k, -1.0, w->W2, n, L1, ldw, 1.0, X + (n - k) * ldx, ldx));
+                if (!X || rows[q] <= 0) continue;
+                const int64_t ldx = lds[q], nr = rows[q];
+                TRY(gemm('N', 'N', nr, k, k, 1.0, X + p0 * ldx, ldx, V + p0, n, 0.0, w->W1, n));
+                TRY(gemm('N', 'N', nr, k, k, 1.0, X + (n - k) * ldx, ldx, L1, ldw, 1.0, w->W1, n));
+                TRY(gemm('N', 'N', nr, k, k, 1.0, w->W1, n, T, nb, 0.0, w->W2, n));
+                TRY(gemm('N', 'T', nr, k, k, -1.0, w->W2, n, V + p0, n, 1.0, X + p0 * ldx, ldx));
+                TRY(gemm('N', 'T', nr, k, k, -1.0, w->W2, n, L1, ldw, 1.0, X + (n - k) * ldx, ldx));
             }
             TRY(gemm('N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
             TRY(gemm('N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
@@ -488,7 +489,7 @@ struct Run {
                                                   1, w->Vhat + x.ov, wdt, w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
             std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, R0}, ChainMat{A, lda, 0, 0, n}};
-            if (wz) mats.push_back(ChainMat{Z, ldz, 0, 0, n});
+            if (wz) mats.push_back(ChainMat{Z, ldz, 0, qz0, qz1});
             TRY(chain(mats, {ChainWin{w->Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}}}));
         }
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
@@ -505,7 +506,7 @@ struct Run {
                 wl.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, J, 0}, {n, n, n}});
             }
             std::vector<ChainMat> mats{ChainMat{B, ldb, 1, J + 1, n}, ChainMat{A, lda, 1, J, n}};
-            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
             TRY(chain(mats, wl));
         }
         // UR = [U1; R~1]  (2k x k)
@@ -523,11 +524,12 @@ struct Run {
                 TRY(gemm('N', 'N', nc, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
                 TRY(gemm('N', 'T', 2 * k, nc, k, -1.0, w->UR, ldur, w->W2, n, 1.0, Xp, e.ld));
             }
-            if (wq) {  // Q(:, p0:p0+2k) <- Q (I - UR S UR^T)
-                double *Xp = Q + p0 * ldq;
-                TRY(gemm('N', 'N', n, k, 2 * k, 1.0, Xp, ldq, w->UR, ldur, 0.0, w->W1, n));
-                TRY(gemm('N', 'N', n, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
-                TRY(gemm('N', 'T', n, 2 * k, k, -1.0, w->W2, n, w->UR, ldur, 1.0, Xp, ldq));
+            if (wq && qz1 > qz0) {  // Q(rows, p0:p0+2k) <- Q (I - UR S UR^T)
+                double *Xp = Q + qz0 + p0 * ldq;
+                const int64_t nr = qz1 - qz0;
+                TRY(gemm('N', 'N', nr, k, 2 * k, 1.0, Xp, ldq, w->UR, ldur, 0.0, w->W1, n));
+                TRY(gemm('N', 'N', nr, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
+                TRY(gemm('N', 'T', nr, 2 * k, k, -1.0, w->W2, n, w->UR, ldur, 1.0, Xp, ldq));
             }
         }
         // ===== L3: QR staircase restoring B, top -> bottom (sec. 3.3.2f) =====
@@ -542,7 +544,7 @@ struct Run {
                                                   w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
             std::vector<ChainMat> mats{ChainMat{B, ldb, 1, R0 + q, n}, ChainMat{A, lda, 1, J, n}};
-            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
             TRY(chain(mats, {ChainWin{w->Qw + x.oq, R0, (int)p, {R0 + q, J, 0}, {n, n, n}}}));
         }
         return 0;
@@ -556,12 +558,12 @@ struct Run {
         // right: A(:, J:n) -= Y V(J:n,:)^T ; B, Z <- . (I - V T V^T)
         TRY(gemm('N', 'T', n, n - J, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
         TRY(right_wy(B, ldb, n, p0, n - p0, V + p0, n, T, nb, k));
-        if (wz) TRY(right_wy(Z, ldz, n, p0, n - p0, V + p0, n, T, nb, k));
+        if (wz && qz1 > qz0) TRY(right_wy(Z + qz0, ldz, qz1 - qz0, p0, n - p0, V + p0, n, T, nb, k));
         // left: A(p0:n, J:n), B(p0:n, p0:n) <- (I - U S^T U^T) . ; Q <- Q (I - U S U^T)
         TRY(left_wy(A, lda, p0, n - p0, J, n - J, U + p0, n, S, nb, k));
         TRY(left_wy(B, ldb, p0, n - p0, p0, n - p0, U + p0, n, S, nb, k));
         TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));  // Fact 3
-        if (wq) TRY(right_wy(Q, ldq, n, p0, n - p0, U + p0, n, S, nb, k));
+        if (wq && qz1 > qz0) TRY(right_wy(Q + qz0, ldq, qz1 - qz0, p0, n - p0, U + p0, n, S, nb, k));
         if (m >= 2) {
             const int64_t R0 = J + 1;
             wins_reset();
@@ -570,7 +572,7 @@ struct Run {
                                                   w->tau + x.ot}};
             TRY(factor_and_form(f1, 0));
             std::vector<ChainMat> mats{ChainMat{A, lda, 1, J, n}};
-            if (wq) mats.push_back(ChainMat{Q, ldq, 0, 0, n});
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
             TRY(chain(mats, {ChainWin{w->Qw + x.oq, R0, (int)m, {J, 0, 0}, {n, n, n}}}));
         }
         return 0;
@@ -586,6 +588,9 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     if (n > 0 && wantq && (!Q || ldq < n)) return HT_EARG_Q;
     if (n > 0 && wantz && (!Z || ldz < n)) return HT_EARG_Z;
     if (opt && opt->n_force_ir_fail > 0 && !opt->force_ir_fail) return HT_EARG_OPT;
+    if (opt && (opt->row_begin != 0 || opt->row_end != 0) &&
+        (opt->row_begin < 0 || opt->row_end > n || opt->row_begin > opt->row_end))
+        return HT_EARG_OPT;
     return 0;
 }
 
@@ -679,6 +684,8 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
     R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
     R.wq = wantq != 0; R.wz = wantz != 0;
+    R.qz0 = 0; R.qz1 = n;
+    if (opt && (opt->row_begin != 0 || opt->row_end != 0)) { R.qz0 = opt->row_begin; R.qz1 = opt->row_end; }
     cudaStream_t st = R.st;
     g_ht_flops = 0.0;
 
