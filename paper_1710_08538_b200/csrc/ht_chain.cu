@@ -38,7 +38,7 @@ struct ChainParams {
 };
 
 template <int KC>
-__global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const ChainParams P)
+__global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_constant__ ChainParams P)
 {
     extern __shared__ __align__(16) double csm[];
     const int h = P.h, cap = P.cap;

@@ -40,7 +40,7 @@ struct Work {
     cudaStream_t own_stream = nullptr;
     double *U = nullptr, *V = nullptr, *Y = nullptr, *S = nullptr, *T = nullptr;
     double *vec = nullptr, *part = nullptr;
-    unsigned long long *flags = nullptr;
+    unsigned long long *yll = nullptr, *yll_exp = nullptr;
     int *bexp = nullptr;
     unsigned epoch = 0;
     int64_t *d_out = nullptr, *h_out = nullptr;
@@ -121,7 +121,9 @@ void work_free(Work &w)
                      &w.VhatL, &w.QwL, &w.TmL, &w.tauL, &w.WtL, &w.fscrL};
     for (auto p : dp)
         if (*p) { cudaFree(*p); *p = nullptr; }
-    if (w.flags) cudaFree(w.flags);
+    if (w.yll) cudaFree(w.yll);
+    if (w.yll_exp) cudaFree(w.yll_exp);
+    w.yll = nullptr; w.yll_exp = nullptr;
     if (w.bexp) cudaFree(w.bexp);
     if (w.d_out) cudaFree(w.d_out);
     if (w.d_iflags) cudaFree(w.d_iflags);
@@ -146,7 +148,7 @@ void work_free(Work &w)
     if (w.d_cw) cudaFree(w.d_cw);
     if (w.h_cw) cudaFreeHost(w.h_cw);
     w.d_cw = nullptr; w.h_cw = nullptr;
-    w.flags = nullptr; w.bexp = nullptr; w.d_out = nullptr; w.d_iflags = nullptr; w.d_force = nullptr;
+    w.bexp = nullptr; w.d_out = nullptr; w.d_iflags = nullptr; w.d_force = nullptr;
     w.d_fd = nullptr; w.d_ld = nullptr; w.h_out = nullptr; w.h_scal = nullptr; w.h_iflags = nullptr;
     w.h_fd = nullptr; w.h_ld = nullptr;
     w.ncap = w.nbcap = 0;
@@ -178,9 +180,11 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.vec, 8 * (size_t)N));
     TRY(dalloc(&w.part, 2 * (size_t)w.gmax * (NB + 8)));
     const size_t nblk = (size_t)(N / 64 + 4);
-    if (cudaMalloc((void **)&w.flags, nblk * sizeof(unsigned long long)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.yll, 2 * (size_t)N * sizeof(unsigned long long)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.yll_exp, nblk * sizeof(unsigned long long)) != cudaSuccess) return HT_ENOMEM;
+    cudaMemset(w.yll, 0, 2 * (size_t)N * sizeof(unsigned long long));
+    cudaMemset(w.yll_exp, 0, nblk * sizeof(unsigned long long));
     if (cudaMalloc((void **)&w.bexp, nblk * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
-    cudaMemset(w.flags, 0, nblk * sizeof(unsigned long long));
     w.epoch = 1;
     if (cudaMalloc((void **)&w.d_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_out, 8 * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
@@ -753,7 +757,7 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.vsave = vv; pa.vrhs = vv + N; pa.vy = vv + 2 * N; pa.vx = vv + 3 * N;
             pa.vw = vv + 4 * N; pa.vw2 = vv + 5 * N; pa.vr = vv + 6 * N;
             pa.part = w->part; pa.pw = (int)nb + 8;
-            pa.flags = w->flags; pa.bexp = w->bexp; pa.epoch = w->epoch;
+            pa.yll = w->yll; pa.yll_exp = w->yll_exp; pa.bexp = w->bexp; pa.epoch = w->epoch;
             pa.Dinv = w->Dinv; pa.Bt = w->Bt; pa.ldbt = n; pa.dsafe = w->dsafe; pa.ypart = w->ypart;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
@@ -806,11 +810,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             unsigned long long t0 = ~0ull;
             for (auto v : h)
                 if (v && v < t0) t0 = v;
-            fprintf(stderr, "[ht trace] col %lld: block: tiles_done wait_done publish (us from first event)\n", (long long)tcol);
+            fprintf(stderr, "[ht trace] col %lld: block: tiles_done wait_done matvec_done publish (us from first event)\n", (long long)tcol);
             for (int b = nbk - 1; b >= 0; --b)
                 if (h[4 * b + 2])
-                    fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f\n", b, h[4 * b] ? (h[4 * b] - t0) * 1e-3 : -1.0,
-                            h[4 * b + 1] ? (h[4 * b + 1] - t0) * 1e-3 : -1.0, (h[4 * b + 2] - t0) * 1e-3);
+                    fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f %8.2f\n", b, h[4 * b] ? (h[4 * b] - t0) * 1e-3 : -1.0,
+                            h[4 * b + 1] ? (h[4 * b + 1] - t0) * 1e-3 : -1.0, h[4 * b + 3] ? (h[4 * b + 3] - t0) * 1e-3 : -1.0,
+                            (h[4 * b + 2] - t0) * 1e-3);
             cudaFree(ttr);
         }
         if (dbg_on) {

@@ -135,7 +135,7 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
     const int p = d.p;
     const int tm = warp >> 2, tn = warp & 3;
-    double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+    double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // 4 independent DMMA chains
     for (int r0 = r_beg; r0 < p; r0 += L::RC) {
         const int rows = min(L::RC, p - r0);
         __syncthreads();
@@ -144,14 +144,14 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
         const double *va = Vs + (8 * tm + g) * L::LDV + t4;
         const double *pb = Ps + (8 * tn + g) * L::LDP + r0 + t4;
         int kk = 0;
-        for (; kk + 8 <= rows; kk += 8) {
-            dmma884(x0, x1, va[kk], pb[kk]);
-            dmma884(y0, y1, va[kk + 4], pb[kk + 4]);
+        for (; kk + 16 <= rows; kk += 16) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dmma884(x[u][0], x[u][1], va[kk + 4 * u], pb[kk + 4 * u]);
         }
-        for (; kk < rows; kk += 4) dmma884(x0, x1, va[kk], pb[kk]);  // padded rows are 0
+        for (; kk < rows; kk += 4) dmma884(x[0][0], x[0][1], va[kk], pb[kk]);  // padded rows are 0
     }
-    o0 = x0 + y0;
-    o1 = x1 + y1;
+    o0 = (x[0][0] + x[1][0]) + (x[2][0] + x[3][0]);
+    o1 = (x[0][1] + x[1][1]) + (x[2][1] + x[3][1]);
 }
 
 // Blocked, left-looking Householder QR of one p x q window view (p <= MAXP), PAPER.md
@@ -521,15 +521,15 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
             {
                 const int tm = warp >> 2, tn = warp & 3;
                 const double *pa = Ps + (8 * tm + g) * L::LDP + t4, *pb = Ps + (8 * tn + g) * L::LDP + t4;
-                double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+                double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
                 int kk = c0;
-                for (; kk + 8 <= p; kk += 8) {
-                    dmma884(x0, x1, pa[kk], pb[kk]);
-                    dmma884(y0, y1, pa[kk + 4], pb[kk + 4]);
+                for (; kk + 16 <= p; kk += 16) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) dmma884(x[u][0], x[u][1], pa[kk + 4 * u], pb[kk + 4 * u]);
                 }
-                for (; kk < p; kk += 4) dmma884(x0, x1, pa[kk], pb[kk]);
-                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = x0 + y0;
-                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = x1 + y1;
+                for (; kk < p; kk += 4) dmma884(x[0][0], x[0][1], pa[kk], pb[kk]);
+                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = (x[0][0] + x[1][0]) + (x[2][0] + x[3][0]);
+                Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = (x[0][1] + x[1][1]) + (x[2][1] + x[3][1]);
             }
             __syncthreads();
             FPROF(11);

@@ -61,7 +61,8 @@ struct PanelArgs {
     double *vsave, *vrhs, *vy, *vx, *vw, *vw2, *vr;  // n-vectors, absolute row index
     double *part;       // gridDim x PW partial sums
     int pw;
-    unsigned long long *flags;  // trsv publish words (epoch << 32 | exponent), per 128-row block
+    unsigned long long *yll;     // trsv solution in flag-in-data words: 2 per double (epoch << 32 | half)
+    unsigned long long *yll_exp; // per 128-row block: epoch << 32 | exponent
     double *Dinv;       // inverted 128x128 diagonal blocks of B(s+1:n, s+1:n)
     double *Bt;         // Dinv_b * B(block b, blocks > b): pre-scaled block rows
     int64_t ldbt;

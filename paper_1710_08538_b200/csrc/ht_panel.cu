@@ -53,6 +53,11 @@ struct __align__(16) PanelSmem {
     int ival[4];
 };
 
+// Shared memory of the panel kernel, declared at namespace scope so that every access
+// compiles to LDS/STS (a pointer kept in a struct would decay to generic loads).
+__shared__ PanelSmem g_sm;
+extern __shared__ __align__(16) double g_dyn[];
+
 __device__ __forceinline__ unsigned long long gtime()
 {
     unsigned long long t;
@@ -61,14 +66,12 @@ __device__ __forceinline__ unsigned long long gtime()
 }
 struct Ctx {
     const PanelArgs &a;
-    PanelSmem &sm;
-    double *dyn;
     int G, bid, tid, lane, warp;
     int64_t n, p0, M, rb0, rb1;
     int nr;
     double *part[2];
     int ph;
-    __device__ Ctx(const PanelArgs &aa, PanelSmem &s, double *d) : a(aa), sm(s), dyn(d)
+    __device__ Ctx(const PanelArgs &aa) : a(aa)
     {
         G = gridDim.x;
         bid = blockIdx.x;
@@ -95,7 +98,7 @@ struct Ctx {
     // (memory-level parallelism); lane partials go through shared staging.
     __device__ void coltdot(const double *X, int64_t ldx, int ncols, int off)
     {
-        double *stg = dyn;  // ncols x 33
+        double *stg = g_dyn;  // ncols x 33
         for (int c0 = warp * 4; c0 < ncols; c0 += NWP * 4) {
             double acc[4];
 #pragma unroll
@@ -104,7 +107,7 @@ struct Ctx {
                 double xv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) xv[u] = (c0 + u < ncols) ? X[(size_t)(c0 + u) * ldx + rb0 + rl] : 0.0;
-                const double vv = sm.vloc[rl];
+                const double vv = g_sm.vloc[rl];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc[u] = fma(xv[u], vv, acc[u]);
             }
@@ -122,10 +125,10 @@ struct Ctx {
         }
         __syncthreads();
     }
-    // returns (in dyn[rl]) sum_c X(rb0+rl, c) * coef[c] for own rows; all warps split the columns.
+    // returns (in g_dyn[rl]) sum_c X(rb0+rl, c) * coef[c] for own rows; all warps split the columns.
     __device__ void rowgemv(const double *X, int64_t ldx, int ncols, const double *coef)
     {
-        double *stg = dyn + TB * 4;  // NWP x RBMAX
+        double *stg = g_dyn + TB * 4;  // NWP x RBMAX
         for (int rc = 0; rc < nr; rc += 32) {
             const int rl = rc + lane;
             double s = 0.0;
@@ -141,7 +144,7 @@ struct Ctx {
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < NWP; ++w) t += stg[w * RBMAX + rl];
-            dyn[rl] = t;
+            g_dyn[rl] = t;
         }
         __syncthreads();
     }
@@ -178,7 +181,7 @@ struct Ctx {
     template <bool TR, class MF>
     __device__ void trimv(MF Mget, int m, const double *v, double *out, double scale = 1.0)
     {
-        double *stg = dyn;  // m x 33
+        double *stg = g_dyn;  // m x 33
 #pragma unroll 2
         for (int o = warp; o < m; o += NWP) {
             double s = 0.0;
@@ -200,7 +203,7 @@ struct Ctx {
     }
     __device__ double block_reduce_to_part(double v, int off)
     {
-        double s = block_sum(v, sm.red);
+        double s = block_sum(v, g_sm.red);
         if (tid == 0) mypart()[off] = s;
         return s;
     }
@@ -214,72 +217,91 @@ __device__ __forceinline__ double pow2i(int e)
     e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
     return __longlong_as_double((long long)(e + 1023) << 52);
 }
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p)
+// Flag-in-data ("LL") publication of the solve blocks: every double of y~_b travels as
+// two 8-byte words (epoch << 32 | 32-bit half), and the block exponent as one more word.
+// 8-byte accesses are single-copy atomic, so a reader that sees the current epoch in a
+// word has that word's payload: no separate flag, no release fence, one L2 round trip.
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long *p)
 {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v)
+__device__ __forceinline__ void st_volatile64(unsigned long long *p, unsigned long long v)
 {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// thread 0 spins until block cb is published for `epoch`; returns its exponent (all threads)
-__device__ __forceinline__ int wait_block(Ctx &C, int cb, unsigned epoch, int slot)
+__device__ __forceinline__ void ll_put(unsigned long long *w, double x, unsigned epoch)
 {
-    if (C.tid == 0) {
-        unsigned long long v;
-        do {
-            v = ld_acquire64(&C.a.flags[cb]);
-        } while ((unsigned)(v >> 32) != epoch);
-        C.sm.ival[slot] = (int)(unsigned)(v & 0xffffffffull);
-    }
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned long long e = (unsigned long long)epoch << 32;
+    st_volatile64(w, e | (b & 0xffffffffull));
+    st_volatile64(w + 1, e | (b >> 32));
+}
+__device__ __forceinline__ double ll_get(const unsigned long long *w, unsigned epoch)
+{
+    unsigned long long lo, hi;
+    do {
+        lo = ld_volatile64(w);
+        hi = ld_volatile64(w + 1);
+    } while ((unsigned)(lo >> 32) != epoch || (unsigned)(hi >> 32) != epoch);
+    return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+}
+__device__ __forceinline__ int ll_get_exp(const unsigned long long *w, unsigned epoch)
+{
+    unsigned long long v;
+    do {
+        v = ld_volatile64(w);
+    } while ((unsigned)(v >> 32) != epoch);
+    return (int)(unsigned)(v & 0xffffffffull);
+}
+// Stage block cb of the solution (w values) into ys[] and return its exponent (all threads).
+__device__ __forceinline__ int fetch_block(Ctx &C, int cb, int w, unsigned epoch, double *ys)
+{
+    const int64_t c0 = C.p0 + (int64_t)cb * TB;
+    if (C.tid < TB) ys[C.tid] = (C.tid < w) ? ll_get(C.a.yll + 2 * (c0 + C.tid), epoch) : 0.0;
+    if (C.tid == TB) g_sm.ival[cb & 1] = ll_get_exp(C.a.yll_exp + cb, epoch);
     __syncthreads();
-    return C.sm.ival[slot];
+    return g_sm.ival[cb & 1];
 }
 
-// acc(ri) += sum_{l < w} Xt(ri, l) * y(l) over one 128 x 128 tile (column-major, ld ldx)
-// for the 128 rows of a block; y from global (L2).  Thread (rp, grp): rows 2rp, 2rp+1,
-// columns grp, grp+8, ...: 16-byte loads, all 16 issued before any FMA.  The 8 column
-// groups are folded through shared memory by the caller (acc8).
-__device__ __forceinline__ void tile_mv(const double *Xt, int64_t ldx, const double *y, int w, int h, int tid,
-                                        double &a0, double &a1)
+// One 128 x 128 tile of the block row (column-major, ld ldx) held in registers by the
+// CTA: thread (rp, grp) keeps rows 2rp, 2rp+1 of columns grp, grp+8, ..., loaded with
+// 16-byte loads BEFORE the solution block it multiplies is waited for (the loads do not
+// depend on it), so HBM latency is off the chain's critical path.
+struct TileRegs {
+    double2 x[16];
+};
+__device__ __forceinline__ void tile_load(TileRegs &t, const double *Xt, int64_t ldx, int w, int h, int tid)
 {
     const int rp = tid & 63, grp = tid >> 6;  // 64 row pairs x 8 column groups
     const bool vec = ((ldx & 1) == 0) && ((((uintptr_t)Xt) & 15) == 0);
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-        double2 xv[8];
-        double yv[8];
-        if (vec) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int l = grp + 8 * (q + 8 * half);
-                if (l < w && 2 * rp + 1 < h) xv[q] = *reinterpret_cast<const double2 *>(Xt + (size_t)l * ldx + 2 * rp);
-                else xv[q] = make_double2((l < w && 2 * rp < h) ? Xt[(size_t)l * ldx + 2 * rp] : 0.0, 0.0);
-                yv[q] = (l < w) ? __ldcg(y + l) : 0.0;
-            }
+    for (int q = 0; q < 16; ++q) {
+        const int l = grp + 8 * q;
+        if (vec && l < w && 2 * rp + 1 < h) {
+            t.x[q] = *reinterpret_cast<const double2 *>(Xt + (size_t)l * ldx + 2 * rp);
         } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int l = grp + 8 * (q + 8 * half);
-                xv[q].x = (l < w && 2 * rp < h) ? Xt[(size_t)l * ldx + 2 * rp] : 0.0;
-                xv[q].y = (l < w && 2 * rp + 1 < h) ? Xt[(size_t)l * ldx + 2 * rp + 1] : 0.0;
-                yv[q] = (l < w) ? __ldcg(y + l) : 0.0;
-            }
+            t.x[q].x = (l < w && 2 * rp < h) ? Xt[(size_t)l * ldx + 2 * rp] : 0.0;
+            t.x[q].y = (l < w && 2 * rp + 1 < h) ? Xt[(size_t)l * ldx + 2 * rp + 1] : 0.0;
         }
+    }
+}
+__device__ __forceinline__ void tile_fma(const TileRegs &t, const double *ys, int tid, double &a0, double &a1)
+{
+    const int grp = tid >> 6;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            a0 = fma(xv[q].x, yv[q], a0);
-            a1 = fma(xv[q].y, yv[q], a1);
-        }
+    for (int q = 0; q < 16; ++q) {
+        const double yv = ys[grp + 8 * q];
+        a0 = fma(t.x[q].x, yv, a0);
+        a1 = fma(t.x[q].y, yv, a1);
     }
 }
 
 // Block back-substitution  y~ = B(p0:n, p0:n)^{-1} rhs  (flag chain, 128-row blocks).
 // rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k).
 // Block b is owned by CTA (Nb-1-b) mod G and published through the 64-bit word
-// flags[b] = (epoch << 32) | exponent, where true y~_b = 2^exponent * vy_b.
+// flag-in-data words (yll, yll_exp) with exponent e_b, where true y~_b = 2^e_b * vy_b.
 // Safe blocks use the pre-scaled block rows  Bt_bc = Dinv_b B_bc  (c > b, formed per
 // panel by ht_panel_run):  y~_b = Dinv_b rhs_b - sum_{c > b} Bt_bc y~_c, the terms
 // accumulated as the y~_c arrive; the chain's critical path is the last term
@@ -290,9 +312,8 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
 {
     unsigned long long *tt = (C.a.ttrace && jcol == C.a.tcol && C.tid == 0) ? C.a.ttrace : nullptr;
     const PanelArgs &a = C.a;
-    PanelSmem &sm = C.sm;
-    double *Dsm = C.dyn;             // TB x TB: Bt_{b,b+1} (safe) or D (unsafe)
-    double *accg = C.dyn + TB * TB;  // 4 x TB (reused as 8 x 64 pairs)
+    double *Dsm = g_dyn;             // TB x TB: Bt_{b,b+1} (safe) or D (unsafe)
+    double *accg = g_dyn + TB * TB;  // 4 x TB (reused as 8 x 64 pairs)
     const int64_t n = C.n, p0 = C.p0, M = C.M;
     const int Nb = (int)((M + TB - 1) / TB);
     const int ri = C.tid & (TB - 1), grp = C.tid >> 7;  // 128 rows x 4 column groups
@@ -330,7 +351,7 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                     rb = base(rr) - ((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]))
                          - unew(rr) * z2[k];
                 }
-                sm.rhs[C.tid] = rb;
+                g_sm.rhs[C.tid] = rb;
             }
             __syncthreads();
         }
@@ -359,12 +380,12 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
 #pragma unroll
                 for (int q = 0; q < 8; ++q) dv[q] = Di[(l0 + 4 * q) * TB + ri];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) s = fma(dv[q], sm.rhs[l0 + 4 * q], s);
+                for (int q = 0; q < 8; ++q) s = fma(dv[q], g_sm.rhs[l0 + 4 * q], s);
             }
             accg[grp * TB + ri] = s;
             __syncthreads();
             if (C.tid < TB)
-                sm.cbv[C.tid] = (accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]);
+                g_sm.cbv[C.tid] = (accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid]);
             __syncthreads();
         } else {
             for (int idx = C.tid; idx < TB * TB; idx += PNT) {
@@ -376,25 +397,24 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         double acc0 = 0.0, acc1 = 0.0;
         int Eacc = 0;
         const int cstop = safe ? b + 1 : b;
+        double *ys = accg + 4 * TB;  // staged solution block (TB doubles)
         for (int cb = Nb - 1; cb > cstop; --cb) {
             const int64_t c0 = p0 + (int64_t)cb * TB;
             const int w = (int)(n - c0 < TB ? n - c0 : TB);
-            const int ecb = wait_block(C, cb, epoch, cb & 1);
+            TileRegs tr;
+            tile_load(tr, Bsrc + (size_t)c0 * ldsrc + r0, ldsrc, w, h, C.tid);  // independent of y~_cb
+            const int ecb = fetch_block(C, cb, w, epoch, ys);
             if (ecb > Eacc) {
                 acc0 *= pow2i(Eacc - ecb);
                 acc1 *= pow2i(Eacc - ecb);
                 Eacc = ecb;
             }
-            if (cb - 1 > cstop && C.tid < TB) {  // pull the next tile into L2 while this one is consumed
-                const double *nt = Bsrc + (size_t)(c0 - TB) * ldsrc + r0;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(nt + (size_t)C.tid * ldsrc));
-                if (h > 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(nt + (size_t)C.tid * ldsrc + 64));
-            }
             double t0 = 0.0, t1 = 0.0;
-            tile_mv(Bsrc + (size_t)c0 * ldsrc + r0, ldsrc, a.vy + c0, w, h, C.tid, t0, t1);
+            tile_fma(tr, ys, C.tid, t0, t1);
             const double sc = pow2i(ecb - Eacc);
             acc0 = fma(t0, sc, acc0);
             acc1 = fma(t1, sc, acc1);
+            __syncthreads();  // ys is reused by the next tile
         }
         if (tt) tt[4 * b + 0] = gtime();
         {   // fold the 8 column groups: rows 2rp, 2rp+1
@@ -414,24 +434,26 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             // (4) critical path: y~_b = c_b 2^(-E) - acc 2^(Eacc-E) - Bt_{b,b+1} y~_{b+1} 2^(e1-E)
             double xv = 0.0;
             if (!last) {
-                const int e1 = wait_block(C, b + 1, epoch, 2);
-                if (tt) tt[4 * b + 1] = gtime();
-                if (C.tid < TB) sm.rhs[C.tid] = (C.tid < hn) ? __ldcg(a.vy + r0 + TB + C.tid) : 0.0;
-                __syncthreads();
+                const int e1 = fetch_block(C, b + 1, hn, epoch, g_sm.rhs);
+                if (tt) tt[4 * b + 1] = gtime() + (g_sm.rhs[0] != g_sm.rhs[0] ? 1 : 0);  // depends on the staged data
                 double sa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int l = grp; l < TB; l += 16)
+                for (int m = 0; m < TB / 16; ++m)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) sa[u] = fma(Dsm[(l + 4 * u) * TB + ri], sm.rhs[l + 4 * u], sa[u]);
+                    for (int u = 0; u < 4; ++u) {
+                        const int l = grp + 16 * m + 4 * u;
+                        sa[u] = fma(Dsm[l * TB + ri], g_sm.rhs[l], sa[u]);
+                    }
                 accg[grp * TB + ri] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
                 __syncthreads();
+                if (tt) tt[4 * b + 3] = gtime() + (accg[0] != accg[0] ? 1 : 0);
                 const int E = max(e1, Eacc);
                 if (C.tid < TB)
-                    xv = sm.cbv[C.tid] * pow2i(-E) - s8 * pow2i(Eacc - E) -
+                    xv = g_sm.cbv[C.tid] * pow2i(-E) - s8 * pow2i(Eacc - E) -
                          ((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid])) * pow2i(e1 - E);
                 e = E;
             } else if (C.tid < TB) {
-                xv = sm.cbv[C.tid] * pow2i(-Eacc) - s8;
+                xv = g_sm.cbv[C.tid] * pow2i(-Eacc) - s8;
             }
             // (5) post-hoc power-of-two rescale, only if some entry of the block is too large
             const bool big = (C.tid < h) && !(fabs(xv) <= BIG);
@@ -439,23 +461,27 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             if (__syncthreads_or(big)) {
                 double mx = (C.tid < h) ? fabs(xv) : 0.0;
                 mx = warp_max(mx);
-                if (C.tid < TB && C.lane == 0) sm.red[C.warp] = mx;
+                if (C.tid < TB && C.lane == 0) g_sm.red[C.warp] = mx;
                 __syncthreads();
-                mx = fmax(fmax(sm.red[0], sm.red[1]), fmax(sm.red[2], sm.red[3]));
+                mx = fmax(fmax(g_sm.red[0], g_sm.red[1]), fmax(g_sm.red[2], g_sm.red[3]));
                 if (!(mx <= BIG)) frexp(mx, &ex);
                 if (!isfinite(mx)) ex = 0;
             }
-            if (C.tid < h) a.vy[r0 + C.tid] = ex ? ldexp(xv, -ex) : xv;
+            if (C.tid < h) {
+                const double yv = ex ? ldexp(xv, -ex) : xv;
+                a.vy[r0 + C.tid] = yv;
+                ll_put(a.yll + 2 * (r0 + C.tid), yv, epoch);
+            }
             e += ex;
         } else {
-            if (C.tid < TB) sm.rhs[C.tid] = (C.tid < h) ? ldexp(sm.rhs[C.tid], -Eacc) - s8 : 0.0;
+            if (C.tid < TB) g_sm.rhs[C.tid] = (C.tid < h) ? ldexp(g_sm.rhs[C.tid], -Eacc) - s8 : 0.0;
             __syncthreads();
             if (C.warp == 0) {
                 // overflow-safe sequential back-substitution (unsafe block, e.g. config 4)
                 const int l = C.lane;
                 double v[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = sm.rhs[l + 32 * q];
+                for (int q = 0; q < 4; ++q) v[q] = g_sm.rhs[l + 32 * q];
                 for (int c = h - 1; c >= 0; --c) {
                     const int own = c & 31, hq = c >> 5;
                     double mine = v[0];
@@ -485,17 +511,19 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (l + 32 * q < h) a.vy[r0 + l + 32 * q] = v[q];
-                if (l == 0) sm.ival[3] = e;
+                    if (l + 32 * q < h) {
+                        a.vy[r0 + l + 32 * q] = v[q];
+                        ll_put(a.yll + 2 * (r0 + l + 32 * q), v[q], epoch);
+                    }
+                if (l == 0) g_sm.ival[3] = e;
             }
             __syncthreads();
-            e = sm.ival[3];
+            e = g_sm.ival[3];
         }
-        // publish: block-wide barrier orders the vy stores before thread 0's release
         __syncthreads();
         if (C.tid == 0) {
             a.bexp[b] = e;
-            st_release64(&a.flags[b], ((unsigned long long)epoch << 32) | (unsigned)e);
+            st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
             if (tt) tt[4 * b + 2] = gtime();
         }
     }
@@ -510,11 +538,11 @@ __device__ int trsv_emax(Ctx &C)
     for (int b = C.tid; b < Nb; b += PNT) e = max(e, __ldcg(&C.a.bexp[b]));  // all loads in parallel
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
-    if (C.lane == 0) C.sm.ival[C.warp & 3] = INT_MIN;
+    if (C.lane == 0) g_sm.ival[C.warp & 3] = INT_MIN;
     __syncthreads();
-    if (C.lane == 0) atomicMax(&C.sm.ival[0], e);
+    if (C.lane == 0) atomicMax(&g_sm.ival[0], e);
     __syncthreads();
-    const int r = C.sm.ival[0];
+    const int r = g_sm.ival[0];
     __syncthreads();
     return r;
 }
@@ -526,7 +554,7 @@ template <bool TRI, class VecF>
 __device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int64_t r1, int64_t cfirst, VecF vec,
                            double *out)
 {
-    double *stg = C.dyn;  // NWP x 64
+    double *stg = g_dyn;  // NWP x 64
     const int64_t n = C.n;
     for (int64_t rc = r0; rc < r1; rc += 64) {
         const int64_t rowA = rc + C.lane, rowB = rc + 32 + C.lane;
@@ -631,8 +659,8 @@ struct TileGeom {
 template <class VF>
 __device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf)
 {
-    double *red = C.dyn;               // [NWP][TRT]
-    double *vs = C.dyn + NWP * TRT;    // [TCW]
+    double *red = g_dyn;               // [NWP][TRT]
+    double *vs = g_dyn + NWP * TRT;    // [TCW]
     const bool vec = (ldx % 2) == 0;
     const int nit = tg.items();
     for (int it = C.bid; it < nit; it += C.G) {
@@ -722,12 +750,10 @@ __device__ __forceinline__ double tiled_sum(const Ctx &C, const TileGeom &tg, in
     return t;
 }
 
-__global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
+__global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ PanelArgs a)
 {
     cg::grid_group grid = cg::this_grid();
-    __shared__ PanelSmem sm;
-    extern __shared__ __align__(16) double dyn[];
-    Ctx C(a, sm, dyn);
+    Ctx C(a);
     const int64_t n = a.n, s0 = a.s0, p0 = C.p0, lda = a.lda;
     double *A = a.A;
     double *U = a.U, *V = a.V, *Y = a.Y, *S = a.S, *T = a.T;
@@ -750,32 +776,32 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         const int ku = k + 1;  // U columns incl. the new u
         C.ph++;
         // ================= P1: update column j of A =========================
-        for (int c = C.tid; c < k; c += PNT) sm.sv1[c] = (c == k - 1) ? 1.0 : V[(size_t)c * n + j0];
+        for (int c = C.tid; c < k; c += PNT) g_sm.sv1[c] = (c == k - 1) ? 1.0 : V[(size_t)c * n + j0];
         __syncthreads();
-        C.rowgemv(Y, n, k, sm.sv1);
+        C.rowgemv(Y, n, k, g_sm.sv1);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
             double a0 = A[(size_t)j0 * lda + r];
             a.vsave[r] = a0;
-            sm.vloc[rl] = a0 - dyn[rl];
+            g_sm.vloc[rl] = a0 - g_dyn[rl];
         }
         __syncthreads();
         C.coltdot(U, n, k, 0);
         grid.sync();
-        C.gather(sm.sv2, k, 0);
+        C.gather(g_sm.sv2, k, 0);
         __syncthreads();
-        C.trimv<true>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, sm.sv2, sm.sv3);  // sv3 = S^T t
-        C.rowgemv(U, n, k, sm.sv3);
+        C.trimv<true>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, g_sm.sv2, g_sm.sv3);  // sv3 = S^T t
+        C.rowgemv(U, n, k, g_sm.sv3);
         C.ph++;
         {
             double ss = 0.0;
             for (int rl = C.tid; rl < C.nr; rl += PNT) {
                 const int64_t r = C.rb0 + rl;
-                double av = sm.vloc[rl] - dyn[rl];
+                double av = g_sm.vloc[rl] - g_dyn[rl];
                 a.vx[r] = av;
                 if (r <= j0) A[(size_t)j0 * lda + r] = av;  // rows s+1:j of the updated column
                 if (r >= j0 + 2) ss += av * av;
-                sm.vloc[rl] = (r >= j0 + 2) ? av : 0.0;     // a_tail for U^T a_tail
+                g_sm.vloc[rl] = (r >= j0 + 2) ? av : 0.0;     // a_tail for U^T a_tail
             }
             __syncthreads();
             C.coltdot(U, n, k, 1);
@@ -786,9 +812,9 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         // ================= P2: left reflector (no barrier needed) ============
         double tau_u, scal_u, beta_u, alpha_u;
         {
-            C.gather(sm.sv1, k + 1, 0);  // [||a_tail||^2, U^T a_tail]
+            C.gather(g_sm.sv1, k + 1, 0);  // [||a_tail||^2, U^T a_tail]
             __syncthreads();
-            const double ss = sm.sv1[0];
+            const double ss = g_sm.sv1[0];
             alpha_u = __ldcg(&a.vx[j0 + 1]);
             tau_u = 0.0;
             scal_u = 0.0;
@@ -801,10 +827,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             }
         }
         // U^T u = scal * U^T a_tail + U(j0+1, :)^T   (u(j0+1) = 1)
-        for (int c = C.tid; c < k; c += PNT) sm.sv2[c] = scal_u * sm.sv1[1 + c] + U[(size_t)c * n + j0 + 1];
+        for (int c = C.tid; c < k; c += PNT) g_sm.sv2[c] = scal_u * g_sm.sv1[1 + c] + U[(size_t)c * n + j0 + 1];
         __syncthreads();
-        C.trimv<false>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, sm.sv2, sm.snew, -tau_u);
-        if (C.tid == 0) sm.snew[k] = tau_u;
+        C.trimv<false>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, g_sm.sv2, g_sm.snew, -tau_u);
+        if (C.tid == 0) g_sm.snew[k] = tau_u;
         auto unew = [&](int64_t r) -> double {
             return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_u);
         };
@@ -816,15 +842,15 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         }
         __syncthreads();
         if (C.bid == 0)
-            for (int i = C.tid; i <= k; i += PNT) S[(size_t)k * nb + i] = sm.snew[i];
-        auto Sget = [&](int i, int c) -> double { return c == k ? sm.snew[i] : S[(size_t)c * nb + i]; };
+            for (int i = C.tid; i <= k; i += PNT) S[(size_t)k * nb + i] = g_sm.snew[i];
+        auto Sget = [&](int i, int c) -> double { return c == k ? g_sm.snew[i] : S[(size_t)c * nb + i]; };
 
         // ================= P3: factored solve ==================================
-        for (int c = C.tid; c < ku; c += PNT) sm.sv1[c] = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
+        for (int c = C.tid; c < ku; c += PNT) g_sm.sv1[c] = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
         __syncthreads();
-        C.trimv<false>(Sget, ku, sm.sv1, sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
+        C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
-        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, sm.sv3, epoch, j0);
+        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch, j0);
         grid.sync();
         mark(1);
         int emax = trsv_emax(C);
@@ -833,15 +859,15 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
             int eb = __ldcg(&a.bexp[(r - p0) / TB]);
-            sm.vloc[rl] = ldexp(__ldcg(&a.vy[r]), eb - emax);
+            g_sm.vloc[rl] = ldexp(__ldcg(&a.vy[r]), eb - emax);
         }
         __syncthreads();
         C.coltdot(V, n, k, 0);
         grid.sync();
-        C.gather(sm.sv1, k, 0);
+        C.gather(g_sm.sv1, k, 0);
         __syncthreads();
-        C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);  // T^T (V^T y~)
-        C.rowgemv(V, n, k, sm.sv2);
+        C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);  // T^T (V^T y~)
+        C.rowgemv(V, n, k, g_sm.sv2);
         C.ph++;
         {
             double sx = 0.0, st = 0.0;
@@ -849,12 +875,12 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 const int64_t r = C.rb0 + rl;
                 double xv = 0.0;
                 if (r >= j0 + 1) {
-                    xv = sm.vloc[rl] - dyn[rl];
+                    xv = g_sm.vloc[rl] - g_dyn[rl];
                     sx += xv * xv;
                     if (r >= j0 + 2) st += xv * xv;
                 }
                 a.vx[r] = xv;
-                sm.vloc[rl] = xv;
+                g_sm.vloc[rl] = xv;
             }
             __syncthreads();
             C.coltdot(V, n, k, 2);
@@ -864,10 +890,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         grid.sync();
         mark(2);
         double xnorm2 = 0.0, xtail2 = 0.0;
-        C.gather(sm.sv1, 2, 0);
+        C.gather(g_sm.sv1, 2, 0);
         __syncthreads();
-        xnorm2 = sm.sv1[0];
-        xtail2 = sm.sv1[1];
+        xnorm2 = g_sm.sv1[0];
+        xtail2 = g_sm.sv1[1];
         __syncthreads();
 
         // ================= P4: residual + iterative refinement ================
@@ -879,13 +905,13 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         bool this_col_ir = false;
         while (!accepted) {
             // w = (I - V T V^T)[0; x]
-            C.gather(sm.sv1, k, 2);  // V^T x
+            C.gather(g_sm.sv1, k, 2);  // V^T x
             __syncthreads();
-            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);  // T t
-            C.rowgemv(V, n, k, sm.sv2);
+            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);  // T t
+            C.rowgemv(V, n, k, g_sm.sv2);
             for (int rl = C.tid; rl < C.nr; rl += PNT) {
                 const int64_t r = C.rb0 + rl;
-                a.vw[r] = __ldcg(&a.vx[r]) - dyn[rl];
+                a.vw[r] = __ldcg(&a.vx[r]) - g_dyn[rl];
             }
             grid.sync();
             // w2 = B w over area-balanced slabs, + partial U^T w2
@@ -898,7 +924,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tgb, C.rb0 + rl);
                 __syncthreads();
                 double *out = C.mypart();
-                double *stg = dyn;
+                double *stg = g_dyn;
                 for (int c = C.warp; c < ku; c += NWP) {
                     double s = 0.0;
 #pragma unroll 4
@@ -915,10 +941,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             grid.sync();
             mark(7);
             // r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:)
-            C.gather(sm.sv1, ku, 0);
+            C.gather(g_sm.sv1, ku, 0);
             __syncthreads();
-            C.trimv<true>(Sget, ku, sm.sv1, sm.sv2);  // S_{k+1}^T t
-            C.rowgemv(U, n, ku, sm.sv2);
+            C.trimv<true>(Sget, ku, g_sm.sv1, g_sm.sv2);  // S_{k+1}^T t
+            C.rowgemv(U, n, ku, g_sm.sv2);
             C.ph++;
             const double sigma = ldexp(1.0, -emax);
             {
@@ -927,20 +953,20 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                     const int64_t r = C.rb0 + rl;
                     double rv = 0.0;
                     if (r >= j0 + 1) {
-                        rv = (r == j0 + 1 ? sigma : 0.0) - (__ldcg(&a.vw2[r]) - dyn[rl]);
+                        rv = (r == j0 + 1 ? sigma : 0.0) - (__ldcg(&a.vw2[r]) - g_dyn[rl]);
                         sr += rv * rv;
                     }
                     a.vr[r] = rv;
-                    sm.vloc[rl] = rv;
+                    g_sm.vloc[rl] = rv;
                 }
                 __syncthreads();
                 C.coltdot(U, n, ku, 1);
                 C.block_reduce_to_part(sr, 0);
             }
             grid.sync();
-            C.gather(sm.sv1, 1, 0);
+            C.gather(g_sm.sv1, 1, 0);
             __syncthreads();
-            const double rn = sqrt(sm.sv1[0]), xn = sqrt(xnorm2);
+            const double rn = sqrt(g_sm.sv1[0]), xn = sqrt(xnorm2);
             __syncthreads();
             if (a.dbg && C.bid == 0 && C.tid == 0 && ir < 12) a.dbg[j0 * 12 + ir] = rn / (a.tol * xn);
             if (!forced && rn <= a.tol * xn && isfinite(rn)) {
@@ -952,25 +978,25 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             ++ir;
             ++ir_steps;
             this_col_ir = true;
-            C.gather(sm.sv1, ku, 1);  // U^T r_ext
+            C.gather(g_sm.sv1, ku, 1);  // U^T r_ext
             __syncthreads();
-            C.trimv<false>(Sget, ku, sm.sv1, sm.sv3);  // S_{k+1} (U^T r)
+            C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // S_{k+1} (U^T r)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
             trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
-                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, sm.sv3, epoch, -1);
+                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, g_sm.sv3, epoch, -1);
             grid.sync();
             const int ec = trsv_emax(C);
             if (ec > 0) { ++rescales; break; }  // a rescaled correction counts as IR failure
             C.ph++;
-            for (int rl = C.tid; rl < C.nr; rl += PNT) sm.vloc[rl] = __ldcg(&a.vy[C.rb0 + rl]);
+            for (int rl = C.tid; rl < C.nr; rl += PNT) g_sm.vloc[rl] = __ldcg(&a.vy[C.rb0 + rl]);
             __syncthreads();
             C.coltdot(V, n, k, 0);
             grid.sync();
-            C.gather(sm.sv1, k, 0);
+            C.gather(g_sm.sv1, k, 0);
             __syncthreads();
-            C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2);
-            C.rowgemv(V, n, k, sm.sv2);
+            C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);
+            C.rowgemv(V, n, k, g_sm.sv2);
             C.ph++;
             {
                 double sx = 0.0, st = 0.0;
@@ -978,12 +1004,12 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                     const int64_t r = C.rb0 + rl;
                     double xv = 0.0;
                     if (r >= j0 + 1) {
-                        xv = __ldcg(&a.vx[r]) + (sm.vloc[rl] - dyn[rl]);
+                        xv = __ldcg(&a.vx[r]) + (g_sm.vloc[rl] - g_dyn[rl]);
                         sx += xv * xv;
                         if (r >= j0 + 2) st += xv * xv;
                     }
                     a.vx[r] = xv;
-                    sm.vloc[rl] = xv;
+                    g_sm.vloc[rl] = xv;
                 }
                 __syncthreads();
                 C.coltdot(V, n, k, 2);
@@ -991,10 +1017,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
                 C.block_reduce_to_part(st, 1);
             }
             grid.sync();
-            C.gather(sm.sv1, 2, 0);
+            C.gather(g_sm.sv1, 2, 0);
             __syncthreads();
-            xnorm2 = sm.sv1[0];
-            xtail2 = sm.sv1[1];
+            xnorm2 = g_sm.sv1[0];
+            xtail2 = g_sm.sv1[1];
             __syncthreads();
         }
         mark(3);
@@ -1028,7 +1054,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
             const int64_t r = C.rb0 + rl;
             double v = vget(r);
             V[(size_t)k * n + r] = v;
-            sm.vloc[rl] = v;
+            g_sm.vloc[rl] = v;
         }
         __syncthreads();
         C.coltdot(V, n, k, 0);
@@ -1039,17 +1065,17 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(PanelArgs a)
         mark(4);
         for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tga, C.rb0 + rl);
         __syncthreads();
-        C.gather(sm.sv1, k, 0);  // z = V^T v
+        C.gather(g_sm.sv1, k, 0);  // z = V^T v
         __syncthreads();
         if (C.bid == 0) {
-            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, sm.sv1, sm.sv2, -gam);
-            for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = sm.sv2[i];
+            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2, -gam);
+            for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = g_sm.sv2[i];
             if (C.tid == 0) T[(size_t)k * nb + k] = gam;
         }
-        C.rowgemv(Y, n, k, sm.sv1);
+        C.rowgemv(Y, n, k, g_sm.sv1);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
-            Y[(size_t)k * n + r] = gam * (a.vw2[r] - dyn[rl]);
+            Y[(size_t)k * n + r] = gam * (a.vw2[r] - g_dyn[rl]);
         }
         ++k;
         __syncthreads();
