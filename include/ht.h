@@ -75,7 +75,8 @@ typedef struct {
     int max_ir;            /* max IR corrections per column; <= 0 -> 10          */
     double tol_factor;     /* IR tolerance factor c in c*u*||B||_F; <= 0 -> 2    */
     uint64_t seed;         /* seed of the desingularisation draws rho            */
-    void *stream;          /* cudaStream_t to run on (NULL: library stream)              */
+    void *stream;          /* cudaStream_t the reduction is ordered on (NULL: the legacy
+                              default stream); the library forks its own streams from it */
     const int64_t *force_ir_fail; /* host array of 0-based columns whose solve is forced
                                      to fail IR (test hook for premature absorption)   */
     int64_t n_force_ir_fail;

@@ -49,15 +49,20 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     double *Qs = Xs + (size_t)cap * ldh;  // [2][kc][ldq]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
 
-    // which matrix / slab
+    // slab tasks over all matrices; a capped grid loops over them (persistent style), so that
+    // concurrent streams keep SMs free for the factorization chain
+    int64_t ntask = 0;
+    for (int q = 0; q < P.nm; ++q) ntask += (P.m[q].s_end - P.m[q].s_begin + h - 1) / h;
+    for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+    __syncthreads();  // the ring of the previous task is no longer read
     int mi = 0;
-    int64_t blk = blockIdx.x;
+    int64_t blk = task;
     for (; mi < P.nm; ++mi) {
         const int64_t ns = (P.m[mi].s_end - P.m[mi].s_begin + h - 1) / h;
         if (blk < ns) break;
         blk -= ns;
     }
-    if (mi >= P.nm) return;
+    if (mi >= P.nm) continue;
     const ChainMat M = P.m[mi];
     const int64_t s0 = M.s_begin + blk * h;
     const int hs = (int)(M.s_end - s0 < (int64_t)h ? M.s_end - s0 : (int64_t)h);  // valid slab rows
@@ -202,13 +207,14 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             store_cols(a0, a1);
         }
     }
+    }  // task loop
 }
 
 }  // namespace
 
 // Apply a chain of explicit window transforms to up to 3 matrices (one launch).
 // d_wins: device array of nw windows (application order, monotone offsets).
-int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax)
+int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax, int maxgrid)
 {
     if (nm <= 0 || nw <= 0) return 0;
     ChainParams P;
@@ -233,8 +239,9 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
         HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         init = true;
     }
-    if (kc == 16) chain_apply_kernel<16><<<(unsigned)nblk, CNT, smem, st>>>(P);
-    else chain_apply_kernel<8><<<(unsigned)nblk, CNT, smem, st>>>(P);
+    const unsigned grid = (unsigned)(maxgrid > 0 && nblk > maxgrid ? maxgrid : nblk);
+    if (kc == 16) chain_apply_kernel<16><<<grid, CNT, smem, st>>>(P);
+    else chain_apply_kernel<8><<<grid, CNT, smem, st>>>(P);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -53,6 +53,14 @@ struct Work {
     double *VhatL = nullptr, *QwL = nullptr, *TmL = nullptr, *tauL = nullptr, *WtL = nullptr, *fscrL = nullptr;
     cudaStream_t side_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // critical path (panel, B, factorization chains) on a high-priority stream; the A
+    // and Q/Z window applies on two low-priority streams that overlap the chains
+    cudaStream_t hp_stream = nullptr, sA = nullptr, sQZ = nullptr;
+    cudaEvent_t ev[12] = {};
+    double *W1A = nullptr, *W2A = nullptr, *W1Q = nullptr, *W2Q = nullptr;
+    // window stores of the R3 and L3 chains (their A/Z/Q applies run after the chain)
+    double *VhatR = nullptr, *QwR = nullptr, *TmR = nullptr, *tauR = nullptr, *WtR = nullptr;
+    double *VhatB = nullptr, *QwB = nullptr, *TmB = nullptr, *tauB = nullptr, *WtB = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
@@ -60,7 +68,7 @@ struct Work {
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     LarftDesc *d_ld = nullptr, *h_ld = nullptr;
     ChainWin *d_cw = nullptr, *h_cw = nullptr;
-    int64_t ndesc = 0, fd_cur = 0, ld_cur = 0, cw_cur = 0;
+    int64_t ndesc = 0, ncw = 0, fd_cur = 0, ld_cur = 0, cw_cur = 0;
 };
 
 std::mutex g_mu;
@@ -118,7 +126,8 @@ void work_free(Work &w)
 {
     double **dp[] = {&w.U, &w.V, &w.Y, &w.S, &w.T, &w.vec, &w.part, &w.VW, &w.UW, &w.Vhat, &w.tau,
                      &w.Gm, &w.Tm, &w.Wt, &w.Qw, &w.tmp, &w.W1, &w.W2, &w.UR, &w.fscr, &w.d_scal,
-                     &w.VhatL, &w.QwL, &w.TmL, &w.tauL, &w.WtL, &w.fscrL};
+                     &w.VhatL, &w.QwL, &w.TmL, &w.tauL, &w.WtL, &w.fscrL, &w.W1A, &w.W2A, &w.W1Q, &w.W2Q,
+                     &w.VhatR, &w.QwR, &w.TmR, &w.tauR, &w.WtR, &w.VhatB, &w.QwB, &w.TmB, &w.tauB, &w.WtB};
     for (auto p : dp)
         if (*p) { cudaFree(*p); *p = nullptr; }
     if (w.yll) cudaFree(w.yll);
@@ -209,6 +218,22 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
         return HT_ECUDA;
     if (!w.ev_fork && cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
     if (!w.ev_join && cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
+    TRY(dalloc(&w.W1A, nnb + 4 * nb2)); TRY(dalloc(&w.W2A, nnb + 4 * nb2));
+    TRY(dalloc(&w.W1Q, nnb + 4 * nb2)); TRY(dalloc(&w.W2Q, nnb + 4 * nb2));
+    TRY(dalloc(&w.VhatR, 2 * nnb + 4 * nb2)); TRY(dalloc(&w.WtR, 2 * nnb + 4 * nb2));
+    TRY(dalloc(&w.QwR, 4 * nnb + 8 * nb2)); TRY(dalloc(&w.TmR, nnb + 2 * nb2)); TRY(dalloc(&w.tauR, (size_t)N + 2 * NB));
+    TRY(dalloc(&w.VhatB, 2 * nnb + 4 * nb2)); TRY(dalloc(&w.WtB, 2 * nnb + 4 * nb2));
+    TRY(dalloc(&w.QwB, 4 * nnb + 8 * nb2)); TRY(dalloc(&w.TmB, nnb + 2 * nb2)); TRY(dalloc(&w.tauB, (size_t)N + 2 * NB));
+    if (!w.hp_stream) {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return HT_ECUDA;
+        if (cudaStreamCreateWithPriority(&w.hp_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&w.sA, cudaStreamNonBlocking, lo) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&w.sQZ, cudaStreamNonBlocking, lo) != cudaSuccess)
+            return HT_ECUDA;
+        for (auto &e : w.ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
+    }
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
@@ -216,12 +241,13 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.ypart, (size_t)(N / 256 + 2) * (size_t)N));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
+    w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
-    if (cudaMalloc((void **)&w.d_cw, w.ndesc * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
-    if (cudaMallocHost((void **)&w.h_cw, w.ndesc * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.d_cw, w.ncw * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_cw, w.ncw * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
     w.ncap = N;
     w.nbcap = NB;
     *out = &w;
@@ -242,14 +268,26 @@ struct Run {
     double extra_flops = 0.0;
 
     // ---------------- helpers --------------------------------------------
+    int gemm_on(cudaStream_t s, char ta, char tb, int64_t M, int64_t N, int64_t K, double al, const double *Ap,
+                int64_t la, const double *Bp, int64_t lb, double be, double *Cp, int64_t lc)
+    {
+        if (M <= 0 || N <= 0) return 0;
+        tm.begin(s, 1);
+        int rc = ht_gemm(s, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
+        tm.end(s);
+        return rc;
+    }
     int gemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double al, const double *Ap, int64_t la,
              const double *Bp, int64_t lb, double be, double *Cp, int64_t lc)
     {
-        if (M <= 0 || N <= 0) return 0;
-        tm.begin(st, 1);
-        int rc = ht_gemm(st, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
-        tm.end(st);
-        return rc;
+        return gemm_on(st, ta, tb, M, N, K, al, Ap, la, Bp, lb, be, Cp, lc);
+    }
+    // s waits for everything issued so far on `from`
+    int dep(cudaStream_t s, cudaStream_t from, int slot)
+    {
+        HT_CUDA_TRY(cudaEventRecord(w->ev[slot], from));
+        HT_CUDA_TRY(cudaStreamWaitEvent(s, w->ev[slot], 0));
+        return 0;
     }
     int gemm_multi_on(cudaStream_t s, char ta, char tb, const std::vector<GemmBatchItem> &it)
     {
@@ -368,11 +406,12 @@ struct Run {
 
     // Chained window applies (ht_chain.cu): every matrix in `mats` takes the windows of
     // `wl` in order; lo/hi of a window are indexed by the matrix position in `mats`.
-    int chain(const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl)
+    int chain(const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl) { return chain_on(st, mats, wl, 0); }
+    int chain_on(cudaStream_t s, const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl, int maxgrid)
     {
         if (wl.empty() || mats.empty()) return 0;
         const int nw = (int)wl.size();
-        if (w->cw_cur + nw > w->ndesc) return HT_ENUMERIC;
+        if (w->cw_cur + nw > w->ncw) return HT_ENUMERIC;
         ChainWin *hc = w->h_cw + w->cw_cur;
         int pmax = 0;
         for (int i = 0; i < nw; ++i) {
@@ -383,25 +422,40 @@ struct Run {
                 if (b > a) g_ht_flops += 2.0 * (double)(b - a) * wl[i].p * (double)wl[i].p;
             }
         }
-        HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, st));
-        tm.begin(st, 1);
-        int rc = ht_chain_apply(st, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax);
-        tm.end(st);
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
+        tm.begin(s, 1);
+        int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid);
+        tm.end(s);
         w->cw_cur += nw;
         return rc;
     }
 
     // ---------------- absorption (sec. 3.3) ---------------------------------
+    // Streams: st (high priority) carries the critical path -- the staircase factorization
+    // chains and every update of B (the chains read B's band); sA applies the same window
+    // transforms to A, sQZ to Z and Q (their rows/columns never feed a factorization), so
+    // those big applies overlap the one-SM factorization chains.  Both are joined before
+    // the next panel.  Per matrix the paper's order of operations is kept.
+    int SIDE_GRID = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 56;  // CTAs of an A or Q/Z chain apply
     int absorb(int64_t s0, int64_t k)
     {
         const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
         double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
+        const bool serial = getenv("HT_SERIAL") != nullptr;  // debug: everything on st
+        const bool dbg_old = serial && getenv("HT_OLDCHAIN") != nullptr;  // debug: per-window A/Z/Q applies
+        cudaStream_t sA = serial ? st : w->sA, sQ = serial ? st : w->sQZ;
         w->fd_cur = w->ld_cur = w->cw_cur = 0;
-        // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns
-        TRY(gemm('N', 'N', p0, k, n - p0, 1.0, A + p0 * lda, lda, V + p0, n, 0.0, w->W1, n));
-        TRY(gemm('N', 'N', p0, k, k, 1.0, w->W1, n, T, nb, 0.0, Y, n));
-        if (J > p0) TRY(gemm('N', 'T', p0, J - p0, k, -1.0, Y, n, V + p0, n, 1.0, A + p0 * lda, lda));
-        if (m <= 2 * k) return absorb_tail(s0, k);
+        TRY(dep(sA, st, 0));
+        TRY(dep(sQ, st, 0));
+        // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns (A: sA)
+        TRY(gemm_on(sA, 'N', 'N', p0, k, n - p0, 1.0, A + p0 * lda, lda, V + p0, n, 0.0, w->W1A, n));
+        TRY(gemm_on(sA, 'N', 'N', p0, k, k, 1.0, w->W1A, n, T, nb, 0.0, Y, n));
+        if (J > p0) TRY(gemm_on(sA, 'N', 'T', p0, J - p0, k, -1.0, Y, n, V + p0, n, 1.0, A + p0 * lda, lda));
+        if (m <= 2 * k) {
+            TRY(dep(st, sA, 1));
+            TRY(dep(st, sQ, 2));
+            return absorb_tail(s0, k);
+        }
 
         // geometry (Remark 4): right boundaries rb = {0, kt-k, kt, ..., m}
         const int64_t rem = (m - k) % k;
@@ -444,35 +498,42 @@ struct Run {
                                      w->Vhat + x.ov, p, w->tau + x.ot});
         }
         TRY(factor_and_form(fds, 0));
+        TRY(dep(sA, st, 3));  // R1 windows and L^_1 (written into VW) are ready
+        TRY(dep(sQ, st, 3));
         // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e) =====
+        const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
         {
             std::vector<ChainWin> wl;
             for (int i = 0; i < r; ++i) {
                 const Win &x = wins[i];
                 wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
             }
-            std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, n}, ChainMat{A, lda, 0, 0, n}};
-            if (wz) mats.push_back(ChainMat{Z, ldz, 0, qz0, qz1});
-            TRY(chain(mats, wl));
+            TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
+            std::vector<ChainWin> wa = wl;
+            for (auto &x : wa) x.hi[0] = n;  // A: all rows
+            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wa, SIDE_GRID));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, SIDE_GRID));
         }
-        const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
         {
-            double *Xs[2] = {B, wz ? Z + qz0 : nullptr};  // Z: only this call's row slab
-            int64_t lds[2] = {ldb, ldz}, rows[2] = {n, qz1 - qz0};
-            for (int q = 0; q < 2; ++q) {
-                double *X = Xs[q];
-                if (!X || rows[q] <= 0) continue;
-                const int64_t ldx = lds[q], nr = rows[q];
-                TRY(gemm('N', 'N', nr, k, k, 1.0, X + p0 * ldx, ldx, V + p0, n, 0.0, w->W1, n));
-                TRY(gemm('N', 'N', nr, k, k, 1.0, X + (n - k) * ldx, ldx, L1, ldw, 1.0, w->W1, n));
-                TRY(gemm('N', 'N', nr, k, k, 1.0, w->W1, n, T, nb, 0.0, w->W2, n));
-                TRY(gemm('N', 'T', nr, k, k, -1.0, w->W2, n, V + p0, n, 1.0, X + p0 * ldx, ldx));
-                TRY(gemm('N', 'T', nr, k, k, -1.0, w->W2, n, L1, ldw, 1.0, X + (n - k) * ldx, ldx));
+            // W-updates: B on st, Z on sQZ, A on sA
+            struct WX { double *X; int64_t ld, rows; cudaStream_t s; double *W1, *W2; } wx[2] = {
+                {B, ldb, n, st, w->W1, w->W2}, {wz ? Z + qz0 : nullptr, ldz, qz1 - qz0, sQ, w->W1Q, w->W2Q}};
+            for (auto &e : wx) {
+                if (!e.X || e.rows <= 0) continue;
+                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + p0 * e.ld, e.ld, V + p0, n, 0.0, e.W1, n));
+                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + (n - k) * e.ld, e.ld, L1, ldw, 1.0, e.W1, n));
+                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.W1, n, T, nb, 0.0, e.W2, n));
+                TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, V + p0, n, 1.0, e.X + p0 * e.ld, e.ld));
+                TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, L1, ldw, 1.0, e.X + (n - k) * e.ld, e.ld));
             }
-            TRY(gemm('N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
-            TRY(gemm('N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
+            TRY(gemm_on(sA, 'N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
+            TRY(gemm_on(sA, 'N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
         }
         // ===== R3: RQ staircase restoring B, bottom -> top (sec. 3.3.1 second "e)") =====
+        // factor + apply to B's rows above, window by window (st); A, Z take the whole chain after.
+        const Store sr{w->VhatR, w->QwR, w->TmR, w->tauR, w->WtR, w->fscr};
+        std::vector<Win> winsR;
+        std::vector<ChainWin> wr;
         for (int t = r; t >= 0; --t) {
             int64_t R0, h, C0, wdt;
             if (t >= 1) {
@@ -487,70 +548,101 @@ struct Run {
                 wdt = h;
             }
             if (wdt <= 1) continue;
-            wins_reset();
-            Win x = add_win((int)wdt, (int)h);
+            Win x = add_win(winsR, (int)wdt, (int)h);
             std::vector<FactorDesc> f1{FactorDesc{B + (R0 + h - 1) + (C0 + wdt - 1) * ldb, -ldb, -1, (int)wdt, (int)h,
-                                                  1, w->Vhat + x.ov, wdt, w->tau + x.ot}};
-            TRY(factor_and_form(f1, 0));
-            std::vector<ChainMat> mats{ChainMat{B, ldb, 0, 0, R0}, ChainMat{A, lda, 0, 0, n}};
-            if (wz) mats.push_back(ChainMat{Z, ldz, 0, qz0, qz1});
-            TRY(chain(mats, {ChainWin{w->Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}}}));
+                                                  1, sr.Vhat + x.ov, wdt, sr.tau + x.ot}};
+            TRY(factor_and_form(f1, std::vector<Win>{x}, sr, st));
+            const ChainWin cw{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}};
+            TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, R0}}, {cw}, 0));
+            if (dbg_old) {
+                TRY(chain_on(st, {ChainMat{A, lda, 0, 0, n}}, {ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}}}, 0));
+                if (wz) TRY(chain_on(st, {ChainMat{Z, ldz, 0, qz0, qz1}}, {ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}}}, 0));
+            } else
+            wr.push_back(ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}});
         }
+        TRY(dep(sA, st, 4));
+        TRY(dep(sQ, st, 4));
+        TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wr, SIDE_GRID));
+        if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wr, SIDE_GRID));
+
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
         // ===== L2: spike, chain on B, A, Q, W-updates =====
         TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
         TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
         TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));
-        {
-            std::vector<ChainWin> wl;
-            for (int i = 0; i < r; ++i) {
-                const Win &x = winsL[i];
-                const int64_t R0 = J + 1 + lb[r - 1 - i];
-                wl.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, J, 0}, {n, n, n}});
-            }
-            std::vector<ChainMat> mats{ChainMat{B, ldb, 1, J + 1, n}, ChainMat{A, lda, 1, J, n}};
-            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
-            TRY(chain(mats, wl));
+        std::vector<ChainWin> wlu;
+        for (int i = 0; i < r; ++i) {
+            const Win &x = winsL[i];
+            const int64_t R0 = J + 1 + lb[r - 1 - i];
+            wlu.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, 0, 0}, {n, n, n}});
         }
+        TRY(chain_on(st, {ChainMat{B, ldb, 1, J + 1, n}}, wlu, 0));
         // UR = [U1; R~1]  (2k x k)
         const int64_t ldur = 2 * k;
         TRY(copy2d(k, k, U + p0, n, w->UR, ldur));
         TRY(copy2d(k, k, w->UW, ldw, w->UR + k, ldur));
         TRY(zero_lower(k, k, w->UR + k, ldur, 0));
+        TRY(dep(sA, st, 5));  // L1 windows and UR are ready
+        TRY(dep(sQ, st, 5));
         {
-            // B(p0:p0+2k, J+1:n) and A(p0:p0+2k, J:n):  X <- X - UR S^T (X^T UR)^T
-            struct LX { double *X; int64_t ld, c0; } lx[2] = {{B, ldb, J + 1}, {A, lda, J}};
+            std::vector<ChainWin> wla = wlu;
+            for (auto &x : wla) x.lo[0] = J;  // A: columns J..n
+            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wla, SIDE_GRID));
+            std::vector<ChainWin> wlq = wlu;
+            for (auto &x : wlq) x.lo[0] = 0;
+            if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, SIDE_GRID));
+        }
+        {
+            // B(p0:p0+2k, J+1:n) (st) and A(p0:p0+2k, J:n) (sA):  X <- X - UR S^T (X^T UR)^T
+            struct LX { double *X; int64_t ld, c0; cudaStream_t s; double *W1, *W2; } lx[2] = {
+                {B, ldb, J + 1, st, w->W1, w->W2}, {A, lda, J, sA, w->W1A, w->W2A}};
             for (auto &e : lx) {
                 const int64_t nc = n - e.c0;
                 double *Xp = e.X + p0 + e.c0 * e.ld;
-                TRY(gemm('T', 'N', nc, k, 2 * k, 1.0, Xp, e.ld, w->UR, ldur, 0.0, w->W1, n));
-                TRY(gemm('N', 'N', nc, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
-                TRY(gemm('N', 'T', 2 * k, nc, k, -1.0, w->UR, ldur, w->W2, n, 1.0, Xp, e.ld));
+                TRY(gemm_on(e.s, 'T', 'N', nc, k, 2 * k, 1.0, Xp, e.ld, w->UR, ldur, 0.0, e.W1, n));
+                TRY(gemm_on(e.s, 'N', 'N', nc, k, k, 1.0, e.W1, n, S, nb, 0.0, e.W2, n));
+                TRY(gemm_on(e.s, 'N', 'T', 2 * k, nc, k, -1.0, w->UR, ldur, e.W2, n, 1.0, Xp, e.ld));
             }
-            if (wq && qz1 > qz0) {  // Q(rows, p0:p0+2k) <- Q (I - UR S UR^T)
+            if (wq && qz1 > qz0) {  // Q(rows, p0:p0+2k) <- Q (I - UR S UR^T)   (sQZ)
                 double *Xp = Q + qz0 + p0 * ldq;
                 const int64_t nr = qz1 - qz0;
-                TRY(gemm('N', 'N', nr, k, 2 * k, 1.0, Xp, ldq, w->UR, ldur, 0.0, w->W1, n));
-                TRY(gemm('N', 'N', nr, k, k, 1.0, w->W1, n, S, nb, 0.0, w->W2, n));
-                TRY(gemm('N', 'T', nr, 2 * k, k, -1.0, w->W2, n, w->UR, ldur, 1.0, Xp, ldq));
+                TRY(gemm_on(sQ, 'N', 'N', nr, k, 2 * k, 1.0, Xp, ldq, w->UR, ldur, 0.0, w->W1Q, n));
+                TRY(gemm_on(sQ, 'N', 'N', nr, k, k, 1.0, w->W1Q, n, S, nb, 0.0, w->W2Q, n));
+                TRY(gemm_on(sQ, 'N', 'T', nr, 2 * k, k, -1.0, w->W2Q, n, w->UR, ldur, 1.0, Xp, ldq));
             }
         }
         // ===== L3: QR staircase restoring B, top -> bottom (sec. 3.3.2f) =====
+        const Store sb{w->VhatB, w->QwB, w->TmB, w->tauB, w->WtB, w->fscr};
+        std::vector<Win> winsB;
+        std::vector<ChainWin> wb;
         for (int t = 0; t <= r; ++t) {
             const int64_t R0 = J + 1 + lb[t];
             const int64_t q = lb[t + 1] - lb[t];
             const int64_t p = (t < r) ? lb[t + 2] - lb[t] : q;
             if (p <= 1) continue;
-            wins_reset();
-            Win x = add_win((int)p, (int)q);
-            std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)p, (int)q, 0, w->Vhat + x.ov, p,
-                                                  w->tau + x.ot}};
-            TRY(factor_and_form(f1, 0));
-            std::vector<ChainMat> mats{ChainMat{B, ldb, 1, R0 + q, n}, ChainMat{A, lda, 1, J, n}};
-            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
-            TRY(chain(mats, {ChainWin{w->Qw + x.oq, R0, (int)p, {R0 + q, J, 0}, {n, n, n}}}));
+            Win x = add_win(winsB, (int)p, (int)q);
+            std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)p, (int)q, 0, sb.Vhat + x.ov, p,
+                                                  sb.tau + x.ot}};
+            TRY(factor_and_form(f1, std::vector<Win>{x}, sb, st));
+            TRY(chain_on(st, {ChainMat{B, ldb, 1, R0 + q, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {R0 + q, 0, 0}, {n, n, n}}}, 0));
+            if (dbg_old) {
+                TRY(chain_on(st, {ChainMat{A, lda, 1, J, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}}}, 0));
+                if (wq) TRY(chain_on(st, {ChainMat{Q, ldq, 0, qz0, qz1}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {0, 0, 0}, {n, n, n}}}, 0));
+            } else
+            wb.push_back(ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}});
         }
+        TRY(dep(sA, st, 6));
+        TRY(dep(sQ, st, 6));
+        TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wb, SIDE_GRID));
+        if (wq) {
+            std::vector<ChainWin> wbq = wb;
+            for (auto &x : wbq) x.lo[0] = 0;
+            TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wbq, SIDE_GRID));
+        }
+        // join: the next panel reads A and B; U, V, S, T, Y, the window stores are reused
+        TRY(dep(st, sA, 7));
+        TRY(dep(st, sQ, 8));
         return 0;
     }
 
@@ -683,7 +775,13 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     Run R;
     memset(&R.rep, 0, sizeof(R.rep));
     R.w = w;
-    R.st = (opt && opt->stream) ? (cudaStream_t)opt->stream : w->own_stream;
+    // the caller's stream forks into the library's high-priority stream and joins it at the end
+    // (NULL is the legacy default stream, exactly as in the CUDA runtime: work the caller
+    //  queued there, e.g. the copies that produced A and B, is ordered before the reduction)
+    const cudaStream_t user_st = opt ? (cudaStream_t)opt->stream : (cudaStream_t)0;
+    R.st = w->hp_stream;
+    HT_CUDA_TRY(cudaEventRecord(w->ev[9], user_st));
+    HT_CUDA_TRY(cudaStreamWaitEvent(R.st, w->ev[9], 0));
     R.n = n; R.nb = nb;
     R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
     R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
@@ -843,6 +941,7 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
         TRY(R.zero_lower(n, n, dB, lddb, 0));
     }
     HT_CUDA_TRY(cudaEventRecord(e1, st));
+    HT_CUDA_TRY(cudaStreamWaitEvent(user_st, e1, 0));
     HT_CUDA_TRY(cudaEventSynchronize(e1));
     R.tm.resolve();
     R.rep.t_panel = R.tm.acc[0];

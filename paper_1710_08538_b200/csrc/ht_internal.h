@@ -43,7 +43,8 @@ struct ChainWin {
     int p;
     int64_t lo[3], hi[3];
 };
-int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax);
+int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax,
+                   int maxgrid = 0);  // maxgrid > 0: at most that many CTAs (they loop over the slabs)
 
 int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp);
 int ht_larft_run(cudaStream_t st, const LarftDesc *d_descs, int nd);

@@ -175,3 +175,22 @@ def test_config2_full_size_vs_oracle():
     check_props(A, B, H, T, Q, Z)
     Hr, Tr, _, _ = oracle.ht_T(A, B)
     check_parity(A, B, H, T, Hr, Tr)
+
+
+def test_repeated_calls_on_the_default_stream_are_identical():
+    """Inputs refreshed by copies queued on torch's (legacy default) stream right before each
+    call: the library must order itself after them (ht_options.stream NULL = default stream)."""
+    A, B = ht_inputs.pencil("qruniform", 700, 21)
+    dA, dB = to_dev(A), to_dev(B)
+    A0, B0 = dA.clone(), dB.clone()
+    dQ, dZ = torch.empty_like(dA), torch.empty_like(dA)
+    outs = []
+    for _ in range(3):
+        dA.copy_(A0)
+        dB.copy_(B0)
+        ht.reduce_device(dA, dB, dQ, dZ, nb=64)
+        torch.cuda.synchronize()
+        outs.append([from_dev(t) for t in (dA, dB, dQ, dZ)])
+    for o in outs[1:]:
+        for x, y in zip(outs[0], o):
+            assert np.array_equal(x, y)
