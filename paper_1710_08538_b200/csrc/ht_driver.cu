@@ -409,6 +409,7 @@ struct Run {
     int chain(const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl) { return chain_on(st, mats, wl, 0); }
     int chain_on(cudaStream_t s, const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl, int maxgrid)
     {
+        if (s != st && getenv("HT_SKIP_SIDE")) return 0;  // debug timing experiment only (wrong results)
         if (wl.empty() || mats.empty()) return 0;
         const int nw = (int)wl.size();
         if (w->cw_cur + nw > w->ncw) return HT_ENUMERIC;
@@ -442,7 +443,7 @@ struct Run {
         const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
         double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
         const bool serial = getenv("HT_SERIAL") != nullptr;  // debug: everything on st
-        const bool dbg_old = serial && getenv("HT_OLDCHAIN") != nullptr;  // debug: per-window A/Z/Q applies
+        const int BATCH = getenv("HT_BATCH") ? atoi(getenv("HT_BATCH")) : 4;  // windows per side-stream apply
         cudaStream_t sA = serial ? st : w->sA, sQ = serial ? st : w->sQZ;
         w->fd_cur = w->ld_cur = w->cw_cur = 0;
         TRY(dep(sA, st, 0));
@@ -532,6 +533,15 @@ struct Run {
         // ===== R3: RQ staircase restoring B, bottom -> top (sec. 3.3.1 second "e)") =====
         // factor + apply to B's rows above, window by window (st); A, Z take the whole chain after.
         const Store sr{w->VhatR, w->QwR, w->TmR, w->tauR, w->WtR, w->fscr};
+        auto flush_right = [&](std::vector<ChainWin> &ws) -> int {
+            if (ws.empty()) return 0;
+            TRY(dep(sA, st, 4));
+            TRY(dep(sQ, st, 4));
+            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, ws, SIDE_GRID));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, SIDE_GRID));
+            ws.clear();
+            return 0;
+        };
         std::vector<Win> winsR;
         std::vector<ChainWin> wr;
         for (int t = r; t >= 0; --t) {
@@ -554,16 +564,10 @@ struct Run {
             TRY(factor_and_form(f1, std::vector<Win>{x}, sr, st));
             const ChainWin cw{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}};
             TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, R0}}, {cw}, 0));
-            if (dbg_old) {
-                TRY(chain_on(st, {ChainMat{A, lda, 0, 0, n}}, {ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}}}, 0));
-                if (wz) TRY(chain_on(st, {ChainMat{Z, ldz, 0, qz0, qz1}}, {ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}}}, 0));
-            } else
             wr.push_back(ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}});
+            if ((int)wr.size() == BATCH || t == 0) TRY(flush_right(wr));  // A, Z take the windows in batches
         }
-        TRY(dep(sA, st, 4));
-        TRY(dep(sQ, st, 4));
-        TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wr, SIDE_GRID));
-        if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wr, SIDE_GRID));
+        TRY(flush_right(wr));
 
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
         // ===== L2: spike, chain on B, A, Q, W-updates =====
@@ -614,6 +618,19 @@ struct Run {
         }
         // ===== L3: QR staircase restoring B, top -> bottom (sec. 3.3.2f) =====
         const Store sb{w->VhatB, w->QwB, w->TmB, w->tauB, w->WtB, w->fscr};
+        auto flush_left = [&](std::vector<ChainWin> &ws) -> int {
+            if (ws.empty()) return 0;
+            TRY(dep(sA, st, 6));
+            TRY(dep(sQ, st, 6));
+            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, SIDE_GRID));
+            if (wq) {
+                std::vector<ChainWin> wq_ = ws;
+                for (auto &x : wq_) x.lo[0] = 0;
+                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, SIDE_GRID));
+            }
+            ws.clear();
+            return 0;
+        };
         std::vector<Win> winsB;
         std::vector<ChainWin> wb;
         for (int t = 0; t <= r; ++t) {
@@ -626,20 +643,10 @@ struct Run {
                                                   sb.tau + x.ot}};
             TRY(factor_and_form(f1, std::vector<Win>{x}, sb, st));
             TRY(chain_on(st, {ChainMat{B, ldb, 1, R0 + q, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {R0 + q, 0, 0}, {n, n, n}}}, 0));
-            if (dbg_old) {
-                TRY(chain_on(st, {ChainMat{A, lda, 1, J, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}}}, 0));
-                if (wq) TRY(chain_on(st, {ChainMat{Q, ldq, 0, qz0, qz1}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {0, 0, 0}, {n, n, n}}}, 0));
-            } else
             wb.push_back(ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}});
+            if ((int)wb.size() == BATCH) TRY(flush_left(wb));
         }
-        TRY(dep(sA, st, 6));
-        TRY(dep(sQ, st, 6));
-        TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wb, SIDE_GRID));
-        if (wq) {
-            std::vector<ChainWin> wbq = wb;
-            for (auto &x : wbq) x.lo[0] = 0;
-            TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wbq, SIDE_GRID));
-        }
+        TRY(flush_left(wb));
         // join: the next panel reads A and B; U, V, S, T, Y, the window stores are reused
         TRY(dep(st, sA, 7));
         TRY(dep(st, sQ, 8));
