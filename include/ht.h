@@ -108,11 +108,15 @@ typedef struct {
     int64_t desingularizations;/* zero pivots replaced by 2u*rho*||B||_F                */
     int64_t solve_rescales;    /* triangular solves that needed power-of-two rescaling  */
     double t_panel;            /* device seconds in panel kernels (CUDA events)         */
-    double t_gemm;             /* device seconds in DMMA GEMM launches                  */
+    double t_gemm;             /* device seconds in DMMA GEMM launches (excl. chains)   */
     double t_factor;           /* device seconds in window factorizations (+larft)      */
     double t_other;            /* device seconds in copies / fills / small kernels      */
     double panel_bytes;        /* algorithmic HBM bytes of the panel phase  */
     int64_t launches;          /* kernels launched by the library                       */
+    double t_chain;            /* device seconds in chained window applies (sum over    */
+                               /* launches; launches on concurrent streams overlap)     */
+    double flops_chain;        /* FP64 flops executed by the chained window applies     */
+    int64_t chain_launches;    /* chained window-apply launches                         */
 } ht_report;
 
 /*

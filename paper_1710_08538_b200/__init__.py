@@ -43,7 +43,8 @@ class HTReport(ctypes.Structure):
                 ("ir_extra_columns", ctypes.c_int64), ("ir_failed_columns", ctypes.c_int64),
                 ("desingularizations", ctypes.c_int64), ("solve_rescales", ctypes.c_int64),
                 ("t_panel", ctypes.c_double), ("t_gemm", ctypes.c_double), ("t_factor", ctypes.c_double),
-                ("t_other", ctypes.c_double), ("panel_bytes", ctypes.c_double), ("launches", ctypes.c_int64)]
+                ("t_other", ctypes.c_double), ("panel_bytes", ctypes.c_double), ("launches", ctypes.c_int64),
+                ("t_chain", ctypes.c_double), ("flops_chain", ctypes.c_double), ("chain_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -75,12 +75,12 @@ std::mutex g_mu;
 Work g_work[16];
 
 // Per-kernel-class device time from CUDA events recorded on the launch stream.
-// Classes: 0 panel, 1 DMMA GEMM, 2 factorizations, 3 other.
+// Classes: 0 panel, 1 DMMA GEMM, 2 factorizations, 3 other, 4 chained window applies.
 struct Timer {
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     std::vector<std::pair<int, size_t>> pending;
-    double acc[4] = {0, 0, 0, 0};
+    double acc[5] = {0, 0, 0, 0, 0};
     int64_t launches = 0;
     int cls = 0;
     size_t start = 0;
@@ -266,6 +266,8 @@ struct Run {
     int64_t qz0 = 0, qz1 = 0;  // rows of Q and Z this call computes (multi-GPU row slabs)
     ht_report rep;
     double extra_flops = 0.0;
+    double chain_flops = 0.0;
+    int64_t chain_launches = 0;
 
     // ---------------- helpers --------------------------------------------
     int gemm_on(cudaStream_t s, char ta, char tb, int64_t M, int64_t N, int64_t K, double al, const double *Ap,
@@ -420,11 +422,16 @@ struct Run {
             pmax = std::max(pmax, wl[i].p);
             for (size_t m = 0; m < mats.size(); ++m) {
                 const int64_t a = std::max(wl[i].lo[m], mats[m].s_begin), b = std::min(wl[i].hi[m], mats[m].s_end);
-                if (b > a) g_ht_flops += 2.0 * (double)(b - a) * wl[i].p * (double)wl[i].p;
+                if (b > a) {
+                    const double f = 2.0 * (double)(b - a) * wl[i].p * (double)wl[i].p;
+                    g_ht_flops += f;
+                    chain_flops += f;
+                }
             }
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
-        tm.begin(s, 1);
+        tm.begin(s, 4);
+        ++chain_launches;
         int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid);
         tm.end(s);
         w->cw_cur += nw;
@@ -955,6 +962,9 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     R.rep.t_gemm = R.tm.acc[1];
     R.rep.t_factor = R.tm.acc[2];
     R.rep.t_other = R.tm.acc[3];
+    R.rep.t_chain = R.tm.acc[4];
+    R.rep.flops_chain = R.chain_flops;
+    R.rep.chain_launches = R.chain_launches;
     R.rep.launches = R.tm.launches;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);

@@ -57,36 +57,23 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                  : "d"(a), "d"(b));
 }
 
-// 1/sqrt(x) and 1/x by a single-precision seed + Newton steps (each step doubles the
-// correct bits: 23 -> 46 -> 92), ~1 ulp; exact library path outside the float range.
-__device__ __forceinline__ double fast_rsqrt(double x)
-{
-    if (!(x > 1e-36 && x < 1e36)) return 1.0 / sqrt(x);
-    double y = (double)rsqrtf((float)x);
-    y = y * fma(-0.5 * x * y, y, 1.5);
-    y = y * fma(-0.5 * x * y, y, 1.5);
-    return y;
-}
-__device__ __forceinline__ double fast_rcp(double x)
-{
-    if (!(fabs(x) > 1e-36 && fabs(x) < 1e36)) return 1.0 / x;
-    double y = (double)(1.0f / (float)x);
-    y = y * fma(-x, y, 2.0);
-    y = y * fma(-x, y, 2.0);
-    return y;
-}
 // Householder scalars of x = [alpha; tail], ||tail||^2 = ss > 0 (dlarfg convention, R-Z1):
 // beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||,
-// scal = 1 / (alpha - beta) (so that v = [1; tail * scal]).
+// scal = 1 / (alpha - beta) = sign(alpha) / (||x|| tau)  (so that v = [1; tail * scal]).
+// One rsqrt and one reciprocal of tau in [1, 2] (float seed + two Newton steps, no range
+// checks needed): a short dependency chain on the column step's critical path.
 __device__ __forceinline__ void house_scalars(double alpha, double ss, double &beta, double &tau, double &scal)
 {
     const double N = fma(alpha, alpha, ss);
-    const double r = fast_rsqrt(N);
+    const double r = rsqrt(N);  // 1 / ||x||
     const double nrm = N * r;
     beta = alpha >= 0.0 ? -nrm : nrm;
     tau = fma(fabs(alpha), r, 1.0);
-    const double den = fast_rcp(fabs(alpha) + nrm);
-    scal = alpha >= 0.0 ? den : -den;
+    double it = (double)(1.0f / (float)tau);  // tau in [1, 2]
+    it = it * fma(-tau, it, 2.0);
+    it = it * fma(-tau, it, 2.0);
+    const double sc = r * it;
+    scal = alpha >= 0.0 ? sc : -sc;
 }
 
 // RPT: rows per thread per leaf; a warp holds 4 row groups x 8 leaf columns, so the
@@ -136,11 +123,15 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
     const int p = d.p;
     const int tm = warp >> 2, tn = warp & 3;
     double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // 4 independent DMMA chains
+    unsigned long long *fp = g_fprof;
+    long long c_a = 0, c_b = 0;
     for (int r0 = r_beg; r0 < p; r0 += L::RC) {
         const int rows = min(L::RC, p - r0);
         __syncthreads();
+        if (fp && tid == 0) c_a = clock64();
         stage_v<RPT>(d, i * PBW, r0, rows, Vs);
         __syncthreads();
+        if (fp && tid == 0) c_b = clock64() + (Vs[0] != Vs[0] ? 1 : 0);
         const double *va = Vs + (8 * tm + g) * L::LDV + t4;
         const double *pb = Ps + (8 * tn + g) * L::LDP + r0 + t4;
         int kk = 0;
@@ -152,6 +143,12 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
     }
     o0 = (x[0][0] + x[1][0]) + (x[2][0] + x[3][0]);
     o1 = (x[0][1] + x[1][1]) + (x[2][1] + x[3][1]);
+    if (fp && tid == 0) {
+        const long long c_c = clock64() + (o0 != o0 ? 1 : 0);
+        atomicAdd(&fp[24], (unsigned long long)(c_b - c_a));
+        atomicAdd(&fp[25], (unsigned long long)(c_c - c_b));
+        atomicAdd(&fp[26], 1ull);
+    }
 }
 
 // Blocked, left-looking Householder QR of one p x q window view (p <= MAXP), PAPER.md
@@ -555,6 +552,8 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     for (int c = 0; c < PBW; ++c)
                         if (c < nc) Tout(c0 + i, c0 + c) = trow[c];
                 }
+#pragma unroll
+                for (int c = 0; c < PBW; ++c) Ts[i * LDT + c] = (i < nc && c < nc) ? trow[c] : 0.0;
             }
             __threadfence_block();
             __syncthreads();
@@ -570,36 +569,72 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 }
                 __threadfence_block();
                 __syncthreads();
-                // Y = G T_b (c0 x 32; T_b upper, zero beyond nc): 8x8 tiles over warps
-                double *Yg = gscratch + (size_t)c0 * PBW;
+                if (c0 * LDX > PBW * L::LDP || c0 * LDX > L::VSZ) {
+                    // large windows (q > ~200): operands in global memory
+                    double *Yg = gscratch + (size_t)c0 * PBW;
+                    for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
+                        const int tr = tile >> 2, tn = tile & 3;
+                        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                        for (int kk = 0; kk < PBW; kk += 4)
+                            dmma884(a0, a1, gscratch[(size_t)(8 * tr + g) * PBW + kk + t4], Ts[(kk + t4) * LDT + 8 * tn + g]);
+                        Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4] = a0;
+                        Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4 + 1] = a1;
+                    }
+                    __threadfence_block();
+                    __syncthreads();
+                    for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
+                        const int tr = tile >> 2, tn = tile & 3;
+                        double a0 = 0.0, a1 = 0.0;
+                        for (int kk = 8 * tr; kk < c0; kk += 4) {
+                            const int row = 8 * tr + g, kr = kk + t4;
+                            const double av = (kr >= row) ? Tout(row, kr) : 0.0;
+                            dmma884(a0, a1, av, Yg[(size_t)kr * PBW + 8 * tn + g]);
+                        }
+                        const int row = 8 * tr + g, cc = 8 * tn + 2 * t4;
+                        if (cc < nc) Tout(row, c0 + cc) = -a0;
+                        if (cc + 1 < nc) Tout(row, c0 + cc + 1) = -a1;
+                    }
+                } else {
+                // stage G = [X_0; ...; X_{b-1}] (c0 x 32) into Ps (free now), ld LDX
+                for (int idx = tid; idx < c0 * PBW; idx += FNT) Ps[(idx / PBW) * LDX + idx % PBW] = __ldcg(gscratch + idx);
+                __syncthreads();
+                // Y = G T_b (c0 x 32; T_b upper, zero beyond nc) into Vs, ld LDX: operands in shared memory
+                double *Ys = Vs;
                 for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
                     const int tr = tile >> 2, tn = tile & 3;
                     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-                    for (int kk = 0; kk < PBW; kk += 4) {
-                        const double av = gscratch[(size_t)(8 * tr + g) * PBW + kk + t4];
-                        const int kr = kk + t4, cc = 8 * tn + g;
-                        const double bv = (kr <= cc && cc < nc) ? Tout(c0 + kr, c0 + cc) : 0.0;
-                        dmma884(a0, a1, av, bv);
-                    }
-                    Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4] = a0;
-                    Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4 + 1] = a1;
+                    for (int kk = 0; kk < PBW; kk += 4)
+                        dmma884(a0, a1, Ps[(8 * tr + g) * LDX + kk + t4], Ts[(kk + t4) * LDT + 8 * tn + g]);
+                    Ys[(8 * tr + g) * LDX + 8 * tn + 2 * t4] = a0;
+                    Ys[(8 * tr + g) * LDX + 8 * tn + 2 * t4 + 1] = a1;
                 }
-                __threadfence_block();
                 __syncthreads();
-                // T(0:c0, c0:c0+nc) = -T(0:c0, 0:c0) Y  (T upper: k from the tile's first row)
+                // T(0:c0, c0:c0+nc) = -T(0:c0, 0:c0) Y  (T upper: k from the tile's first row); the
+                // A fragments (rows of the previous T, global) are all loaded before the DMMAs
                 for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
                     const int tr = tile >> 2, tn = tile & 3;
+                    const int row = 8 * tr + g;
+                    constexpr int MAXK = 128;  // c0 <= 480: chunks of 32 k-steps
                     double a0 = 0.0, a1 = 0.0;
-                    for (int kk = 8 * tr; kk < c0; kk += 4) {
-                        const int row = 8 * tr + g, kr = kk + t4;
-                        const double av = (kr >= row) ? Tout(row, kr) : 0.0;
-                        const double bv = Yg[(size_t)kr * PBW + 8 * tn + g];
-                        dmma884(a0, a1, av, bv);
+                    for (int k0 = 8 * tr; k0 < c0; k0 += MAXK) {
+                        double av[MAXK / 4];
+#pragma unroll
+                        for (int u = 0; u < MAXK / 4; ++u) {
+                            const int kr = k0 + 4 * u + t4;
+                            av[u] = (kr < c0 && kr >= row) ? Tout(row, kr) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < MAXK / 4; ++u) {
+                            const int kr = k0 + 4 * u + t4;
+                            if (k0 + 4 * u < c0) dmma884(a0, a1, av[u], kr < c0 ? Ys[kr * LDX + 8 * tn + g] : 0.0);
+                        }
                     }
-                    const int row = 8 * tr + g, cc = 8 * tn + 2 * t4;
+                    const int cc = 8 * tn + 2 * t4;
                     if (cc < nc) Tout(row, c0 + cc) = -a0;
                     if (cc + 1 < nc) Tout(row, c0 + cc + 1) = -a1;
+                }
                 }
             }
             FPROF(6);
