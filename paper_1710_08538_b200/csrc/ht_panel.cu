@@ -50,7 +50,9 @@ struct __align__(16) PanelSmem {
     double red[32];
     double rhs[TB];
     double cbv[TB];
+    double yrecv[TB];  // y~_{b+1} handed over by the partner CTA of the cluster (DSMEM)
     int ival[4];
+    int erecv;
 };
 
 // Shared memory of the panel kernel, declared at namespace scope so that every access
@@ -90,10 +92,12 @@ struct Ctx {
         part[1] = a.part + (size_t)G * a.pw;
         ph = 0;
     }
-    __device__ double *mypart() { return part[ph & 1] + (size_t)bid * a.pw; }
+    // partials are stored index-major: (CTA b, index c) at part[ph][c * G + b], so a gather
+    // reads contiguous CTA runs
+    __device__ void putpart(int c, double v) { part[ph & 1][(size_t)c * G + bid] = v; }
     __device__ double *curpart() { return part[ph & 1]; }
 
-    // out[c] = sum over own rows of X(r,c) * vloc[r - rb0], c < ncols -> mypart()[off + c].
+    // out[c] = sum over own rows of X(r,c) * vloc[r - rb0], c < ncols -> partial (off + c).
     // Warps take 4 columns at a time and issue all their loads before summing
     // (memory-level parallelism); lane partials go through shared staging.
     __device__ void coltdot(const double *X, int64_t ldx, int ncols, int off)
@@ -116,12 +120,11 @@ struct Ctx {
                 if (c0 + u < ncols) stg[(c0 + u) * 33 + lane] = acc[u];
         }
         __syncthreads();
-        double *out = mypart() + off;
         for (int c = tid; c < ncols; c += PNT) {
             double t = 0.0;
 #pragma unroll 8
             for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
-            out[c] = t;
+            putpart(off + c, t);
         }
         __syncthreads();
     }
@@ -153,7 +156,7 @@ struct Ctx {
     // are issued before the sums (the partials live in L2: latency, not bandwidth, bound).
     __device__ void gather(double *dst, int ncols, int off)
     {
-        const double *pp = curpart() + off;
+        const double *pp = curpart() + (size_t)off * G;
         constexpr int MAXB = 8;  // G <= 256 CTAs
         for (int c0 = warp * 2; c0 < ncols; c0 += NWP * 2) {
             double v[2][MAXB];
@@ -162,7 +165,7 @@ struct Ctx {
 #pragma unroll
                 for (int q = 0; q < MAXB; ++q) {
                     const int b = lane + 32 * q;
-                    v[u][q] = (b < G && c0 + u < ncols) ? __ldcg(pp + (size_t)b * a.pw + c0 + u) : 0.0;
+                    v[u][q] = (b < G && c0 + u < ncols) ? __ldcg(pp + (size_t)(c0 + u) * G + b) : 0.0;
                 }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -181,6 +184,37 @@ struct Ctx {
     template <bool TR, class MF>
     __device__ void trimv(MF Mget, int m, const double *v, double *out, double scale = 1.0)
     {
+        if (!TR) {
+            // out[i] = sum_{c >= i} M(i, c) v[c], column-oriented: warps over columns, lanes over
+            // rows, so every load is a contiguous column segment and all of a lane's loads are
+            // independent; the 16 warp partials are added in a fixed order (deterministic)
+            double *stg = g_dyn;  // NWP x m
+            double acc[NBMAX / 32];
+#pragma unroll
+            for (int q = 0; q < NBMAX / 32; ++q) acc[q] = 0.0;
+            for (int c = warp; c < m; c += NWP) {
+                const double vc = v[c];
+#pragma unroll
+                for (int q = 0; q < NBMAX / 32; ++q) {
+                    const int i = lane + 32 * q;
+                    if (i <= c) acc[q] = fma(Mget(i, c), vc, acc[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NBMAX / 32; ++q) {
+                const int i = lane + 32 * q;
+                if (i < m) stg[warp * m + i] = acc[q];
+            }
+            __syncthreads();
+            for (int o = tid; o < m; o += PNT) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWP; ++w) t += stg[w * m + o];
+                out[o] = scale * t;
+            }
+            __syncthreads();
+            return;
+        }
         double *stg = g_dyn;  // m x 33
 #pragma unroll 2
         for (int o = warp; o < m; o += NWP) {
@@ -204,7 +238,7 @@ struct Ctx {
     __device__ double block_reduce_to_part(double v, int off)
     {
         double s = block_sum(v, g_sm.red);
-        if (tid == 0) mypart()[off] = s;
+        if (tid == 0) putpart(off, s);
         return s;
     }
 };
@@ -241,18 +275,22 @@ __device__ __forceinline__ void ll_put(unsigned long long *w, double x, unsigned
 __device__ __forceinline__ double ll_get(const unsigned long long *w, unsigned epoch)
 {
     unsigned long long lo, hi;
-    do {
+    while (true) {
         lo = ld_volatile64(w);
         hi = ld_volatile64(w + 1);
-    } while ((unsigned)(lo >> 32) != epoch || (unsigned)(hi >> 32) != epoch);
+        if ((unsigned)(lo >> 32) == epoch && (unsigned)(hi >> 32) == epoch) break;
+        __nanosleep(64);  // back off: the pollers of all waiting CTAs share L2 with the chain
+    }
     return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
 __device__ __forceinline__ int ll_get_exp(const unsigned long long *w, unsigned epoch)
 {
     unsigned long long v;
-    do {
+    while (true) {
         v = ld_volatile64(w);
-    } while ((unsigned)(v >> 32) != epoch);
+        if ((unsigned)(v >> 32) == epoch) break;
+        __nanosleep(64);
+    }
     return (int)(unsigned)(v & 0xffffffffull);
 }
 // Stage block cb of the solution (w values) into ys[] and return its exponent (all threads).
@@ -317,7 +355,19 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
     const int64_t n = C.n, p0 = C.p0, M = C.M;
     const int Nb = (int)((M + TB - 1) / TB);
     const int ri = C.tid & (TB - 1), grp = C.tid >> 7;  // 128 rows x 4 column groups
-    for (int b = Nb - 1 - C.bid; b >= 0; b -= C.G) {
+    // Blocks are paired from the bottom into super-blocks {hi = Nb-1-2s, lo = hi-1}, one
+    // super-block per 2-CTA cluster: rank 0 solves hi, rank 1 solves lo, and hi's solution
+    // reaches lo through distributed shared memory instead of a flag round trip through L2.
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(), ncl = C.G / 2, cid = C.bid / 2;
+    const int Nsb = (Nb + 1) / 2;
+    for (int sb = cid; sb < Nsb; sb += ncl) {
+        const int b = Nb - 1 - 2 * sb - rank;  // hi (rank 0) or lo (rank 1)
+        const bool paired_lo = (rank == 1);     // lo: y~_{b+1} comes from the partner
+        if (b < 0) {                            // odd Nb: the top super-block has no lo
+            cl.sync();
+            continue;
+        }
         const int64_t r0 = p0 + (int64_t)b * TB;
         const int h = (int)(n - r0 < TB ? n - r0 : TB);
         const bool safe = a.dsafe[b] != 0;
@@ -434,7 +484,15 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             // (4) critical path: y~_b = c_b 2^(-E) - acc 2^(Eacc-E) - Bt_{b,b+1} y~_{b+1} 2^(e1-E)
             double xv = 0.0;
             if (!last) {
-                const int e1 = fetch_block(C, b + 1, hn, epoch, g_sm.rhs);
+                int e1;
+                if (paired_lo) {
+                    cl.sync();  // partner wrote y~_{b+1} and its exponent into yrecv / erecv
+                    if (C.tid < TB) g_sm.rhs[C.tid] = (C.tid < hn) ? g_sm.yrecv[C.tid] : 0.0;
+                    e1 = g_sm.erecv;
+                    __syncthreads();
+                } else {
+                    e1 = fetch_block(C, b + 1, hn, epoch, g_sm.rhs);
+                }
                 if (tt) tt[4 * b + 1] = gtime() + (g_sm.rhs[0] != g_sm.rhs[0] ? 1 : 0);  // depends on the staged data
                 double sa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -525,6 +583,15 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             a.bexp[b] = e;
             st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
             if (tt) tt[4 * b + 2] = gtime();
+        }
+        if (!paired_lo) {
+            // hand y~_b (this CTA's values, exponent e) to the lo partner's shared memory
+            PanelSmem *peer = cl.map_shared_rank(&g_sm, 1);
+            if (C.tid < TB) peer->yrecv[C.tid] = (C.tid < h) ? a.vy[r0 + C.tid] : 0.0;
+            if (C.tid == 0) peer->erecv = e;
+            cl.sync();
+        } else if (!(safe && !last)) {
+            cl.sync();  // lo blocks that did not wait on the handoff still complete the cluster phase
         }
     }
     __syncthreads();
@@ -923,7 +990,6 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             {
                 for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tgb, C.rb0 + rl);
                 __syncthreads();
-                double *out = C.mypart();
                 double *stg = g_dyn;
                 for (int c = C.warp; c < ku; c += NWP) {
                     double s = 0.0;
@@ -935,7 +1001,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
                 for (int c = C.tid; c < ku; c += PNT) {
                     double t = 0.0;
                     for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
-                    out[c] = t;
+                    C.putpart(c, t);
                 }
             }
             grid.sync();
@@ -1180,8 +1246,24 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         int rc = ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size());
         if (rc) return rc;
     }
-    void *args[] = {(void *)a};
-    HT_CUDA_TRY(cudaLaunchCooperativeKernel((void *)panel_kernel, dim3(nblocks), dim3(PNT), args,
-                                            DYN_DOUBLES * sizeof(double), st));
+    // cooperative launch (grid barriers) in clusters of 2 CTAs (the solve hands blocks over
+    // through distributed shared memory); the grid is even
+    nblocks &= ~1;
+    if (nblocks < 2) nblocks = 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nblocks);
+    cfg.blockDim = dim3(PNT);
+    cfg.dynamicSmemBytes = DYN_DOUBLES * sizeof(double);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    HT_CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_kernel, *a));
     return 0;
 }
