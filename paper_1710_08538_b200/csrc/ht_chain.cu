@@ -14,6 +14,7 @@
 //
 // Left applies X(rows, cols) <- Qhat^T X are the same operation on the transposed
 // view (slab = columns, window dimension = rows).
+#include <algorithm>
 #include "ht_common.cuh"
 #include "ht_internal.h"
 
@@ -210,7 +211,173 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     }  // task loop
 }
 
+// ---------------------------------------------------------------------------
+// Band apply from the compact-WY factors (ht_band_wy): Qhat = Q_0 Q_1 ... with one
+// 32-column panel block Q_b = I - V_b T_b V_b^T per factorization panel (only the
+// diagonal 32x32 blocks of T are used), so that on the slab view S (8 slabs per CTA)
+//   for b = 0, 1, ...:   Y = S V_b,  Y2 = Y T_b,  S -= Y2 V_b^T        (DMMA m8n8k4)
+// With ident = 1 the slabs start as rows of the identity: the CTA rows of Qhat itself
+// (the explicit window transform the chained applies stream, ht_chain_apply).
+struct BandDesc {
+    double *X;
+    int64_t ld;
+    int left, ident;
+    int64_t s0;
+    int cnt;
+    int64_t o;
+    int p, q;
+    const double *V;
+    int64_t ldv;
+    const double *T;
+    int64_t ldt;
+};
+constexpr int BPW = 32;  // panel width of the factorization (ht_factor.cu PBW)
+
+__global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, const __grid_constant__ BandDesc one)
+{
+    extern __shared__ __align__(16) double bsm[];
+    const BandDesc &A = descs ? descs[blockIdx.y] : one;
+    if (8 * (int)blockIdx.x >= A.cnt) return;
+    const int p = A.p, q = A.q;
+    const int p8 = (p + 7) & ~7;
+    const int lds = ((p8 + 31) & ~31) + 8;  // == 8 mod 32: conflict-free A fragments
+    constexpr int LDY = BPW + 8;
+    double *Ss = bsm;                  // [8][lds]  slab rows (window dimension contiguous)
+    double *Yp = Ss + 8 * lds;         // [2][8][LDY]  K-half partials of S V_b
+    double *Y2 = Yp + 16 * LDY;        // [8][LDY]  S V_b T_b
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+    const int64_t sb = A.s0 + 8 * (int64_t)blockIdx.x;
+    const int ns = min(8, A.cnt - 8 * (int)blockIdx.x);
+    auto xp = [&](int s, int c) -> double * {
+        return A.left ? A.X + (sb + s) * A.ld + A.o + c : A.X + (A.o + c) * A.ld + sb + s;
+    };
+    for (int i = tid; i < 8 * p8; i += 256) {
+        int s, c;
+        if (A.left) { s = i / p8; c = i % p8; }  // contiguous along c
+        else { c = i >> 3; s = i & 7; }          // contiguous along s
+        double v = 0.0;
+        if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
+        Ss[s * lds + c] = v;
+    }
+    const int nblk = (q + BPW - 1) / BPW;
+    for (int b = 0; b < nblk; ++b) {
+        const int j0 = b * BPW, nc = min(BPW, q - j0);
+        __syncthreads();
+        // Y = S V_b: warp = (n-tile, K half); B fragments V(k, j0 + n) from L2
+        {
+            const int nt = warp & 3, kh = warp >> 2;
+            const int n = 8 * nt + g;
+            const double *vc = A.V + (int64_t)(j0 + n) * A.ldv;
+            const int kb = kh * (p8 / 2 & ~3), ke = kh ? p8 : (p8 / 2 & ~3);
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+            for (int k = kb; k < ke; k += 32) {
+                double bv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int kr = k + 4 * u + t4;
+                    bv[u] = (n < nc && kr < p && k + 4 * u < ke) ? vc[kr] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    if (k + 4 * u < ke) dmma(c0, c1, Ss[g * lds + k + 4 * u + t4], bv[u]);
+                    if (k + 4 * u + 4 < ke) dmma(d0, d1, Ss[g * lds + k + 4 * u + 4 + t4], bv[u + 1]);
+                }
+            }
+            Yp[(kh * 8 + g) * LDY + 8 * nt + 2 * t4] = c0 + d0;
+            Yp[(kh * 8 + g) * LDY + 8 * nt + 2 * t4 + 1] = c1 + d1;
+        }
+        __syncthreads();
+        // Y2 = Y T_b (T_b upper, diagonal block of T): warps 0..3, one n-tile each
+        if (warp < 4) {
+            const int nt = warp, n = 8 * nt + g;
+            const double *tc = A.T + (int64_t)(j0 + n) * A.ldt + j0;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < BPW; k += 4) {
+                if (k < 8 * nt + 8) {
+                    const int kr = k + t4;
+                    const double bv = (n < nc && kr <= n) ? tc[kr] : 0.0;
+                    const double av = Yp[g * LDY + kr] + Yp[(8 + g) * LDY + kr];
+                    dmma(c0, c1, av, bv);
+                }
+            }
+            Y2[g * LDY + 8 * nt + 2 * t4] = c0;
+            Y2[g * LDY + 8 * nt + 2 * t4 + 1] = c1;
+        }
+        __syncthreads();
+        // S -= Y2 V_b^T: B fragments V^T(k, n) = V(n, j0 + k)
+        for (int nt = warp; nt < p8 / 8; nt += 8) {
+            const int n = 8 * nt + g;
+            double bv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int kr = 4 * u + t4;
+                bv[u] = (n < p && kr < nc) ? A.V[(int64_t)(j0 + kr) * A.ldv + n] : 0.0;
+            }
+            double c0 = Ss[g * lds + 8 * nt + 2 * t4], c1 = Ss[g * lds + 8 * nt + 2 * t4 + 1];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dmma(c0, c1, -Y2[g * LDY + 4 * u + t4], bv[u]);
+            Ss[g * lds + 8 * nt + 2 * t4] = c0;
+            Ss[g * lds + 8 * nt + 2 * t4 + 1] = c1;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < 8 * p8; i += 256) {
+        int s, c;
+        if (A.left) { s = i / p8; c = i % p8; }
+        else { c = i >> 3; s = i & 7; }
+        if (s < ns && c < p) *xp(s, c) = Ss[s * lds + c];
+    }
+}
+
+size_t band_smem(int pmax)
+{
+    const int p8 = (pmax + 7) & ~7;
+    return (size_t)(8 * (((p8 + 31) & ~31) + 8) + 24 * (BPW + 8)) * sizeof(double);
+}
+int band_init()
+{
+    static bool init = false;
+    if (!init) {
+        HT_CUDA_TRY(cudaFuncSetAttribute(band_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        init = true;
+    }
+    return 0;
+}
+
 }  // namespace
+
+int ht_band_wy(cudaStream_t st, double *X, int64_t ld, int left, int64_t s0, int64_t cnt, int64_t o, int p, int q,
+               const double *V, int64_t ldv, const double *T, int64_t ldt)
+{
+    if (cnt <= 0 || p <= 0 || q <= 0) return 0;
+    if (band_init()) return 2;
+    BandDesc A{X, ld, left, 0, s0, (int)cnt, o, p, q, V, ldv, T, ldt};
+    band_wy_kernel<<<(unsigned)((cnt + 7) / 8), 256, band_smem(p), st>>>(nullptr, A);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// Explicit Qhat (p x p, ld p) of nw windows: window i has Qw[i], V[i] (p x q, ld p), T[i]
+// (diagonal 32x32 blocks, ld q).  d_descs: device scratch for nw descriptors, h_descs pinned.
+int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const int *q, const double *const *V,
+                 const double *const *T, void *d_descs, void *h_descs)
+{
+    if (nw <= 0) return 0;
+    if (band_init()) return 2;
+    BandDesc *hd = reinterpret_cast<BandDesc *>(h_descs);
+    int pmax = 0;
+    for (int i = 0; i < nw; ++i) {
+        hd[i] = BandDesc{Qw[i], p[i], 0, 1, 0, p[i], 0, p[i], q[i], V[i], p[i], T[i], q[i]};
+        pmax = std::max(pmax, p[i]);
+    }
+    HT_CUDA_TRY(cudaMemcpyAsync(d_descs, hd, nw * sizeof(BandDesc), cudaMemcpyHostToDevice, st));
+    const dim3 grid((unsigned)((pmax + 7) / 8), (unsigned)nw);
+    band_wy_kernel<<<grid, 256, band_smem(pmax), st>>>(reinterpret_cast<const BandDesc *>(d_descs), BandDesc{});
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+size_t ht_band_desc_size() { return sizeof(BandDesc); }
 
 // Apply a chain of explicit window transforms to up to 3 matrices (one launch).
 // d_wins: device array of nw windows (application order, monotone offsets).

@@ -56,6 +56,10 @@ struct Work {
     // critical path (panel, B, factorization chains) on a high-priority stream; the A
     // and Q/Z window applies on two low-priority streams that overlap the chains
     cudaStream_t hp_stream = nullptr, sA = nullptr, sQZ = nullptr;
+    // sB (high priority): Qhat formation and the full-height B updates of the R3/L3
+    // windows; the critical stream only updates the band the next window reads
+    cudaStream_t sB = nullptr;
+    cudaEvent_t evF = nullptr, evE = nullptr;
     cudaEvent_t ev[12] = {};
     double *W1A = nullptr, *W2A = nullptr, *W1Q = nullptr, *W2Q = nullptr;
     // window stores of the R3 and L3 chains (their A/Z/Q applies run after the chain)
@@ -66,7 +70,7 @@ struct Work {
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
     int *dsafe = nullptr;
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
-    LarftDesc *d_ld = nullptr, *h_ld = nullptr;
+    void *d_bd = nullptr, *h_bd = nullptr;  // band/Qhat-formation descriptors (one per factor descriptor)
     ChainWin *d_cw = nullptr, *h_cw = nullptr;
     int64_t ndesc = 0, ncw = 0, fd_cur = 0, ld_cur = 0, cw_cur = 0;
 };
@@ -148,18 +152,19 @@ void work_free(Work &w)
     w.Dinv = nullptr;
     w.dsafe = nullptr;
     if (w.d_fd) cudaFree(w.d_fd);
-    if (w.d_ld) cudaFree(w.d_ld);
     if (w.h_out) cudaFreeHost(w.h_out);
     if (w.h_scal) cudaFreeHost(w.h_scal);
     if (w.h_iflags) cudaFreeHost(w.h_iflags);
     if (w.h_fd) cudaFreeHost(w.h_fd);
-    if (w.h_ld) cudaFreeHost(w.h_ld);
     if (w.d_cw) cudaFree(w.d_cw);
     if (w.h_cw) cudaFreeHost(w.h_cw);
+    if (w.d_bd) cudaFree(w.d_bd);
+    if (w.h_bd) cudaFreeHost(w.h_bd);
+    w.d_bd = w.h_bd = nullptr;
     w.d_cw = nullptr; w.h_cw = nullptr;
     w.bexp = nullptr; w.d_out = nullptr; w.d_iflags = nullptr; w.d_force = nullptr;
-    w.d_fd = nullptr; w.d_ld = nullptr; w.h_out = nullptr; w.h_scal = nullptr; w.h_iflags = nullptr;
-    w.h_fd = nullptr; w.h_ld = nullptr;
+    w.d_fd = nullptr; w.h_out = nullptr; w.h_scal = nullptr; w.h_iflags = nullptr;
+    w.h_fd = nullptr;
     w.ncap = w.nbcap = 0;
 }
 
@@ -229,7 +234,11 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
         if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return HT_ECUDA;
         if (cudaStreamCreateWithPriority(&w.hp_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
             cudaStreamCreateWithPriority(&w.sA, cudaStreamNonBlocking, lo) != cudaSuccess ||
-            cudaStreamCreateWithPriority(&w.sQZ, cudaStreamNonBlocking, lo) != cudaSuccess)
+            cudaStreamCreateWithPriority(&w.sQZ, cudaStreamNonBlocking, lo) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&w.sB, cudaStreamNonBlocking, hi) != cudaSuccess)
+            return HT_ECUDA;
+        if (cudaEventCreateWithFlags(&w.evF, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&w.evE, cudaEventDisableTiming) != cudaSuccess)
             return HT_ECUDA;
         for (auto &e : w.ev)
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return HT_ECUDA;
@@ -243,9 +252,9 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     w.ndesc = 4 * (N + 16);
     w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
-    if (cudaMalloc((void **)&w.d_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
-    if (cudaMallocHost((void **)&w.h_ld, w.ndesc * sizeof(LarftDesc)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc(&w.d_bd, w.ndesc * ht_band_desc_size()) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost(&w.h_bd, w.ndesc * ht_band_desc_size()) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_cw, w.ncw * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_cw, w.ncw * sizeof(ChainWin)) != cudaSuccess) return HT_ENOMEM;
     w.ncap = N;
@@ -254,10 +263,55 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     return 0;
 }
 
+// Critical-stream phase profile (HT_PHASES=1, development only): the time between two
+// consecutive marks on the high-priority stream is charged to the later mark's phase.
+struct Phases {
+    bool on = getenv("HT_PHASES") != nullptr;
+    std::vector<cudaEvent_t> pool;
+    std::vector<int> cls;
+    double acc[16] = {0};
+    void mark(cudaStream_t st, int c)
+    {
+        if (!on) return;
+        if (cls.size() == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        cudaEventRecord(pool[cls.size()], st);
+        cls.push_back(c);
+    }
+    void resolve()  // every recorded mark has completed
+    {
+        if (!on || cls.empty()) return;
+        for (size_t i = 1; i < cls.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pool[i - 1], pool[i]);
+            acc[cls[i]] += ms * 1e-3;
+        }
+        std::swap(pool[0], pool[cls.size() - 1]);
+        cls.assign(1, 0);
+    }
+    void print()
+    {
+        if (!on) return;
+        static const char *nm[16] = {"panel", "pre-R1", "R2 B+W", "R3 rest", "L1 wait", "L2", "L3 rest", "join",
+                                     "factor", "form", "B apply", "", "", "", "", ""};
+        fprintf(stderr, "[ht phases] critical stream (s):");
+        for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.3f", nm[i], acc[i]);
+        fprintf(stderr, "\n");
+    }
+    ~Phases()
+    {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 // One reduction in flight.
 struct Run {
     Work *w;
     Timer tm;
+    Phases ph;
     cudaStream_t st;
     int64_t n, nb;
     double *A, *B, *Q, *Z;
@@ -290,14 +344,6 @@ struct Run {
         HT_CUDA_TRY(cudaEventRecord(w->ev[slot], from));
         HT_CUDA_TRY(cudaStreamWaitEvent(s, w->ev[slot], 0));
         return 0;
-    }
-    int gemm_multi_on(cudaStream_t s, char ta, char tb, const std::vector<GemmBatchItem> &it)
-    {
-        if (it.empty()) return 0;
-        tm.begin(s, 1, (int)((it.size() + 15) / 16));
-        int rc = ht_gemm_multi(s, ta, tb, it.data(), (int)it.size());
-        tm.end(s);
-        return rc;
     }
     int copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd)
     {
@@ -363,9 +409,10 @@ struct Run {
     Win add_win(int p, int q) { return add_win(wins, p, q); }
 
     // Factor the windows `ws` (descriptors `fds`, one per window) on stream `s` with the
-    // window store `sto`, then form Qw = I - V T V^T for each.
+    // window store `sto`, then form Qw = I - V T V^T for each (on `sf` if given: it waits
+    // for the factorization through evF).
     int factor_and_form(const std::vector<FactorDesc> &fds, const std::vector<Win> &ws, const Store &sto,
-                        cudaStream_t s)
+                        cudaStream_t s, cudaStream_t sf = nullptr)
     {
         const int nd = (int)fds.size();
         if (nd == 0) return 0;
@@ -384,19 +431,29 @@ struct Run {
         tm.begin(s, 2);
         TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
         tm.end(s);
-        std::vector<GemmBatchItem> it(nd);
-        // Wt = V T
+        if (s == st) ph.mark(st, 8);
+        if (sf) {
+            HT_CUDA_TRY(cudaEventRecord(w->evF, s));
+            HT_CUDA_TRY(cudaStreamWaitEvent(sf, w->evF, 0));
+            s = sf;
+        }
+        // Qw = Q_0 Q_1 ... (panel blocks of the factorization, ht_form_qhat)
+        std::vector<double *> qp(nd);
+        std::vector<const double *> vp(nd), tp(nd);
+        std::vector<int> pp(nd), qq(nd);
         for (int i = 0; i < nd; ++i) {
             const Win &x = ws[i];
-            it[i] = GemmBatchItem{sto.Vhat + x.ov, sto.Tm + x.og, sto.Wt + x.ov, x.p, x.q, x.p, x.p, x.q, x.q, 1.0, 0.0, 0.0};
+            qp[i] = sto.Qw + x.oq;
+            vp[i] = sto.Vhat + x.ov;
+            tp[i] = sto.Tm + x.og;
+            pp[i] = x.p;
+            qq[i] = x.q;
         }
-        TRY(gemm_multi_on(s, 'N', 'N', it));
-        // Qw = I - Wt V^T
-        for (int i = 0; i < nd; ++i) {
-            const Win &x = ws[i];
-            it[i] = GemmBatchItem{sto.Wt + x.ov, sto.Vhat + x.ov, sto.Qw + x.oq, x.p, x.p, x.p, x.p, x.p, x.q, -1.0, 0.0, 1.0};
-        }
-        TRY(gemm_multi_on(s, 'N', 'T', it));
+        tm.begin(s, 1);
+        TRY(ht_form_qhat(s, nd, qp.data(), pp.data(), qq.data(), vp.data(), tp.data(),
+                         (char *)w->d_bd + w->fd_cur * ht_band_desc_size(), (char *)w->h_bd + w->fd_cur * ht_band_desc_size()));
+        tm.end(s);
+        if (s == st) ph.mark(st, 9);
         w->fd_cur += nd;
         return 0;
     }
@@ -505,45 +562,55 @@ struct Run {
             fds.push_back(FactorDesc{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1,
                                      w->Vhat + x.ov, p, w->tau + x.ot});
         }
+        ph.mark(st, 1);
         TRY(factor_and_form(fds, 0));
-        TRY(dep(sA, st, 3));  // R1 windows and L^_1 (written into VW) are ready
-        TRY(dep(sQ, st, 3));
         // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e) =====
+        // B (critical) first with the whole GPU; A (sA) and Z (sQZ) start after it.
         const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
+        std::vector<ChainWin> wl;
+        for (int i = 0; i < r; ++i) {
+            const Win &x = wins[i];
+            wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
+        }
+        TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
+        // W-updates: B on st, Z on sQZ, A on sA
+        struct WX { double *X; int64_t ld, rows; cudaStream_t s; double *W1, *W2; } wx[2] = {
+            {B, ldb, n, st, w->W1, w->W2}, {wz ? Z + qz0 : nullptr, ldz, qz1 - qz0, sQ, w->W1Q, w->W2Q}};
+        auto wupdate = [&](const WX &e) -> int {
+            if (!e.X || e.rows <= 0) return 0;
+            TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + p0 * e.ld, e.ld, V + p0, n, 0.0, e.W1, n));
+            TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + (n - k) * e.ld, e.ld, L1, ldw, 1.0, e.W1, n));
+            TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.W1, n, T, nb, 0.0, e.W2, n));
+            TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, V + p0, n, 1.0, e.X + p0 * e.ld, e.ld));
+            TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, L1, ldw, 1.0, e.X + (n - k) * e.ld, e.ld));
+            return 0;
+        };
+        TRY(wupdate(wx[0]));
+        TRY(dep(sA, st, 3));  // R1 windows, L^_1 (in VW) ready; B's R2 issued first
+        TRY(dep(sQ, st, 3));
         {
-            std::vector<ChainWin> wl;
-            for (int i = 0; i < r; ++i) {
-                const Win &x = wins[i];
-                wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
-            }
-            TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
             std::vector<ChainWin> wa = wl;
             for (auto &x : wa) x.hi[0] = n;  // A: all rows
             TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wa, SIDE_GRID));
             if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, SIDE_GRID));
         }
-        {
-            // W-updates: B on st, Z on sQZ, A on sA
-            struct WX { double *X; int64_t ld, rows; cudaStream_t s; double *W1, *W2; } wx[2] = {
-                {B, ldb, n, st, w->W1, w->W2}, {wz ? Z + qz0 : nullptr, ldz, qz1 - qz0, sQ, w->W1Q, w->W2Q}};
-            for (auto &e : wx) {
-                if (!e.X || e.rows <= 0) continue;
-                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + p0 * e.ld, e.ld, V + p0, n, 0.0, e.W1, n));
-                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.X + (n - k) * e.ld, e.ld, L1, ldw, 1.0, e.W1, n));
-                TRY(gemm_on(e.s, 'N', 'N', e.rows, k, k, 1.0, e.W1, n, T, nb, 0.0, e.W2, n));
-                TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, V + p0, n, 1.0, e.X + p0 * e.ld, e.ld));
-                TRY(gemm_on(e.s, 'N', 'T', e.rows, k, k, -1.0, e.W2, n, L1, ldw, 1.0, e.X + (n - k) * e.ld, e.ld));
-            }
-            TRY(gemm_on(sA, 'N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
-            TRY(gemm_on(sA, 'N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
-        }
+        TRY(wupdate(wx[1]));
+        TRY(gemm_on(sA, 'N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
+        TRY(gemm_on(sA, 'N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
+        ph.mark(st, 2);
         // ===== R3: RQ staircase restoring B, bottom -> top (sec. 3.3.1 second "e)") =====
-        // factor + apply to B's rows above, window by window (st); A, Z take the whole chain after.
+        // Window t is factored on st; the next window (t-1) reads only the band of rows
+        // [C0, R0) of its columns, which st updates straight from (V, T) (ht_band_wy).
+        // sB forms Qhat and updates the rows above the band (their next reader is window
+        // t-1's band update, which waits for it through evE -- a full factorization later);
+        // A and Z take the windows in batches after sB has formed them.
         const Store sr{w->VhatR, w->QwR, w->TmR, w->tauR, w->WtR, w->fscr};
+        cudaStream_t sBq = serial ? st : w->sB;
+        TRY(dep(sBq, st, 9));  // B after R2
         auto flush_right = [&](std::vector<ChainWin> &ws) -> int {
             if (ws.empty()) return 0;
-            TRY(dep(sA, st, 4));
-            TRY(dep(sQ, st, 4));
+            TRY(dep(sA, sBq, 4));
+            TRY(dep(sQ, sBq, 4));
             TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, ws, SIDE_GRID));
             if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, SIDE_GRID));
             ws.clear();
@@ -551,6 +618,7 @@ struct Run {
         };
         std::vector<Win> winsR;
         std::vector<ChainWin> wr;
+        bool have_e = false;
         for (int t = r; t >= 0; --t) {
             int64_t R0, h, C0, wdt;
             if (t >= 1) {
@@ -568,15 +636,31 @@ struct Run {
             Win x = add_win(winsR, (int)wdt, (int)h);
             std::vector<FactorDesc> f1{FactorDesc{B + (R0 + h - 1) + (C0 + wdt - 1) * ldb, -ldb, -1, (int)wdt, (int)h,
                                                   1, sr.Vhat + x.ov, wdt, sr.tau + x.ot}};
-            TRY(factor_and_form(f1, std::vector<Win>{x}, sr, st));
-            const ChainWin cw{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {R0, n, n}};
-            TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, R0}}, {cw}, 0));
+            TRY(factor_and_form(f1, std::vector<Win>{x}, sr, st, sBq));
+            // sB: rows [0, C0) of the window's columns
+            const ChainWin cw{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {C0, n, n}};
+            if (C0 > 0) TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, C0}}, {cw}, 0));
+            // st: the band [C0, R0) after the previous window's sB update
+            if (R0 > C0) {
+                if (have_e) HT_CUDA_TRY(cudaStreamWaitEvent(st, w->evE, 0));
+                tm.begin(st, 4);
+                TRY(ht_band_wy(st, B, ldb, 0, C0, R0 - C0, C0, (int)wdt, (int)h, sr.Vhat + x.ov, wdt, sr.Tm + x.og, h));
+                tm.end(st);
+                chain_flops += 4.0 * (double)(R0 - C0) * wdt * h;
+            }
+            if (sBq != st) {
+                HT_CUDA_TRY(cudaEventRecord(w->evE, sBq));
+                have_e = true;
+            }
+            ph.mark(st, 10);
             wr.push_back(ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}});
             if ((int)wr.size() == BATCH || t == 0) TRY(flush_right(wr));  // A, Z take the windows in batches
         }
         TRY(flush_right(wr));
-
+        TRY(dep(st, sBq, 10));  // B complete
+        ph.mark(st, 3);
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
+        ph.mark(st, 4);
         // ===== L2: spike, chain on B, A, Q, W-updates =====
         TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
@@ -623,12 +707,16 @@ struct Run {
                 TRY(gemm_on(sQ, 'N', 'T', nr, 2 * k, k, -1.0, w->W2Q, n, w->UR, ldur, 1.0, Xp, ldq));
             }
         }
+        ph.mark(st, 5);
         // ===== L3: QR staircase restoring B, top -> bottom (sec. 3.3.2f) =====
+        // As R3 with columns: st updates the next window's columns [R0+q, R0+q+qn) from
+        // (V, T), sB forms Qhat and updates the columns to their right.
         const Store sb{w->VhatB, w->QwB, w->TmB, w->tauB, w->WtB, w->fscr};
+        TRY(dep(sBq, st, 9));
         auto flush_left = [&](std::vector<ChainWin> &ws) -> int {
             if (ws.empty()) return 0;
-            TRY(dep(sA, st, 6));
-            TRY(dep(sQ, st, 6));
+            TRY(dep(sA, sBq, 6));
+            TRY(dep(sQ, sBq, 6));
             TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, SIDE_GRID));
             if (wq) {
                 std::vector<ChainWin> wq_ = ws;
@@ -640,23 +728,42 @@ struct Run {
         };
         std::vector<Win> winsB;
         std::vector<ChainWin> wb;
+        have_e = false;
         for (int t = 0; t <= r; ++t) {
             const int64_t R0 = J + 1 + lb[t];
             const int64_t q = lb[t + 1] - lb[t];
             const int64_t p = (t < r) ? lb[t + 2] - lb[t] : q;
             if (p <= 1) continue;
+            const int64_t qn = (t < r) ? lb[t + 2] - lb[t + 1] : 0;  // columns of the next window
             Win x = add_win(winsB, (int)p, (int)q);
             std::vector<FactorDesc> f1{FactorDesc{B + R0 + R0 * ldb, 1, ldb, (int)p, (int)q, 0, sb.Vhat + x.ov, p,
                                                   sb.tau + x.ot}};
-            TRY(factor_and_form(f1, std::vector<Win>{x}, sb, st));
-            TRY(chain_on(st, {ChainMat{B, ldb, 1, R0 + q, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {R0 + q, 0, 0}, {n, n, n}}}, 0));
+            TRY(factor_and_form(f1, std::vector<Win>{x}, sb, st, sBq));
+            const int64_t c1 = R0 + q + qn;  // sB: columns [c1, n)
+            if (c1 < n)
+                TRY(chain_on(sBq, {ChainMat{B, ldb, 1, c1, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {c1, 0, 0}, {n, n, n}}}, 0));
+            if (qn > 0) {
+                if (have_e) HT_CUDA_TRY(cudaStreamWaitEvent(st, w->evE, 0));
+                tm.begin(st, 4);
+                TRY(ht_band_wy(st, B, ldb, 1, R0 + q, qn, R0, (int)p, (int)q, sb.Vhat + x.ov, p, sb.Tm + x.og, q));
+                tm.end(st);
+                chain_flops += 4.0 * (double)qn * p * q;
+            }
+            if (sBq != st) {
+                HT_CUDA_TRY(cudaEventRecord(w->evE, sBq));
+                have_e = true;
+            }
+            ph.mark(st, 10);
             wb.push_back(ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}});
             if ((int)wb.size() == BATCH) TRY(flush_left(wb));
         }
         TRY(flush_left(wb));
+        TRY(dep(st, sBq, 10));
+        ph.mark(st, 6);
         // join: the next panel reads A and B; U, V, S, T, Y, the window stores are reused
         TRY(dep(st, sA, 7));
         TRY(dep(st, sQ, 8));
+        ph.mark(st, 7);
         return 0;
     }
 
@@ -853,6 +960,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             HT_CUDA_TRY(cudaMalloc((void **)&ttr, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
             HT_CUDA_TRY(cudaMemset(ttr, 0, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
         }
+        unsigned long long *fprof = nullptr;
+        if (getenv("HT_FPROF")) {
+            HT_CUDA_TRY(cudaMalloc((void **)&fprof, 32 * sizeof(unsigned long long)));
+            HT_CUDA_TRY(cudaMemset(fprof, 0, 32 * sizeof(unsigned long long)));
+            TRY(ht_factor_set_prof(fprof));
+        }
         int64_t s0 = 0;
         while (s0 <= n - 3) {
             const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
@@ -881,12 +994,15 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             pa.ptime = ptime;
             const int64_t M = n - s0 - 1;
             int G = (int)std::min<int64_t>(w->gmax, std::max<int64_t>(1, (M + 31) / 32));
+            R.ph.mark(st, 7);
             R.tm.begin(st, 0);
             TRY(ht_panel_run(st, &pa, G));
             R.tm.end(st);
+            R.ph.mark(st, 0);
             HT_CUDA_TRY(cudaMemcpyAsync(w->h_out, w->d_out, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             HT_CUDA_TRY(cudaStreamSynchronize(st));
             R.tm.resolve();
+            R.ph.resolve();
             const int64_t k = w->h_out[0];
             const int failed = (int)w->h_out[1];
             w->epoch = (unsigned)w->h_out[5] + 1;
@@ -913,6 +1029,18 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.3f", names[i], hp[i]);
             fprintf(stderr, "\n");
             cudaFree(ptime);
+        }
+        if (fprof) {
+            HT_CUDA_TRY(cudaDeviceSynchronize());
+            unsigned long long hp[32];
+            HT_CUDA_TRY(cudaMemcpy(hp, fprof, sizeof(hp), cudaMemcpyDeviceToHost));
+            fprintf(stderr, "[ht fprof] factor phases (s): load %.3f left[X %.3f TX %.3f upd %.3f] steps %.3f leafupd %.3f "
+                            "write %.3f G %.3f T %.3f offT %.3f zero %.3f | vt calls %llu stage %.0f dmma %.0f cyc/call\n",
+                    hp[0] * 1e-9, hp[8] * 1e-9, hp[9] * 1e-9, hp[10] * 1e-9, hp[2] * 1e-9, hp[3] * 1e-9, hp[4] * 1e-9,
+                    hp[11] * 1e-9, hp[5] * 1e-9, hp[6] * 1e-9, hp[7] * 1e-9, hp[26], hp[24] / (double)(hp[26] ? hp[26] : 1),
+                    hp[25] / (double)(hp[26] ? hp[26] : 1));
+            TRY(ht_factor_set_prof(nullptr));
+            cudaFree(fprof);
         }
         if (ttr) {
             HT_CUDA_TRY(cudaStreamSynchronize(st));
@@ -958,6 +1086,10 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     HT_CUDA_TRY(cudaStreamWaitEvent(user_st, e1, 0));
     HT_CUDA_TRY(cudaEventSynchronize(e1));
     R.tm.resolve();
+    R.ph.mark(st, 7);
+    HT_CUDA_TRY(cudaStreamSynchronize(st));
+    R.ph.resolve();
+    R.ph.print();
     R.rep.t_panel = R.tm.acc[0];
     R.rep.t_gemm = R.tm.acc[1];
     R.rep.t_factor = R.tm.acc[2];

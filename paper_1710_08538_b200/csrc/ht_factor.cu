@@ -23,8 +23,6 @@
 
 namespace {
 
-constexpr int FNT = 512;  // threads of the factor CTA (16 warps)
-constexpr int FNW = FNT / 32;
 constexpr int PBW = 32;   // panel width (left-looking granularity)
 constexpr int LW = 8;     // leaf width (columns factored one by one)
 constexpr int NLF = PBW / LW;
@@ -76,75 +74,101 @@ __device__ __forceinline__ void house_scalars(double alpha, double ss, double &b
     scal = alpha >= 0.0 ? sc : -sc;
 }
 
-// RPT: rows per thread per leaf; a warp holds 4 row groups x 8 leaf columns, so the
-// CTA covers MAXP = 16 warps * 4 * RPT rows.
-template <int RPT>
+// Layout of one factor CTA.  Two register layouts of the 32-column panel:
+//  * leaf layout (WIDE = false, 512 threads): a warp holds 4 row groups x 8 leaf columns,
+//    RPT rows per thread and leaf, MAXP = 16 warps * 4 * RPT rows;
+//  * wide layout (WIDE = true, 256 threads): lane = panel column, warp w holds rows
+//    w*RPT .. w*RPT+RPT-1 of all 32 columns, MAXP = 8 * RPT rows (p <= 256).
+template <int NT_, int RPT_, bool WIDE_>
 struct FactorSmem {
-    static constexpr int MAXP = FNW * 4 * RPT;
+    static constexpr int NT = NT_, NW = NT / 32, RPT = RPT_;
+    static constexpr bool WIDE = WIDE_;
+    static constexpr int MAXP = WIDE ? NW * RPT : NW * 4 * RPT;
     static constexpr int LDP = MAXP + 4;                       // == 4 mod 32
     static constexpr int RC = MAXP < VRC ? MAXP : VRC;
     static constexpr int LDV = RC + 4;                         // == 4 mod 32
-    static constexpr int VSZ = (PBW * LDV > FNW * LW * PBW) ? PBW * LDV : FNW * LW * PBW;
-    static constexpr int DOUBLES = PBW * LDP + VSZ + PBW * LDX + PBW * LDT + 2 * FNW * LW + 2 * LW + PBW + 2 * 64 + 4 * LW;
+    static constexpr int TPW = 16 / NW;                        // 8x8 tiles of a 32x32 product per warp
+    static constexpr int VSZ = (WIDE || PBW * LDV > NW * LW * PBW) ? PBW * LDV : NW * LW * PBW;
+    static constexpr int DOUBLES = PBW * LDP + VSZ + PBW * LDX + PBW * LDT + 2 * NW * PBW + 2 * PBW + PBW + 2 * 64 + 4 * LW +
+                                   (WIDE ? 2 * MAXP : 0);
 };
 
 // Vs[c][rr] = V(r0 + rr, col0 + c) (view row order), rr < RC, zero beyond `rows`.
 // All loads of a thread are issued before any store (memory-level parallelism).
-template <int RPT>
+template <class L>
 __device__ __forceinline__ void stage_v(const FactorDesc &d, int col0, int r0, int rows, double *Vs)
 {
-    using L = FactorSmem<RPT>;
-    constexpr int PER = (PBW * L::RC + FNT - 1) / FNT;
+    constexpr int PER = (PBW * L::RC + L::NT - 1) / L::NT;
     const int tid = threadIdx.x, p = d.p;
     double t[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
-        const int idx = tid + e * FNT;
+        const int idx = tid + e * L::NT;
         const int c = idx / L::RC, rr = idx % L::RC, r = r0 + rr;
         t[e] = (c < PBW && rr < rows) ? d.V[(int64_t)(col0 + c) * d.ldv + (d.rev ? p - 1 - r : r)] : 0.0;
     }
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
-        const int idx = tid + e * FNT;
+        const int idx = tid + e * L::NT;
         const int c = idx / L::RC, rr = idx % L::RC;
         if (c < PBW) Vs[c * L::LDV + rr] = t[e];
     }
 }
 
 // X(32 x 32) = V_i(r_beg:p, :)^T * Ps(r_beg:p, :) by DMMA (K = rows), V_i = columns
-// 32i..32i+31 of the window's V (view row order).  Warp w computes the 8x8 tile
-// (w/4, w%4) and returns it in (o0, o1) = X(8tm+g, 8tn+2t4 + {0,1}).
-template <int RPT>
+// 32i..32i+31 of the window's V (view row order).  Warp w computes the 8x8 tiles
+// t = w + NW*j (j < TPW), (tm, tn) = (t/4, t%4), and returns them in
+// o[j] = X(8tm+g, 8tn+2t4 + {0,1}).
+template <class L>
 __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r_beg, const double *Ps, double *Vs,
-                                               double &o0, double &o1)
+                                               double (&o)[L::TPW][2])
 {
-    using L = FactorSmem<RPT>;
+    constexpr int TPW = L::TPW, CH = 4;  // 4 independent DMMA chains per tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
     const int p = d.p;
-    const int tm = warp >> 2, tn = warp & 3;
-    double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // 4 independent DMMA chains
+    double x[TPW][CH][2];
+#pragma unroll
+    for (int j = 0; j < TPW; ++j)
+#pragma unroll
+        for (int u = 0; u < CH; ++u) x[j][u][0] = x[j][u][1] = 0.0;
     unsigned long long *fp = g_fprof;
     long long c_a = 0, c_b = 0;
     for (int r0 = r_beg; r0 < p; r0 += L::RC) {
         const int rows = min(L::RC, p - r0);
         __syncthreads();
         if (fp && tid == 0) c_a = clock64();
-        stage_v<RPT>(d, i * PBW, r0, rows, Vs);
+        stage_v<L>(d, i * PBW, r0, rows, Vs);
         __syncthreads();
         if (fp && tid == 0) c_b = clock64() + (Vs[0] != Vs[0] ? 1 : 0);
-        const double *va = Vs + (8 * tm + g) * L::LDV + t4;
-        const double *pb = Ps + (8 * tn + g) * L::LDP + r0 + t4;
-        int kk = 0;
-        for (; kk + 16 <= rows; kk += 16) {
+        const double *va[TPW], *pb[TPW];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) dmma884(x[u][0], x[u][1], va[kk + 4 * u], pb[kk + 4 * u]);
+        for (int j = 0; j < TPW; ++j) {
+            const int t = warp + L::NW * j, tm = t >> 2, tn = t & 3;
+            va[j] = Vs + (8 * tm + g) * L::LDV + t4;
+            pb[j] = Ps + (8 * tn + g) * L::LDP + r0 + t4;
         }
-        for (; kk < rows; kk += 4) dmma884(x[0][0], x[0][1], va[kk], pb[kk]);  // padded rows are 0
+        constexpr int KS = 4 * CH;
+        int kk = 0;
+        for (; kk + KS <= rows; kk += KS) {
+#pragma unroll
+            for (int u = 0; u < CH; ++u)
+#pragma unroll
+                for (int j = 0; j < TPW; ++j) dmma884(x[j][u][0], x[j][u][1], va[j][kk + 4 * u], pb[j][kk + 4 * u]);
+        }
+        for (; kk < rows; kk += 4)  // padded rows are 0
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) dmma884(x[j][0][0], x[j][0][1], va[j][kk], pb[j][kk]);
     }
-    o0 = (x[0][0] + x[1][0]) + (x[2][0] + x[3][0]);
-    o1 = (x[0][1] + x[1][1]) + (x[2][1] + x[3][1]);
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < CH; ++u) { a0 += x[j][u][0]; a1 += x[j][u][1]; }
+        o[j][0] = a0;
+        o[j][1] = a1;
+    }
     if (fp && tid == 0) {
-        const long long c_c = clock64() + (o0 != o0 ? 1 : 0);
+        const long long c_c = clock64() + (o[0][0] != o[0][0] ? 1 : 0);
         atomicAdd(&fp[24], (unsigned long long)(c_b - c_a));
         atomicAdd(&fp[25], (unsigned long long)(c_c - c_b));
         atomicAdd(&fp[26], 1ull);
@@ -158,26 +182,29 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
 //     for each 8-column leaf:    column steps (one block reduction per column gives the
 //                                tail norm and the leaf's dot products), then the leaf's
 //                                8 reflectors update the rest of the panel (WY, T_leaf)
-//   T_b from G = V_b^T V_b (DMMA) by the dlarft recurrence;
-//   T(0:c0, panel b) = -T(0:c0, 0:c0) (V(:, 0:c0)^T V_b) T_b.
+//   T_b from G = V_b^T V_b (DMMA) by the dlarft recurrence.
 // Outputs: R (upper trapezoid, exact zeros below) back through the view, V in natural
-// row order, tau, and the q x q T of Q = H_0 ... H_{q-1} = I - V T V^T.
-// gscratch: >= 64 * q doubles.
-template <int RPT>
-__global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch)
+// row order, tau, and the diagonal 32x32 blocks T_b of T:  Q = H_0 ... H_{q-1} =
+// Q_0 Q_1 ...,  Q_b = I - V_b T_b V_b^T  (V_b = columns 32b..32b+31).  The off-diagonal
+// blocks of T are never formed: every consumer applies Q panel block by panel block
+// (ht_band_wy / ht_form_qhat, ht_chain.cu).  (The 512-thread leaf layout shares this code.)
+template <class L>
+__global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch)
 {
-    using L = FactorSmem<RPT>;
+    constexpr int FNT = L::NT, FNW = L::NW, RPT = L::RPT, TPW = L::TPW;
+    constexpr bool WIDE = L::WIDE;
     extern __shared__ __align__(16) double fsm[];
     double *Ps = fsm;                         // [PBW][LDP]   panel, column-major
     double *Vs = Ps + PBW * L::LDP;           // [PBW][LDV]   staged V_i chunk / leaf partials
     double *Xs = Vs + L::VSZ;                 // [PBW][LDX]   X = T^T V^T P (row-major) / G_b
     double *Ts = Xs + PBW * LDX;              // [PBW][LDT]   T_i (left-looking) / leaf W
-    double *part = Ts + PBW * LDT;            // [2][FNW][LW]
-    double *rowc = part + 2 * FNW * LW;       // [2][LW]
-    double *taus = rowc + 2 * LW;             // [PBW]
+    double *part = Ts + PBW * LDT;            // [2][FNW][LW] (wide: [2][FNW][PBW])
+    double *rowc = part + 2 * FNW * PBW;      // [2][LW]      (wide: [2][PBW])
+    double *taus = rowc + 2 * PBW;            // [PBW]
     double *Zl = taus + PBW;                  // [LW][LW] leaf Z
     double *Tl = Zl + 64;                     // [LW][LW] leaf T
     double *coef = Tl + 64;                   // [2][2][LW] column-step update coefficients
+    double *pivs = coef + 4 * LW;             // wide: [2][MAXP] pivot column (per-warp row slices)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int c8 = lane & 7, rq = lane >> 3;    // leaf column / row group of this lane
@@ -218,23 +245,29 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 const int r_lo = i * PBW;  // V_i is zero above row r_lo
                 __syncthreads();
                 {
-                    const int c = tid / PBW, a = tid % PBW;  // 2 elements per thread, both loads first
-                    const double t0 = Tout(r_lo + a, r_lo + c), t1 = Tout(r_lo + a, r_lo + c + FNT / PBW);
-                    Ts[a * LDT + c] = t0;
-                    Ts[a * LDT + c + FNT / PBW] = t1;  // diagonal block T_i
+                    constexpr int E = PBW * PBW / FNT;  // elements per thread, all loads first
+                    const int c = tid / PBW, a = tid % PBW;
+                    double tv[E];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) tv[e] = Tout(r_lo + a, r_lo + c + e * (FNT / PBW));
+#pragma unroll
+                    for (int e = 0; e < E; ++e) Ts[a * LDT + c + e * (FNT / PBW)] = tv[e];  // diagonal block T_i
                 }
-                double o0, o1;
-                vt_times_panel<RPT>(d, i, r_lo, Ps, Vs, o0, o1);
-                {
-                    const int tm = warp >> 2, tn = warp & 3;
-                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = o0;
-                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = o1;
+                double o[TPW][2];
+                vt_times_panel<L>(d, i, r_lo, Ps, Vs, o);
+#pragma unroll
+                for (int j = 0; j < TPW; ++j) {
+                    const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = o[j][0];
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = o[j][1];
                 }
                 __syncthreads();
                 FPROF(8);
                 // X <- T_i^T X  (T_i upper triangular): X'(a, c) = sum_{l <= a} T(l, a) X(l, c)
-                double xv[2];
-                for (int e = 0; e < 2; ++e) {
+                constexpr int EX = PBW * PBW / FNT;
+                double xv[EX];
+#pragma unroll
+                for (int e = 0; e < EX; ++e) {
                     const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
                     double sa[4] = {0.0, 0.0, 0.0, 0.0};
                     int l = 0;
@@ -246,22 +279,22 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     xv[e] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
                 }
                 __syncthreads();
-                for (int e = 0; e < 2; ++e) {
+#pragma unroll
+                for (int e = 0; e < EX; ++e) {
                     const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
                     Xs[a * LDX + c] = -xv[e];
                 }
                 __syncthreads();
                 FPROF(9);
-                // P -= V_i X : per chunk, warp w owns row tiles {2w, 2w+1} x 4 column tiles
+                // P -= V_i X : per chunk, warp w owns row tiles w, w + FNW, ... x 4 column tiles
                 for (int r0 = r_lo; r0 < p; r0 += L::RC) {
                     const int rows = min(L::RC, p - r0);
                     if (p - r_lo > L::RC) {  // multi-chunk: Vs holds the last chunk -> re-stage
                         __syncthreads();
-                        stage_v<RPT>(d, r_lo, r0, rows, Vs);
+                        stage_v<L>(d, r_lo, r0, rows, Vs);
                         __syncthreads();
                     }
-                    for (int tr = 2 * warp; tr < 2 * warp + 2; ++tr) {
-                        if (8 * tr >= rows) break;
+                    for (int tr = warp; 8 * tr < rows; tr += FNW) {
                         double acc[4][2];
 #pragma unroll
                         for (int tn2 = 0; tn2 < 4; ++tn2) {
@@ -285,6 +318,132 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
             }
             __syncthreads();
             FPROF(10);
+            // R (upper trapezoid of the panel columns) and V go through Ps so that the global
+            // stores are coalesced along the view's contiguous direction.
+            auto store_R = [&]() {
+                __syncthreads();
+                if (rs == 1 || rs == -1) {  // contiguous along rows: lanes over rows
+                    for (int j = warp; j < nc; j += FNW)
+                        for (int r = lane; r < p; r += 32) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = Ps[j * L::LDP + r];
+                } else {                     // contiguous along columns: lanes over columns
+                    for (int r = warp; r < p; r += FNW)
+                        if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = Ps[lane * L::LDP + r];
+                }
+                __syncthreads();
+            };
+            auto store_V = [&]() {
+                __syncthreads();
+                for (int j = warp; j < nc; j += FNW)
+                    for (int r = lane; r < p; r += 32) d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = Ps[j * L::LDP + r];
+            };
+            if constexpr (WIDE) {
+                // ---- wide layout: val[e] = P(w0 + e, c0 + lane), all 32 columns of the panel ----
+                // One column step = every active warp: pivot column of its rows by shuffles,
+                // partial dot products with all 32 columns -> part; ONE barrier; every active
+                // warp sums the partials (same fixed order everywhere, so the scalars agree
+                // bitwise), forms the reflector scalars and updates its own rows of all
+                // later columns.  Rows above the diagonal row dr never change.
+                const int w0 = warp * RPT;
+                double val[RPT];
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) val[e] = Ps[lane * L::LDP + w0 + e];
+                // the pivot column of the next step goes through shared memory: its owner lane
+                // stores the warp's rows, the warp reads them back as broadcasts (a 64-bit
+                // shuffle per element would cost two SHFL per row and lane)
+                auto put_pivot = [&](int jn, int bn) {
+                    if (lane == jn) {
+                        double2 *dst = reinterpret_cast<double2 *>(pivs + bn * L::MAXP + w0);
+#pragma unroll
+                        for (int e = 0; e < RPT; e += 2) dst[e / 2] = make_double2(val[e], val[e + 1]);
+                    }
+                    __syncwarp();
+                };
+                put_pivot(0, 0);
+#pragma unroll
+                for (int jj = 0; jj < PBW; ++jj) {
+                    if (jj >= nc) break;
+                    const int buf = jj & 1;
+                    const int dr = c0 + jj;           // diagonal row of column jj
+                    const int bw = dr / RPT;          // warp holding row dr
+                    const int eo = jj % RPT;          // its element index (c0 % RPT == 0 or RPT % 32 == 0)
+                    const bool act = warp >= bw, own = warp == bw;
+                    double xr[RPT];
+                    const bool cp = fprof && lane == 0 && warp == FNW - 1;
+                    long long ck0 = cp ? clock64() : 0, ck1 = 0, ck2 = 0, ck3 = 0, ck4 = 0;
+                    if (act) {
+                        double sa[4] = {0.0, 0.0, 0.0, 0.0};
+                        const double2 *src = reinterpret_cast<const double2 *>(pivs + buf * L::MAXP + w0);
+#pragma unroll
+                        for (int e = 0; e < RPT; e += 2) {
+                            const double2 t = src[e / 2];
+                            xr[e] = t.x;
+                            xr[e + 1] = t.y;
+                        }
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e) {
+                            const bool on = !own || e > eo;
+                            sa[e & 3] = fma(on ? xr[e] : 0.0, val[e], sa[e & 3]);
+                        }
+                        part[(buf * FNW + warp) * PBW + lane] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+                        if (own) rowc[buf * PBW + lane] = val[eo];
+                        if (cp) ck1 = clock64() + (sa[0] != sa[0] ? 1 : 0);
+                    }
+                    __syncthreads();
+                    if (cp) ck2 = clock64();
+                    if (act) {
+                        double pr[FNW];
+#pragma unroll
+                        for (int w = 0; w < FNW; ++w) pr[w] = (w >= bw) ? part[(buf * FNW + w) * PBW + lane] : 0.0;
+#pragma unroll
+                        for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
+#pragma unroll
+                            for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
+                        const double S = pr[0];                              // v_jj-tail . column lane
+                        const double ss = __shfl_sync(0xffffffffu, S, jj);   // squared tail norm
+                        const double alpha = rowc[buf * PBW + jj];
+                        const double myrow = rowc[buf * PBW + lane];
+                        double tau = 0.0, scal = 0.0, beta = alpha;
+                        if (cp) ck3 = clock64() + (ss != ss ? 1 : 0) + (myrow != myrow ? 1 : 0);
+                        if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
+                        const double wj = tau * (myrow + scal * S);
+                        if (cp) ck4 = clock64() + (wj != wj ? 1 : 0);
+                        // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
+                        const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
+#pragma unroll
+                        for (int e = 0; e < RPT; ++e)
+                            if (!own || e > eo) val[e] = fma(mx, xr[e], val[e]);
+                        if (own) {
+                            val[eo] = lane > jj ? val[eo] - wj : (lane == jj ? beta : val[eo]);
+                            if (lane == jj) taus[jj] = tau;
+                        }
+                        if (jj + 1 < nc) put_pivot(jj + 1, buf ^ 1);
+                    }
+                    if (cp) {
+                        const long long ck5 = clock64() + (val[RPT - 1] != val[RPT - 1] ? 1 : 0);
+                        atomicAdd(&fprof[12], (unsigned long long)(ck1 - ck0));
+                        atomicAdd(&fprof[13], (unsigned long long)(ck2 - ck1));
+                        atomicAdd(&fprof[14], (unsigned long long)(ck3 - ck2));
+                        atomicAdd(&fprof[15], (unsigned long long)(ck4 - ck3));
+                        atomicAdd(&fprof[16], (unsigned long long)(ck5 - ck4));
+                    }
+                }
+                FPROF(2);
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = w0 + e, col = c0 + lane;
+                    Ps[lane * L::LDP + r] = (r <= col && r < p && lane < nc) ? val[e] : 0.0;
+                }
+                store_R();
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = w0 + e, col = c0 + lane;
+                    const double tv = taus[lane < nc ? lane : 0];
+                    const double v = (lane >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[e]));
+                    Ps[lane * L::LDP + r] = (r < p) ? v : 0.0;
+                }
+                store_V();
+            } else {
             // ---- the panel in registers: val[l][e] = P(rw0 + e, 8l + c8) ----
             double val[NLF][RPT];
 #pragma unroll
@@ -479,9 +638,6 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                 FPROF(3);
             }
             __syncthreads();
-            // ---- write R (through the view), V (natural order), tau; V_b stays in Ps ----
-            // R (upper trapezoid of the panel columns) goes through Ps first so that the
-            // global stores are coalesced along the view's contiguous direction.
 #pragma unroll
             for (int l = 0; l < NLF; ++l)
 #pragma unroll
@@ -489,15 +645,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     const int r = rw0 + e, jl = LW * l + c8, col = c0 + jl;
                     Ps[jl * L::LDP + r] = (r <= col && r < p && jl < nc) ? val[l][e] : 0.0;
                 }
-            __syncthreads();
-            if (rs == 1 || rs == -1) {  // contiguous along rows: lanes over rows
-                for (int j = warp; j < nc; j += FNW)
-                    for (int r = lane; r < p; r += 32) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = Ps[j * L::LDP + r];
-            } else {                     // contiguous along columns: lanes over columns
-                for (int r = warp; r < p; r += FNW)
-                    if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = Ps[lane * L::LDP + r];
-            }
-            __syncthreads();
+            store_R();
 #pragma unroll
             for (int l = 0; l < NLF; ++l)
 #pragma unroll
@@ -507,16 +655,16 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     const double v = (jl >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[l][e]));
                     Ps[jl * L::LDP + r] = (r < p) ? v : 0.0;
                 }
-            __syncthreads();
-            for (int j = warp; j < nc; j += FNW)
-                for (int r = lane; r < p; r += 32) d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = Ps[j * L::LDP + r];
+            store_V();
+            }
             if (tid < nc) d.tau[c0 + tid] = taus[tid];
             __threadfence_block();
             FPROF(4);
             // ---- G_b = V_b^T V_b (DMMA) and T_b by the dlarft recurrence (row i per lane) ----
             __syncthreads();
-            {
-                const int tm = warp >> 2, tn = warp & 3;
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) {
+                const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
                 const double *pa = Ps + (8 * tm + g) * L::LDP + t4, *pb = Ps + (8 * tn + g) * L::LDP + t4;
                 double x[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
                 int kk = c0;
@@ -547,7 +695,7 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
                     if (c > i && c < nc) trow[c] = tv;
                 }
                 if (i < nc) {
-                    // row i of T_b -> global T (columns c0..c0+nc) and the shared copy for the off-diagonal step
+                    // row i of T_b -> the diagonal block of the global T (columns c0..c0+nc)
 #pragma unroll
                     for (int c = 0; c < PBW; ++c)
                         if (c < nc) Tout(c0 + i, c0 + c) = trow[c];
@@ -558,121 +706,44 @@ __global__ void __launch_bounds__(FNT, 1) factor_qr_kernel(const FactorDesc *des
             __threadfence_block();
             __syncthreads();
             FPROF(5);
-            // ---- off-diagonal T blocks: T(0:c0, c0:c0+nc) = -T(0:c0,0:c0) G T_b,  G = V(:,0:c0)^T V_b ----
-            if (b > 0) {
-                for (int i = 0; i < b; ++i) {
-                    double o0, o1;
-                    vt_times_panel<RPT>(d, i, c0, Ps, Vs, o0, o1);  // V_i^T V_b (V_b = 0 above row c0)
-                    const int tm = warp >> 2, tn = warp & 3;
-                    gscratch[(size_t)(i * PBW + 8 * tm + g) * PBW + 8 * tn + 2 * t4] = o0;
-                    gscratch[(size_t)(i * PBW + 8 * tm + g) * PBW + 8 * tn + 2 * t4 + 1] = o1;
-                }
-                __threadfence_block();
-                __syncthreads();
-                if (c0 * LDX > PBW * L::LDP || c0 * LDX > L::VSZ) {
-                    // large windows (q > ~200): operands in global memory
-                    double *Yg = gscratch + (size_t)c0 * PBW;
-                    for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
-                        const int tr = tile >> 2, tn = tile & 3;
-                        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-                        for (int kk = 0; kk < PBW; kk += 4)
-                            dmma884(a0, a1, gscratch[(size_t)(8 * tr + g) * PBW + kk + t4], Ts[(kk + t4) * LDT + 8 * tn + g]);
-                        Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4] = a0;
-                        Yg[(size_t)(8 * tr + g) * PBW + 8 * tn + 2 * t4 + 1] = a1;
-                    }
-                    __threadfence_block();
-                    __syncthreads();
-                    for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
-                        const int tr = tile >> 2, tn = tile & 3;
-                        double a0 = 0.0, a1 = 0.0;
-                        for (int kk = 8 * tr; kk < c0; kk += 4) {
-                            const int row = 8 * tr + g, kr = kk + t4;
-                            const double av = (kr >= row) ? Tout(row, kr) : 0.0;
-                            dmma884(a0, a1, av, Yg[(size_t)kr * PBW + 8 * tn + g]);
-                        }
-                        const int row = 8 * tr + g, cc = 8 * tn + 2 * t4;
-                        if (cc < nc) Tout(row, c0 + cc) = -a0;
-                        if (cc + 1 < nc) Tout(row, c0 + cc + 1) = -a1;
-                    }
-                } else {
-                // stage G = [X_0; ...; X_{b-1}] (c0 x 32) into Ps (free now), ld LDX
-                for (int idx = tid; idx < c0 * PBW; idx += FNT) Ps[(idx / PBW) * LDX + idx % PBW] = __ldcg(gscratch + idx);
-                __syncthreads();
-                // Y = G T_b (c0 x 32; T_b upper, zero beyond nc) into Vs, ld LDX: operands in shared memory
-                double *Ys = Vs;
-                for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
-                    const int tr = tile >> 2, tn = tile & 3;
-                    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-                    for (int kk = 0; kk < PBW; kk += 4)
-                        dmma884(a0, a1, Ps[(8 * tr + g) * LDX + kk + t4], Ts[(kk + t4) * LDT + 8 * tn + g]);
-                    Ys[(8 * tr + g) * LDX + 8 * tn + 2 * t4] = a0;
-                    Ys[(8 * tr + g) * LDX + 8 * tn + 2 * t4 + 1] = a1;
-                }
-                __syncthreads();
-                // T(0:c0, c0:c0+nc) = -T(0:c0, 0:c0) Y  (T upper: k from the tile's first row); the
-                // A fragments (rows of the previous T, global) are all loaded before the DMMAs
-                for (int tile = warp; tile < (c0 / 8) * 4; tile += FNW) {
-                    const int tr = tile >> 2, tn = tile & 3;
-                    const int row = 8 * tr + g;
-                    constexpr int MAXK = 128;  // c0 <= 480: chunks of 32 k-steps
-                    double a0 = 0.0, a1 = 0.0;
-                    for (int k0 = 8 * tr; k0 < c0; k0 += MAXK) {
-                        double av[MAXK / 4];
-#pragma unroll
-                        for (int u = 0; u < MAXK / 4; ++u) {
-                            const int kr = k0 + 4 * u + t4;
-                            av[u] = (kr < c0 && kr >= row) ? Tout(row, kr) : 0.0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < MAXK / 4; ++u) {
-                            const int kr = k0 + 4 * u + t4;
-                            if (k0 + 4 * u < c0) dmma884(a0, a1, av[u], kr < c0 ? Ys[kr * LDX + 8 * tn + g] : 0.0);
-                        }
-                    }
-                    const int cc = 8 * tn + 2 * t4;
-                    if (cc < nc) Tout(row, c0 + cc) = -a0;
-                    if (cc + 1 < nc) Tout(row, c0 + cc + 1) = -a1;
-                }
-                }
-            }
-            FPROF(6);
-            // zeros below the diagonal block
-            for (int idx = tid; idx < nc * (q - c0); idx += FNT) {
-                const int c = idx / (q - c0), a = c0 + idx % (q - c0);
-                if (a > c0 + c) Tout(a, c0 + c) = 0.0;
-            }
-            __threadfence_block();
-            __syncthreads();
-            FPROF(7);
         }
         __threadfence();
         __syncthreads();
     }
 }
 
-template <int RPT>
+template <class L>
 int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch)
 {
-    const int smem = FactorSmem<RPT>::DOUBLES * (int)sizeof(double);
+    const int smem = L::DOUBLES * (int)sizeof(double);
     static bool init = false;
     if (!init) {
-        HT_CUDA_TRY(cudaFuncSetAttribute(factor_qr_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HT_CUDA_TRY(cudaFuncSetAttribute(factor_qr_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         init = true;
     }
-    factor_qr_kernel<RPT><<<1, FNT, smem, st>>>(d_descs, nd, gscratch);
+    factor_qr_kernel<L><<<1, L::NT, smem, st>>>(d_descs, nd, gscratch);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
 
+using FWide128 = FactorSmem<256, 16, true>;   // p <= 128
+using FWide256 = FactorSmem<256, 32, true>;   // p <= 256
+using FLeaf512 = FactorSmem<512, 8, false>;   // p <= 512
+
 }  // namespace
+
+// Development profile of the factorization phases (HT_FPROF): dev = 32 zeroed counters or null.
+int ht_factor_set_prof(unsigned long long *dev)
+{
+    HT_CUDA_TRY(cudaMemcpyToSymbol(g_fprof, &dev, sizeof(dev)));
+    return 0;
+}
 
 int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp)
 {
     if (nd <= 0) return 0;
-    if (maxp <= FactorSmem<2>::MAXP) return launch_factor<2>(st, d_descs, nd, gscratch);
-    if (maxp <= FactorSmem<4>::MAXP) return launch_factor<4>(st, d_descs, nd, gscratch);
-    if (maxp <= FactorSmem<8>::MAXP) return launch_factor<8>(st, d_descs, nd, gscratch);
+    if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch);
+    if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch);
+    if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch);
     return 4;  // HT_ENUMERIC: window taller than 512 rows (nb <= 256 guarantees p <= 512)
 }

@@ -18,14 +18,6 @@ struct FactorDesc {
     double *T;     // q x q upper-triangular compact-WY factor of Q = H_0 H_1 ... H_{q-1}
     int64_t ldt;
 };
-struct LarftDesc {
-    const double *G;  // V^T V (q x q)
-    int64_t ldg;
-    const double *tau;
-    double *T;  // out (q x q, upper)
-    int64_t ldt;
-    int q;
-};
 
 // chained window applies (ht_chain.cu): per matrix, slab dimension s in [s_begin, s_end)
 // (rows if !left, columns if left), window dimension c; element (s, c) is X[s + c*ld]
@@ -45,9 +37,21 @@ struct ChainWin {
 };
 int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax,
                    int maxgrid = 0);  // maxgrid > 0: at most that many CTAs (they loop over the slabs)
+// One window transform applied to a narrow band of slabs straight from its factors (no
+// explicit Qhat): on the slab view S(s, c) (element X[s + c*ld] for a right apply,
+// X[c + s*ld] for a left apply; s in [s0, s0+cnt), c in [0, p) offset by o)
+//   S <- S Q_0 Q_1 ...,  Q_b = I - V_b T_b V_b^T  (32-column panel blocks of V, p x q,
+// ld ldv, and the diagonal 32x32 blocks T_b of T, ld ldt), i.e. X <- X Qhat (right) or
+// X <- Qhat^T X (left).  8 slabs per CTA.
+int ht_band_wy(cudaStream_t st, double *X, int64_t ld, int left, int64_t s0, int64_t cnt, int64_t o, int p, int q,
+               const double *V, int64_t ldv, const double *T, int64_t ldt);
+// Explicit Qhat = Q_0 Q_1 ... (p x p, ld p) for nw windows (the same kernel on identity rows).
+int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const int *q, const double *const *V,
+                 const double *const *T, void *d_descs, void *h_descs);
+size_t ht_band_desc_size();
 
 int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp);
-int ht_larft_run(cudaStream_t st, const LarftDesc *d_descs, int nd);
+int ht_factor_set_prof(unsigned long long *dev);
 
 // panel kernel (ht_panel.cu)
 struct PanelArgs {

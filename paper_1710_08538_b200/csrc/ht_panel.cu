@@ -746,7 +746,30 @@ __device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_
         const int cw0 = C.warp * (TCW / NWP);  // 16 columns per warp
         const bool diag = tg.tri && (r0 + TRT - 1 > c0);
         const bool full = (r0 + TRT <= tg.r_end);
-        if (vec && full && !diag) {
+        if (vec && full && diag) {
+            // triangular item: vector loads, entries below the diagonal masked out
+#pragma unroll 1
+            for (int u0 = 0; u0 < TCW / NWP; u0 += 2) {
+                double2 xv[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int64_t c = c0 + cw0 + u0 + u;
+                    const double2 *col = reinterpret_cast<const double2 *>(X + (size_t)(c < tg.c_end ? c : c0) * ldx + r0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[u][i] = col[C.lane + 32 * i];
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const double v = vs[cw0 + u0 + u];
+                    const int kk = (int)(c0 - r0) + cw0 + u0 + u - 2 * C.lane;  // c - r(i=0,h=0)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        acc[2 * i] = fma(64 * i > kk ? 0.0 : xv[u][i].x, v, acc[2 * i]);
+                        acc[2 * i + 1] = fma(64 * i + 1 > kk ? 0.0 : xv[u][i].y, v, acc[2 * i + 1]);
+                    }
+                }
+            }
+        } else if (vec && full) {
 #pragma unroll 1
             for (int u0 = 0; u0 < TCW / NWP; u0 += 4) {
                 double2 xv[4][4];

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cmath>
+#include <algorithm>
 int ht_cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 {
     fprintf(stderr, "CUDA error %s at %s:%d (%s)\n", cudaGetErrorString(e), file, line, what);
@@ -44,6 +45,8 @@ int main(int argc, char **argv)
         if (it < reps) best = ms < best ? ms : best;
     }
     unsigned long long hp[32]; cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost);
+    printf("wide column step cycles/col (last warp): loads+dots %.0f bar %.0f partials+sum %.0f house %.0f update %.0f\n",
+           hp[12] / (double)q, hp[13] / (double)q, hp[14] / (double)q, hp[15] / (double)q, hp[16] / (double)q);
     printf("column step cycles/col: warp0 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]  warp15 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]\n",
            hp[12] / (double)q, hp[13] / (double)q, hp[14] / (double)q, hp[15] / (double)q, hp[16] / (double)q,
            hp[17] / (double)q, hp[18] / (double)q, hp[19] / (double)q, hp[20] / (double)q, hp[21] / (double)q);
@@ -59,28 +62,41 @@ int main(int argc, char **argv)
     cudaMemcpy(T.data(), dT, T.size() * 8, cudaMemcpyDeviceToHost);
     // view accessors on host (natural storage index)
     auto vidx = [&](int i, int j) -> size_t { return rev ? (size_t)(p - 1 - i) + (size_t)(q - 1 - j) * p : (size_t)i + (size_t)j * p; };
-    // Qv = I - Vv T Vv^T in view row order (Vv(i,j) = V(nat(i), j))
+    // Q = Q_0 Q_1 ..., Q_b = I - V_b T_b V_b^T (32-column blocks, view row order Vv(i,j) = V(nat(i), j));
+    // X = R, then X <- Q_b X for b = last .. 0, compare with W0
     double maxres = 0, nrm = 0, maxlow = 0;
-    std::vector<double> VT((size_t)p * q, 0.0);  // Vv * T
+    std::vector<double> X((size_t)p * q);
     for (int i = 0; i < p; ++i)
         for (int j = 0; j < q; ++j) {
-            double s = 0;
-            for (int l = 0; l <= j; ++l) s += V[(size_t)l * p + (rev ? p - 1 - i : i)] * T[(size_t)j * q + l];
-            VT[(size_t)j * p + i] = s;
-        }
-    for (int i = 0; i < p; ++i)
-        for (int j = 0; j < q; ++j) {
-            // (Qv R)(i, j) = R(i,j) - sum_l VT(i,l) * (Vv^T R)(l, j)
-            double r = 0;
-            double acc = (i <= j) ? Wf[vidx(i, j)] : 0.0;
+            X[(size_t)j * p + i] = (i <= j) ? Wf[vidx(i, j)] : 0.0;
             if (i > j && Wf[vidx(i, j)] != 0.0) maxlow = fmax(maxlow, fabs(Wf[vidx(i, j)]));
-            for (int l = 0; l < q; ++l) {
-                double vr = 0;
-                for (int m = 0; m <= j && m < p; ++m) vr += V[(size_t)l * p + (rev ? p - 1 - m : m)] * Wf[vidx(m, j)] * (m <= j);
-                acc -= VT[(size_t)l * p + i] * vr;
+        }
+    auto Vv = [&](int i, int l) { return V[(size_t)l * p + (rev ? p - 1 - i : i)]; };
+    const int nbk = (q + 31) / 32;
+    for (int b = nbk - 1; b >= 0; --b) {
+        const int j0 = 32 * b, nc = std::min(32, q - j0);
+        for (int j = 0; j < q; ++j) {
+            double y[32], z[32];
+            for (int l = 0; l < nc; ++l) {
+                double sacc = 0;
+                for (int i = 0; i < p; ++i) sacc += Vv(i, j0 + l) * X[(size_t)j * p + i];
+                y[l] = sacc;
             }
-            (void)r;
-            maxres = fmax(maxres, fabs(acc - W0[vidx(i, j)]));
+            for (int l = 0; l < nc; ++l) {
+                double sacc = 0;
+                for (int m = l; m < nc; ++m) sacc += T[(size_t)(j0 + m) * q + j0 + l] * y[m];
+                z[l] = sacc;
+            }
+            for (int i = 0; i < p; ++i) {
+                double sacc = 0;
+                for (int l = 0; l < nc; ++l) sacc += Vv(i, j0 + l) * z[l];
+                X[(size_t)j * p + i] -= sacc;
+            }
+        }
+    }
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < q; ++j) {
+            maxres = fmax(maxres, fabs(X[(size_t)j * p + i] - W0[vidx(i, j)]));
             nrm = fmax(nrm, fabs(W0[vidx(i, j)]));
         }
     printf("check: max |Q R - W0| / max|W0| = %.2e, nonzero below diag = %.2e\n", maxres / nrm, maxlow);
