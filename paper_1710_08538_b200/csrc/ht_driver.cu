@@ -14,6 +14,7 @@
 //   Remark 4: first right window has kt rows, k < kt <= 2k, k | (m-kt);
 //         restore chunks are aligned to the window boundaries.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -81,47 +82,56 @@ Work g_work[16];
 // Per-kernel-class device time from CUDA events recorded on the launch stream.
 // Classes: 0 panel, 1 DMMA GEMM, 2 factorizations, 3 other, 4 chained window applies.
 struct Timer {
-    std::vector<cudaEvent_t> pool;
-    size_t used = 0;
-    std::vector<std::pair<int, size_t>> pending;
+    std::vector<cudaEvent_t> all, free_;
+    struct Pend { int cls; cudaEvent_t a, b; };
+    std::vector<Pend> pending;
     double acc[5] = {0, 0, 0, 0, 0};
     int64_t launches = 0;
     int cls = 0;
-    size_t start = 0;
+    cudaEvent_t cur = nullptr;
     cudaEvent_t get()
     {
-        if (used == pool.size()) {
+        if (free_.empty()) {
             cudaEvent_t e;
             cudaEventCreate(&e);
-            pool.push_back(e);
+            all.push_back(e);
+            return e;
         }
-        return pool[used++];
+        cudaEvent_t e = free_.back();
+        free_.pop_back();
+        return e;
     }
     void begin(cudaStream_t st, int c, int nlaunch = 1)
     {
         cls = c;
-        start = used;
-        cudaEventRecord(get(), st);
+        cur = get();
+        cudaEventRecord(cur, st);
         launches += nlaunch;
     }
     void end(cudaStream_t st)
     {
-        cudaEventRecord(get(), st);
-        pending.push_back({cls, start});
+        cudaEvent_t e = get();
+        cudaEventRecord(e, st);
+        pending.push_back({cls, cur, e});
     }
-    void resolve()  // all pending events must have completed (called after a stream sync)
+    // Resolve the first `upto` pending intervals (their events must have completed); the
+    // driver calls this after enqueueing the next absorption so that the host work of
+    // reading events overlaps the device instead of delaying the next launches.
+    void resolve(size_t upto = (size_t)-1)
     {
-        for (auto &p : pending) {
+        upto = std::min(upto, pending.size());
+        for (size_t i = 0; i < upto; ++i) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, pool[p.second], pool[p.second + 1]);
-            acc[p.first] += ms * 1e-3;
+            cudaEventElapsedTime(&ms, pending[i].a, pending[i].b);
+            acc[pending[i].cls] += ms * 1e-3;
+            free_.push_back(pending[i].a);
+            free_.push_back(pending[i].b);
         }
-        pending.clear();
-        used = 0;
+        pending.erase(pending.begin(), pending.begin() + upto);
     }
     ~Timer()
     {
-        for (auto e : pool) cudaEventDestroy(e);
+        for (auto e : all) cudaEventDestroy(e);
     }
 };
 
@@ -270,6 +280,7 @@ struct Phases {
     std::vector<cudaEvent_t> pool;
     std::vector<int> cls;
     double acc[16] = {0};
+    double host[2] = {0, 0};  // host seconds: event resolution after the panel sync, absorption enqueue
     void mark(cudaStream_t st, int c)
     {
         if (!on) return;
@@ -299,7 +310,7 @@ struct Phases {
                                      "factor", "form", "B apply", "", "", "", "", ""};
         fprintf(stderr, "[ht phases] critical stream (s):");
         for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.3f", nm[i], acc[i]);
-        fprintf(stderr, "\n");
+        fprintf(stderr, " | host: resolve=%.3f absorb-enqueue=%.3f\n", host[0], host[1]);
     }
     ~Phases()
     {
@@ -1001,8 +1012,10 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             R.ph.mark(st, 0);
             HT_CUDA_TRY(cudaMemcpyAsync(w->h_out, w->d_out, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             HT_CUDA_TRY(cudaStreamSynchronize(st));
-            R.tm.resolve();
+            const auto h0 = std::chrono::steady_clock::now();
+            const size_t done = R.tm.pending.size();  // complete: st has passed the joins of every stream
             R.ph.resolve();
+            const auto h1 = std::chrono::steady_clock::now();
             const int64_t k = w->h_out[0];
             const int failed = (int)w->h_out[1];
             w->epoch = (unsigned)w->h_out[5] + 1;
@@ -1016,6 +1029,12 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             R.rep.panel_bytes += panel_bytes(n, s0, k, w->h_out[2]);
             if (k <= 0) return HT_ENUMERIC;
             TRY(R.absorb(s0, k));
+            R.tm.resolve(done);
+            if (R.ph.on) {
+                const auto h2 = std::chrono::steady_clock::now();
+                R.ph.host[0] += std::chrono::duration<double>(h1 - h0).count();
+                R.ph.host[1] += std::chrono::duration<double>(h2 - h1).count();
+            }
             s0 += k;
             if (opt && opt->max_panels > 0 && R.rep.panels >= opt->max_panels) break;
         }

@@ -345,8 +345,15 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 // later columns.  Rows above the diagonal row dr never change.
                 const int w0 = warp * RPT;
                 double val[RPT];
+                {
+                    const double2 *src = reinterpret_cast<const double2 *>(Ps + lane * L::LDP + w0);
 #pragma unroll
-                for (int e = 0; e < RPT; ++e) val[e] = Ps[lane * L::LDP + w0 + e];
+                    for (int e = 0; e < RPT; e += 2) {
+                        const double2 t = src[e / 2];
+                        val[e] = t.x;
+                        val[e + 1] = t.y;
+                    }
+                }
                 // the pivot column of the next step goes through shared memory: its owner lane
                 // stores the warp's rows, the warp reads them back as broadcasts (a 64-bit
                 // shuffle per element would cost two SHFL per row and lane)
@@ -405,7 +412,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                         double tau = 0.0, scal = 0.0, beta = alpha;
                         if (cp) ck3 = clock64() + (ss != ss ? 1 : 0) + (myrow != myrow ? 1 : 0);
                         if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
-                        const double wj = tau * (myrow + scal * S);
+                        const double zc = myrow + scal * S;  // lanes < jj: v_lane^T v_jj = G_b(lane, jj)
+                        const double wj = tau * zc;
+                        if (own && lane < jj) Xs[jj * LDX + lane] = zc;
                         if (cp) ck4 = clock64() + (wj != wj ? 1 : 0);
                         // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
                         const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
@@ -429,18 +438,32 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 }
                 FPROF(2);
                 __syncthreads();
+                {
+                    double2 *dst = reinterpret_cast<double2 *>(Ps + lane * L::LDP + w0);
 #pragma unroll
-                for (int e = 0; e < RPT; ++e) {
-                    const int r = w0 + e, col = c0 + lane;
-                    Ps[lane * L::LDP + r] = (r <= col && r < p && lane < nc) ? val[e] : 0.0;
+                    for (int e = 0; e < RPT; e += 2) {
+                        const int r = w0 + e, col = c0 + lane;
+                        const double a0 = (r <= col && r < p && lane < nc) ? val[e] : 0.0;
+                        const double a1 = (r + 1 <= col && r + 1 < p && lane < nc) ? val[e + 1] : 0.0;
+                        dst[e / 2] = make_double2(a0, a1);
+                    }
                 }
                 store_R();
-#pragma unroll
-                for (int e = 0; e < RPT; ++e) {
-                    const int r = w0 + e, col = c0 + lane;
+                {
+                    double2 *dst = reinterpret_cast<double2 *>(Ps + lane * L::LDP + w0);
                     const double tv = taus[lane < nc ? lane : 0];
-                    const double v = (lane >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[e]));
-                    Ps[lane * L::LDP + r] = (r < p) ? v : 0.0;
+                    const int col = c0 + lane;
+#pragma unroll
+                    for (int e = 0; e < RPT; e += 2) {
+                        double a[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int r = w0 + e + h;
+                            const double v = (lane >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[e + h]));
+                            a[h] = (r < p) ? v : 0.0;
+                        }
+                        dst[e / 2] = make_double2(a[0], a[1]);
+                    }
                 }
                 store_V();
             } else {
@@ -660,8 +683,10 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
             if (tid < nc) d.tau[c0 + tid] = taus[tid];
             __threadfence_block();
             FPROF(4);
-            // ---- G_b = V_b^T V_b (DMMA) and T_b by the dlarft recurrence (row i per lane) ----
+            // ---- G_b = V_b^T V_b (DMMA; the wide layout has it from the column steps) and
+            //      T_b by the dlarft recurrence (row i per lane) ----
             __syncthreads();
+            if constexpr (!WIDE)
 #pragma unroll
             for (int j = 0; j < TPW; ++j) {
                 const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
