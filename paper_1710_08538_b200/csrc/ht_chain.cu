@@ -21,6 +21,9 @@
 namespace {
 
 constexpr int CNT = 512;  // threads (16 warps)
+#ifndef CHAIN_PAD
+#define CHAIN_PAD 4
+#endif
 constexpr int SLAB_ELEMS = 16384;  // h * CAP doubles of the ring (128 KB)
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
@@ -44,8 +47,8 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     extern __shared__ __align__(16) double csm[];
     const int h = P.h, cap = P.cap;
     constexpr int kc = KC;
-    const int ldh = h + 8;          // == 8 mod 32: conflict-free A fragments
-    const int ldq = cap + 8;        // == 8 mod 32: conflict-free B fragments
+    const int ldh = h + CHAIN_PAD;    // == 4 mod 16 (in doubles): conflict-free 64-bit A fragments
+    const int ldq = cap + CHAIN_PAD;  // (lanes t4*ld + g hit 16 distinct bank pairs per half-warp)
     double *Xs = csm;               // [cap][ldh]  ring of slab columns
     double *Qs = Xs + (size_t)cap * ldh;  // [2][kc][ldq]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
@@ -240,8 +243,8 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
     if (8 * (int)blockIdx.x >= A.cnt) return;
     const int p = A.p, q = A.q;
     const int p8 = (p + 7) & ~7;
-    const int lds = ((p8 + 31) & ~31) + 8;  // == 8 mod 32: conflict-free A fragments
-    constexpr int LDY = BPW + 8;
+    const int lds = ((p8 + 31) & ~31) + 4;  // == 4 mod 16: conflict-free 64-bit A fragments
+    constexpr int LDY = BPW + 4;
     double *Ss = bsm;                  // [8][lds]  slab rows (window dimension contiguous)
     double *Yp = Ss + 8 * lds;         // [2][8][LDY]  K-half partials of S V_b
     double *Y2 = Yp + 16 * LDY;        // [8][LDY]  S V_b T_b
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
 size_t band_smem(int pmax)
 {
     const int p8 = (pmax + 7) & ~7;
-    return (size_t)(8 * (((p8 + 31) & ~31) + 8) + 24 * (BPW + 8)) * sizeof(double);
+    return (size_t)(8 * (((p8 + 31) & ~31) + 4) + 24 * (BPW + 4)) * sizeof(double);
 }
 int band_init()
 {
@@ -398,10 +401,10 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
         if (mats[i].s_end > mats[i].s_begin) nblk += (mats[i].s_end - mats[i].s_begin + P.h - 1) / P.h;
     if (nblk == 0) return 0;
     const int kc = P.cap <= 256 ? 16 : 8;
-    const size_t smem = ((size_t)P.cap * (P.h + 8) + 2 * (size_t)kc * (P.cap + 8)) * sizeof(double);
+    const size_t smem = ((size_t)P.cap * (P.h + CHAIN_PAD) + 2 * (size_t)kc * (P.cap + CHAIN_PAD)) * sizeof(double);
     static bool init = false;
     if (!init) {
-        const int mx = (int)(SLAB_ELEMS + 8 * 512 + 2 * 16 * 264) * 8;
+        const int mx = (int)(SLAB_ELEMS + CHAIN_PAD * 512 + 2 * 16 * (256 + CHAIN_PAD)) * 8;
         HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         init = true;

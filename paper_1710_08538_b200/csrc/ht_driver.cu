@@ -583,8 +583,11 @@ struct Run {
             const Win &x = wins[i];
             wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
         }
+        // (Deferring part of this B update to sB does not pay: the next R3 band update would
+        // wait for all of it.)
+        cudaStream_t sBq = serial ? st : w->sB;
         TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
-        // W-updates: B on st, Z on sQZ, A on sA
+        // W-updates: B on st (+ sB), Z on sQZ, A on sA
         struct WX { double *X; int64_t ld, rows; cudaStream_t s; double *W1, *W2; } wx[2] = {
             {B, ldb, n, st, w->W1, w->W2}, {wz ? Z + qz0 : nullptr, ldz, qz1 - qz0, sQ, w->W1Q, w->W2Q}};
         auto wupdate = [&](const WX &e) -> int {
@@ -616,7 +619,6 @@ struct Run {
         // t-1's band update, which waits for it through evE -- a full factorization later);
         // A and Z take the windows in batches after sB has formed them.
         const Store sr{w->VhatR, w->QwR, w->TmR, w->tauR, w->WtR, w->fscr};
-        cudaStream_t sBq = serial ? st : w->sB;
         TRY(dep(sBq, st, 9));  // B after R2
         auto flush_right = [&](std::vector<ChainWin> &ws) -> int {
             if (ws.empty()) return 0;
@@ -689,6 +691,7 @@ struct Run {
         TRY(copy2d(k, k, U + p0, n, w->UR, ldur));
         TRY(copy2d(k, k, w->UW, ldw, w->UR + k, ldur));
         TRY(zero_lower(k, k, w->UR + k, ldur, 0));
+
         TRY(dep(sA, st, 5));  // L1 windows and UR are ready
         TRY(dep(sQ, st, 5));
         {
@@ -701,10 +704,11 @@ struct Run {
         }
         {
             // B(p0:p0+2k, J+1:n) (st) and A(p0:p0+2k, J:n) (sA):  X <- X - UR S^T (X^T UR)^T
-            struct LX { double *X; int64_t ld, c0; cudaStream_t s; double *W1, *W2; } lx[2] = {
-                {B, ldb, J + 1, st, w->W1, w->W2}, {A, lda, J, sA, w->W1A, w->W2A}};
+            struct LX { double *X; int64_t ld, c0, c1; cudaStream_t s; double *W1, *W2; } lx[2] = {
+                {B, ldb, J + 1, n, st, w->W1, w->W2}, {A, lda, J, n, sA, w->W1A, w->W2A}};
             for (auto &e : lx) {
-                const int64_t nc = n - e.c0;
+                const int64_t nc = e.c1 - e.c0;
+                if (nc <= 0) continue;
                 double *Xp = e.X + p0 + e.c0 * e.ld;
                 TRY(gemm_on(e.s, 'T', 'N', nc, k, 2 * k, 1.0, Xp, e.ld, w->UR, ldur, 0.0, e.W1, n));
                 TRY(gemm_on(e.s, 'N', 'N', nc, k, k, 1.0, e.W1, n, S, nb, 0.0, e.W2, n));

@@ -27,7 +27,7 @@ constexpr int PBW = 32;   // panel width (left-looking granularity)
 constexpr int LW = 8;     // leaf width (columns factored one by one)
 constexpr int NLF = PBW / LW;
 constexpr int VRC = 256;  // rows per staged chunk of a previous panel's V
-constexpr int LDX = 40;   // ld of the 32x32 X buffer (== 8 mod 32: conflict-free B fragments)
+constexpr int LDX = 36;   // ld of the 32x32 X buffer (== 4 mod 16: conflict-free 64-bit B fragments)
 constexpr int LDT = 33;
 
 // Optional phase profile (micro-benchmarks only): when non-null, thread 0 accumulates
@@ -703,30 +703,45 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
             }
             __syncthreads();
             FPROF(11);
-            if (warp == 0) {
-                // T_b by the dlarft forward recurrence, lane i = row i held in registers
-                // (T upper triangular: trow[l] = 0 for l < i, so the sums run over all l < c):
-                //   T(i,i) = tau_i,  T(i,c) = -tau_c sum_{l<c} T(i,l) G(l,c)   (G symmetric: G(c,l))
-                const int i = lane;
-                double trow[PBW];
+            if (fprof && tid == 0) atomicAdd(&fprof[27], (unsigned long long)(-clock64()));
+            {
+                // T_b by the dlarft forward recurrence
+                //   T(i,i) = tau_i,  T(i,c) = -tau_c sum_{l<c} T(i,l) G(l,c)
+                // Rows are independent: warp w takes rows w*RW .. w*RW+RW-1, the LPR lanes of a
+                // row split its columns (lane cl: columns cl, cl+LPR, ...).  In right-looking
+                // order, T(i,c) (computed by the owner lane of column c, then shuffled to the
+                // row's lanes) is added into the sums of the later columns right away.
+                constexpr int RW = PBW / FNW, LPR = 32 / RW, CPL = PBW / LPR;
+                const int rr = lane / LPR, cl = lane % LPR, i = warp * RW + rr;
+                double acc[CPL], tr[CPL];
 #pragma unroll
-                for (int c = 0; c < PBW; ++c) trow[c] = (c == i && i < nc) ? taus[i] : 0.0;
+                for (int u = 0; u < CPL; ++u) acc[u] = tr[u] = 0.0;
 #pragma unroll
-                for (int c = 1; c < PBW; ++c) {
-                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int c = 0; c < PBW; ++c) {
+                    const int uo = c / LPR, clo = c % LPR;
+                    const double tc = taus[c < nc ? c : 0];
+                    double tv = (c > i) ? -tc * acc[uo] : (c == i ? tc : 0.0);
+                    tv = (c < nc && i < nc) ? tv : 0.0;
+                    tv = __shfl_sync(0xffffffffu, tv, rr * LPR + clo);
+                    if (cl == clo) tr[uo] = tv;
 #pragma unroll
-                    for (int l = 0; l < c; ++l) sa[l & 3] = fma(trow[l], Xs[c * LDX + l], sa[l & 3]);
-                    const double tv = -taus[c < nc ? c : 0] * ((sa[0] + sa[1]) + (sa[2] + sa[3]));
-                    if (c > i && c < nc) trow[c] = tv;
+                    for (int u = 0; u < CPL; ++u) {
+                        const int c2 = cl + LPR * u;
+                        if (c2 > c) acc[u] = fma(tv, Xs[c2 * LDX + c], acc[u]);
+                    }
+                }
+                if (fprof && tid == 0) {
+                    const long long ckT = clock64() + (tr[0] != tr[0] ? 1 : 0);
+                    atomicAdd(&fprof[27], (unsigned long long)ckT);
                 }
                 if (i < nc) {
                     // row i of T_b -> the diagonal block of the global T (columns c0..c0+nc)
 #pragma unroll
-                    for (int c = 0; c < PBW; ++c)
-                        if (c < nc) Tout(c0 + i, c0 + c) = trow[c];
+                    for (int u = 0; u < CPL; ++u) {
+                        const int c2 = cl + LPR * u;
+                        if (c2 < nc) Tout(c0 + i, c0 + c2) = tr[u];
+                    }
                 }
-#pragma unroll
-                for (int c = 0; c < PBW; ++c) Ts[i * LDT + c] = (i < nc && c < nc) ? trow[c] : 0.0;
             }
             __threadfence_block();
             __syncthreads();
