@@ -557,6 +557,7 @@ struct Run {
                 const int p = (int)(bot - top);
                 Win x = add_win(winsL, p, K);
                 fl.push_back(FactorDesc{w->UW + top, 1, ldw, p, K, 0, sl.Vhat + x.ov, p, sl.tau + x.ot});
+                if (i > 0) fl.back().dense = p - K;  // [k new rows; R of the window below]
             }
             HT_CUDA_TRY(cudaEventRecord(w->ev_fork, st));
             HT_CUDA_TRY(cudaStreamWaitEvent(w->side_stream, w->ev_fork, 0));
@@ -572,6 +573,7 @@ struct Run {
             Win x = add_win(p, K);
             fds.push_back(FactorDesc{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1,
                                      w->Vhat + x.ov, p, w->tau + x.ot});
+            if (i > 0) fds.back().dense = p - K;  // view: [k new rows; L of the window above, reversed]
         }
         ph.mark(st, 1);
         TRY(factor_and_form(fds, 0));

@@ -120,12 +120,11 @@ __device__ __forceinline__ void stage_v(const FactorDesc &d, int col0, int r0, i
 // t = w + NW*j (j < TPW), (tm, tn) = (t/4, t%4), and returns them in
 // o[j] = X(8tm+g, 8tn+2t4 + {0,1}).
 template <class L>
-__device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r_beg, const double *Ps, double *Vs,
-                                               double (&o)[L::TPW][2])
+__device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r_beg, int r_end, const double *Ps,
+                                               double *Vs, double (&o)[L::TPW][2])
 {
     constexpr int TPW = L::TPW, CH = 4;  // 4 independent DMMA chains per tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
-    const int p = d.p;
     double x[TPW][CH][2];
 #pragma unroll
     for (int j = 0; j < TPW; ++j)
@@ -133,8 +132,8 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
         for (int u = 0; u < CH; ++u) x[j][u][0] = x[j][u][1] = 0.0;
     unsigned long long *fp = g_fprof;
     long long c_a = 0, c_b = 0;
-    for (int r0 = r_beg; r0 < p; r0 += L::RC) {
-        const int rows = min(L::RC, p - r0);
+    for (int r0 = r_beg; r0 < r_end; r0 += L::RC) {
+        const int rows = min(L::RC, r_end - r0);
         __syncthreads();
         if (fp && tid == 0) c_a = clock64();
         stage_v<L>(d, i * PBW, r0, rows, Vs);
@@ -215,6 +214,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
     for (int di = 0; di < nd; ++di) {
         const FactorDesc d = descs[di];
         const int p = d.p, q = d.q;
+        // rows >= dense + c + 1 of view column c are exactly zero (staircase windows)
+        const int dense = (d.dense > 0 && d.dense < p) ? d.dense : p;
         const int64_t rs = d.rs, cs = d.cs;
         auto nat = [&](int r) -> int64_t { return d.rev ? (int64_t)(p - 1 - r) : (int64_t)r; };
         auto Tout = [&](int a, int c) -> double & { return d.T[(int64_t)c * d.ldt + a]; };
@@ -253,8 +254,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
 #pragma unroll
                     for (int e = 0; e < E; ++e) Ts[a * LDT + c + e * (FNT / PBW)] = tv[e];  // diagonal block T_i
                 }
+                const int r_hi = min(p, dense + r_lo + PBW);  // V_i is zero below this row
                 double o[TPW][2];
-                vt_times_panel<L>(d, i, r_lo, Ps, Vs, o);
+                vt_times_panel<L>(d, i, r_lo, r_hi, Ps, Vs, o);
 #pragma unroll
                 for (int j = 0; j < TPW; ++j) {
                     const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
@@ -287,9 +289,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 __syncthreads();
                 FPROF(9);
                 // P -= V_i X : per chunk, warp w owns row tiles w, w + FNW, ... x 4 column tiles
-                for (int r0 = r_lo; r0 < p; r0 += L::RC) {
-                    const int rows = min(L::RC, p - r0);
-                    if (p - r_lo > L::RC) {  // multi-chunk: Vs holds the last chunk -> re-stage
+                for (int r0 = r_lo; r0 < r_hi; r0 += L::RC) {
+                    const int rows = min(L::RC, r_hi - r0);
+                    if (r_hi - r_lo > L::RC) {  // multi-chunk: Vs holds the last chunk -> re-stage
                         __syncthreads();
                         stage_v<L>(d, r_lo, r0, rows, Vs);
                         __syncthreads();
@@ -373,7 +375,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     const int dr = c0 + jj;           // diagonal row of column jj
                     const int bw = dr / RPT;          // warp holding row dr
                     const int eo = jj % RPT;          // its element index (c0 % RPT == 0 or RPT % 32 == 0)
-                    const bool act = warp >= bw, own = warp == bw;
+                    const int rmax = dense + dr;      // last row that can be nonzero in column jj
+                    const bool act = warp >= bw && warp * RPT <= rmax, own = warp == bw;
                     double xr[RPT];
                     const bool cp = fprof && lane == 0 && warp == FNW - 1;
                     long long ck0 = cp ? clock64() : 0, ck1 = 0, ck2 = 0, ck3 = 0, ck4 = 0;
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     if (act) {
                         double pr[FNW];
 #pragma unroll
-                        for (int w = 0; w < FNW; ++w) pr[w] = (w >= bw) ? part[(buf * FNW + w) * PBW + lane] : 0.0;
+                        for (int w = 0; w < FNW; ++w) pr[w] = (w >= bw && w * RPT <= rmax) ? part[(buf * FNW + w) * PBW + lane] : 0.0;
 #pragma unroll
                         for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
 #pragma unroll
@@ -425,8 +428,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                             val[eo] = lane > jj ? val[eo] - wj : (lane == jj ? beta : val[eo]);
                             if (lane == jj) taus[jj] = tau;
                         }
-                        if (jj + 1 < nc) put_pivot(jj + 1, buf ^ 1);
                     }
+                    // next step's pivot slices (a warp may become active at the next step)
+                    if (jj + 1 < nc && warp >= (dr + 1) / RPT && warp * RPT <= rmax + 1) put_pivot(jj + 1, buf ^ 1);
                     if (cp) {
                         const long long ck5 = clock64() + (val[RPT - 1] != val[RPT - 1] ? 1 : 0);
                         atomicAdd(&fprof[12], (unsigned long long)(ck1 - ck0));

@@ -17,6 +17,8 @@ struct FactorDesc {
     double *tau;
     double *T;     // q x q upper-triangular compact-WY factor of Q = H_0 H_1 ... H_{q-1}
     int64_t ldt;
+    int dense;     // > 0: view rows >= dense + c + 1 of column c are exactly zero (staircase
+                   // windows [k new rows; R of the previous window]); 0: no structure
 };
 
 // chained window applies (ht_chain.cu): per matrix, slab dimension s in [s_begin, s_end)

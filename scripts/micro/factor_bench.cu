@@ -18,6 +18,7 @@ int main(int argc, char **argv)
     const int p = argc > 1 ? atoi(argv[1]) : 256, q = argc > 2 ? atoi(argv[2]) : 128;
     const int reps = argc > 3 ? atoi(argv[3]) : 10;
     const int rev = argc > 4 ? atoi(argv[4]) : 0;
+    const int dense = argc > 5 ? atoi(argv[5]) : 0;  // staircase structure: view rows > dense + c of column c are 0
     std::vector<double> W0((size_t)p * q);
     srand(1);
     for (auto &x : W0) x = (double)rand() / RAND_MAX - 0.5;
@@ -28,6 +29,11 @@ int main(int argc, char **argv)
     // view: rev -> reversed rows and columns (QL-type); W(i, j) = base[i*rs + j*cs]
     if (rev) hd = FactorDesc{dW + (p - 1) + (size_t)(q - 1) * p, -1, -(int64_t)p, p, q, 1, dV, p, dtau, dT, q};
     else hd = FactorDesc{dW, 1, p, p, q, 0, dV, p, dtau, dT, q};
+    hd.dense = dense;
+    if (dense > 0)
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j < q; ++j)
+                if (i > dense + j) W0[rev ? (size_t)(p - 1 - i) + (size_t)(q - 1 - j) * p : (size_t)i + (size_t)j * p] = 0.0;
     FactorDesc *dd; cudaMalloc(&dd, sizeof(FactorDesc));
     cudaMemcpy(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice);
     unsigned long long *dprof; cudaMalloc(&dprof, 32 * 8); cudaMemset(dprof, 0, 32 * 8);
