@@ -28,7 +28,7 @@ constexpr int LW = 8;     // leaf width (columns factored one by one)
 constexpr int NLF = PBW / LW;
 constexpr int VRC = 256;  // rows per staged chunk of a previous panel's V
 constexpr int LDX = 36;   // ld of the 32x32 X buffer (== 4 mod 16: conflict-free 64-bit B fragments)
-constexpr int LDT = 33;
+constexpr int LDT = 36;   // == 4 mod 16: conflict-free 64-bit A fragments of T_i^T
 
 // Optional phase profile (micro-benchmarks only): when non-null, thread 0 accumulates
 // globaltimer nanoseconds per phase into g_fprof[phase].
@@ -265,26 +265,25 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 }
                 __syncthreads();
                 FPROF(8);
-                // X <- T_i^T X  (T_i upper triangular): X'(a, c) = sum_{l <= a} T(l, a) X(l, c)
-                constexpr int EX = PBW * PBW / FNT;
-                double xv[EX];
+                // X <- -T_i^T X  (T_i upper triangular, zero below the diagonal) on the tensor
+                // pipe: X'(a, c) = sum_{l <= a} T(l, a) X(l, c), 16 8x8 tiles, K <= 32
+                double xo[TPW][2];
 #pragma unroll
-                for (int e = 0; e < EX; ++e) {
-                    const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
-                    double sa[4] = {0.0, 0.0, 0.0, 0.0};
-                    int l = 0;
-                    for (; l + 4 <= a + 1; l += 4) {
+                for (int j = 0; j < TPW; ++j) {
+                    const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
+                    double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) sa[u] = fma(Ts[(l + u) * LDT + a], Xs[(l + u) * LDX + c], sa[u]);
-                    }
-                    for (; l <= a; ++l) sa[0] = fma(Ts[l * LDT + a], Xs[l * LDX + c], sa[0]);
-                    xv[e] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+                    for (int k = 0; k < PBW; k += 4)
+                        if (k < 8 * tm + 8) dmma884(c0, c1, Ts[(k + t4) * LDT + 8 * tm + g], Xs[(k + t4) * LDX + 8 * tn + g]);
+                    xo[j][0] = -c0;
+                    xo[j][1] = -c1;
                 }
                 __syncthreads();
 #pragma unroll
-                for (int e = 0; e < EX; ++e) {
-                    const int idx = tid + e * FNT, a = idx / PBW, c = idx % PBW;
-                    Xs[a * LDX + c] = -xv[e];
+                for (int j = 0; j < TPW; ++j) {
+                    const int t = warp + FNW * j, tm = t >> 2, tn = t & 3;
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4] = xo[j][0];
+                    Xs[(8 * tm + g) * LDX + 8 * tn + 2 * t4 + 1] = xo[j][1];
                 }
                 __syncthreads();
                 FPROF(9);
@@ -320,6 +319,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
             }
             __syncthreads();
             FPROF(10);
+
             // R (upper trapezoid of the panel columns) and V go through Ps so that the global
             // stores are coalesced along the view's contiguous direction.
             auto store_R = [&]() {
