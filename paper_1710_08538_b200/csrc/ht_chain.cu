@@ -236,6 +236,14 @@ struct BandDesc {
 };
 constexpr int BPW = 32;  // panel width of the factorization (ht_factor.cu PBW)
 
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool ok)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
+// smem layout (doubles): Ss [8][lds] | Yp [2][8][LDY] | Y2 [8][LDY] | Vb [2][BPW][ldr] | Tb [2][BPW][LDY]
+// (ld == 4 mod 16 everywhere: conflict-free 64-bit fragments)
 __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, const __grid_constant__ BandDesc one)
 {
     extern __shared__ __align__(16) double bsm[];
@@ -243,17 +251,38 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
     if (8 * (int)blockIdx.x >= A.cnt) return;
     const int p = A.p, q = A.q;
     const int p8 = (p + 7) & ~7;
-    const int lds = ((p8 + 31) & ~31) + 4;  // == 4 mod 16: conflict-free 64-bit A fragments
+    const int lds = ((p8 + 31) & ~31) + 4;
+    const int ldr = ((p8 + 15) & ~15) + 4;  // V_b block, column-major
     constexpr int LDY = BPW + 4;
-    double *Ss = bsm;                  // [8][lds]  slab rows (window dimension contiguous)
-    double *Yp = Ss + 8 * lds;         // [2][8][LDY]  K-half partials of S V_b
-    double *Y2 = Yp + 16 * LDY;        // [8][LDY]  S V_b T_b
+    double *Ss = bsm;
+    double *Yp = Ss + 8 * lds;
+    double *Y2 = Yp + 16 * LDY;
+    double *Vb = Y2 + 8 * LDY;             // [2][BPW][ldr]
+    double *Tb = Vb + 2 * BPW * ldr;       // [2][BPW][LDY]  T_b(k, n) at Tb[n * LDY + k]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
     const int64_t sb = A.s0 + 8 * (int64_t)blockIdx.x;
     const int ns = min(8, A.cnt - 8 * (int)blockIdx.x);
     auto xp = [&](int s, int c) -> double * {
         return A.left ? A.X + (sb + s) * A.ld + A.o + c : A.X + (A.o + c) * A.ld + sb + s;
     };
+    const int nblk = (q + BPW - 1) / BPW;
+    // stage V_b (p x 32, rows contiguous) and T_b (32 x 32) of block b into buffer b & 1
+    auto stage = [&](int b) {
+        const int j0 = b * BPW, nc = min(BPW, q - j0);
+        double *vb = Vb + (b & 1) * BPW * ldr, *tb = Tb + (b & 1) * BPW * LDY;
+        for (int i = tid; i < BPW * p8; i += 256) {
+            const int j = i / p8, r = i % p8;
+            const bool ok = j < nc && r < p;
+            cp_async8(vb + j * ldr + r, ok ? A.V + (int64_t)(j0 + j) * A.ldv + r : A.V, ok);
+        }
+        for (int i = tid; i < BPW * BPW; i += 256) {
+            const int n = i / BPW, k = i % BPW;
+            const bool ok = n < nc && k <= n;  // T_b upper: lower part read as 0
+            cp_async8(tb + n * LDY + k, ok ? A.T + (int64_t)(j0 + n) * A.ldt + j0 + k : A.T, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    stage(0);
     for (int i = tid; i < 8 * p8; i += 256) {
         int s, c;
         if (A.left) { s = i / p8; c = i % p8; }  // contiguous along c
@@ -262,64 +291,56 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
         Ss[s * lds + c] = v;
     }
-    const int nblk = (q + BPW - 1) / BPW;
     for (int b = 0; b < nblk; ++b) {
-        const int j0 = b * BPW, nc = min(BPW, q - j0);
+        if (b > 0) __syncthreads();  // pass b-1 has finished reading buffer (b+1) & 1
+        if (b + 1 < nblk) {
+            stage(b + 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncthreads();
-        // Y = S V_b: warp = (n-tile, K half); B fragments V(k, j0 + n) from L2
+        const double *vb = Vb + (b & 1) * BPW * ldr, *tb = Tb + (b & 1) * BPW * LDY;
+        // Y = S V_b: warp = (n-tile, K half)
         {
             const int nt = warp & 3, kh = warp >> 2;
-            const int n = 8 * nt + g;
-            const double *vc = A.V + (int64_t)(j0 + n) * A.ldv;
-            const int kb = kh * (p8 / 2 & ~3), ke = kh ? p8 : (p8 / 2 & ~3);
+            const int half = (p8 / 2) & ~3;
+            const int kb = kh ? half : 0, ke = kh ? p8 : half;
+            const double *bcol = vb + (8 * nt + g) * ldr + t4;
+            const double *arow = Ss + g * lds + t4;
             double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-            for (int k = kb; k < ke; k += 32) {
-                double bv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int kr = k + 4 * u + t4;
-                    bv[u] = (n < nc && kr < p && k + 4 * u < ke) ? vc[kr] : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; u += 2) {
-                    if (k + 4 * u < ke) dmma(c0, c1, Ss[g * lds + k + 4 * u + t4], bv[u]);
-                    if (k + 4 * u + 4 < ke) dmma(d0, d1, Ss[g * lds + k + 4 * u + 4 + t4], bv[u + 1]);
-                }
+            int k = kb;
+            for (; k + 8 <= ke; k += 8) {
+                dmma(c0, c1, arow[k], bcol[k]);
+                dmma(d0, d1, arow[k + 4], bcol[k + 4]);
             }
+            if (k < ke) dmma(c0, c1, arow[k], bcol[k]);
             Yp[(kh * 8 + g) * LDY + 8 * nt + 2 * t4] = c0 + d0;
             Yp[(kh * 8 + g) * LDY + 8 * nt + 2 * t4 + 1] = c1 + d1;
         }
         __syncthreads();
-        // Y2 = Y T_b (T_b upper, diagonal block of T): warps 0..3, one n-tile each
+        // Y2 = Y T_b: warps 0..3, one n-tile each
         if (warp < 4) {
-            const int nt = warp, n = 8 * nt + g;
-            const double *tc = A.T + (int64_t)(j0 + n) * A.ldt + j0;
+            const int nt = warp;
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
             for (int k = 0; k < BPW; k += 4) {
                 if (k < 8 * nt + 8) {
                     const int kr = k + t4;
-                    const double bv = (n < nc && kr <= n) ? tc[kr] : 0.0;
                     const double av = Yp[g * LDY + kr] + Yp[(8 + g) * LDY + kr];
-                    dmma(c0, c1, av, bv);
+                    dmma(c0, c1, av, tb[(8 * nt + g) * LDY + kr]);
                 }
             }
             Y2[g * LDY + 8 * nt + 2 * t4] = c0;
             Y2[g * LDY + 8 * nt + 2 * t4 + 1] = c1;
         }
         __syncthreads();
-        // S -= Y2 V_b^T: B fragments V^T(k, n) = V(n, j0 + k)
+        // S -= Y2 V_b^T: B fragments V^T(k, n) = V_b(n, k)
         for (int nt = warp; nt < p8 / 8; nt += 8) {
             const int n = 8 * nt + g;
-            double bv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int kr = 4 * u + t4;
-                bv[u] = (n < p && kr < nc) ? A.V[(int64_t)(j0 + kr) * A.ldv + n] : 0.0;
-            }
             double c0 = Ss[g * lds + 8 * nt + 2 * t4], c1 = Ss[g * lds + 8 * nt + 2 * t4 + 1];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) dmma(c0, c1, -Y2[g * LDY + 4 * u + t4], bv[u]);
+            for (int u = 0; u < 8; ++u) dmma(c0, c1, -Y2[g * LDY + 4 * u + t4], vb[(4 * u + t4) * ldr + n]);
             Ss[g * lds + 8 * nt + 2 * t4] = c0;
             Ss[g * lds + 8 * nt + 2 * t4 + 1] = c1;
         }
@@ -336,13 +357,14 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
 size_t band_smem(int pmax)
 {
     const int p8 = (pmax + 7) & ~7;
-    return (size_t)(8 * (((p8 + 31) & ~31) + 4) + 24 * (BPW + 4)) * sizeof(double);
+    const int lds = ((p8 + 31) & ~31) + 4, ldr = ((p8 + 15) & ~15) + 4, ldy = BPW + 4;
+    return (size_t)(8 * lds + 24 * ldy + 2 * BPW * ldr + 2 * BPW * ldy) * sizeof(double);
 }
 int band_init()
 {
     static bool init = false;
     if (!init) {
-        HT_CUDA_TRY(cudaFuncSetAttribute(band_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        HT_CUDA_TRY(cudaFuncSetAttribute(band_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         init = true;
     }
     return 0;

@@ -359,12 +359,14 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
     // super-block per 2-CTA cluster: rank 0 solves hi, rank 1 solves lo, and hi's solution
     // reaches lo through distributed shared memory instead of a flag round trip through L2.
     cg::cluster_group cl = cg::this_cluster();
-    const int rank = (int)cl.block_rank(), ncl = C.G / 2, cid = C.bid / 2;
-    const int Nsb = (Nb + 1) / 2;
+    const bool pair = cl.num_blocks() == 2;  // else (profiling launch) single CTAs, L2 hand-offs only
+    const int per = pair ? 2 : 1;
+    const int rank = pair ? (int)cl.block_rank() : 0, ncl = C.G / per, cid = C.bid / per;
+    const int Nsb = (Nb + per - 1) / per;
     for (int sb = cid; sb < Nsb; sb += ncl) {
-        const int b = Nb - 1 - 2 * sb - rank;  // hi (rank 0) or lo (rank 1)
-        const bool paired_lo = (rank == 1);     // lo: y~_{b+1} comes from the partner
-        if (b < 0) {                            // odd Nb: the top super-block has no lo
+        const int b = Nb - 1 - per * sb - rank;  // hi (rank 0) or lo (rank 1)
+        const bool paired_lo = pair && rank == 1;  // lo: y~_{b+1} comes from the partner
+        if (b < 0) {                               // odd Nb: the top super-block has no lo
             cl.sync();
             continue;
         }
@@ -584,7 +586,8 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
             if (tt) tt[4 * b + 2] = gtime();
         }
-        if (!paired_lo) {
+        if (!pair) {
+        } else if (!paired_lo) {
             // hand y~_b (this CTA's values, exponent e) to the lo partner's shared memory
             PanelSmem *peer = cl.map_shared_rank(&g_sm, 1);
             if (C.tid < TB) peer->yrecv[C.tid] = (C.tid < h) ? a.vy[r0 + C.tid] : 0.0;
@@ -1270,9 +1273,13 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         if (rc) return rc;
     }
     // cooperative launch (grid barriers) in clusters of 2 CTAs (the solve hands blocks over
-    // through distributed shared memory); the grid is even
-    nblocks &= ~1;
-    if (nblocks < 2) nblocks = 2;
+    // through distributed shared memory); the grid is even.  HT_PANEL_NOCLUSTER=1 (profiling
+    // only: ncu cannot replay cooperative cluster launches) runs unpaired single CTAs.
+    static const bool nocl = getenv("HT_PANEL_NOCLUSTER") != nullptr;
+    if (!nocl) {
+        nblocks &= ~1;
+        if (nblocks < 2) nblocks = 2;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nblocks);
     cfg.blockDim = dim3(PNT);
@@ -1286,7 +1293,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = nocl ? 1 : 2;
     HT_CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_kernel, *a));
     return 0;
 }
