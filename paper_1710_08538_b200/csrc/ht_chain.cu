@@ -128,16 +128,19 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-            const int per = (kc * pp + CNT - 1) / CNT;  // staged elements per thread (<= 8)
+            // k-chunk of Qhat (row-major, Qhat(k, c) at Qw[k p + c]): lanes run along c for
+            // both the global read and the shared store (conflict-free)
+            const int lcap = __ffs(cap) - 1;            // cap is a power of two
+            const int per = (kc * cap) >> 9;            // staged elements per thread (<= 8; CNT = 512)
             double rq[8];
             auto fetch = [&](int k0) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     if (e >= per) break;
                     const int idx = tid + e * CNT;
-                    const int kr = idx % KC, c = idx / KC;
+                    const int kr = idx >> lcap, c = idx & (cap - 1);
                     double v = 0.0;
-                    if (c < p && k0 + kr < p) v = W.Qw[(size_t)(k0 + kr) + (size_t)c * p];
+                    if (c < p && k0 + kr < p) v = W.Qw[(size_t)(k0 + kr) * p + c];
                     rq[e] = v;
                 }
             };
@@ -146,8 +149,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                 for (int e = 0; e < 8; ++e) {
                     if (e >= per) break;
                     const int idx = tid + e * CNT;
-                    const int kr = idx % KC, c = idx / KC;
-                    if (c < pp) Qs[(size_t)buf * kc * ldq + kr * ldq + c] = rq[e];
+                    Qs[(size_t)buf * kc * ldq + (idx >> lcap) * ldq + (idx & (cap - 1))] = rq[e];
                 }
             };
             const int nk = pp / kc + (pp % kc ? 1 : 0);
@@ -383,7 +385,7 @@ int ht_band_wy(cudaStream_t st, double *X, int64_t ld, int left, int64_t s0, int
     return 0;
 }
 
-// Explicit Qhat (p x p, ld p) of nw windows: window i has Qw[i], V[i] (p x q, ld p), T[i]
+// Explicit Qhat (p x p, row-major: Qhat(k, c) at [k p + c]) of nw windows: window i has Qw[i], V[i] (p x q, ld p), T[i]
 // (diagonal 32x32 blocks, ld q).  d_descs: device scratch for nw descriptors, h_descs pinned.
 int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const int *q, const double *const *V,
                  const double *const *T, void *d_descs, void *h_descs)
@@ -393,7 +395,7 @@ int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const
     BandDesc *hd = reinterpret_cast<BandDesc *>(h_descs);
     int pmax = 0;
     for (int i = 0; i < nw; ++i) {
-        hd[i] = BandDesc{Qw[i], p[i], 0, 1, 0, p[i], 0, p[i], q[i], V[i], p[i], T[i], q[i]};
+        hd[i] = BandDesc{Qw[i], p[i], 1, 1, 0, p[i], 0, p[i], q[i], V[i], p[i], T[i], q[i]};  // row-major Qhat
         pmax = std::max(pmax, p[i]);
     }
     HT_CUDA_TRY(cudaMemcpyAsync(d_descs, hd, nw * sizeof(BandDesc), cudaMemcpyHostToDevice, st));

@@ -30,7 +30,8 @@ struct ChainMat {
     int left;
     int64_t s_begin, s_end;
 };
-// one window: columns (rows) [o, o+p) <- . * Qw (p x p, ld p); applied to slabs s in [lo[m], hi[m])
+// one window: columns (rows) [o, o+p) <- . * Qw (p x p, stored ROW-major: Qw(k, c) at Qw[k p + c]);
+// applied to slabs s in [lo[m], hi[m])
 struct ChainWin {
     const double *Qw;
     int64_t o;
@@ -47,7 +48,7 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
 // X <- Qhat^T X (left).  8 slabs per CTA.
 int ht_band_wy(cudaStream_t st, double *X, int64_t ld, int left, int64_t s0, int64_t cnt, int64_t o, int p, int q,
                const double *V, int64_t ldv, const double *T, int64_t ldt);
-// Explicit Qhat = Q_0 Q_1 ... (p x p, ld p) for nw windows (the same kernel on identity rows).
+// Explicit Qhat = Q_0 Q_1 ... (p x p, row-major) for nw windows (the same kernel on identity rows).
 int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const int *q, const double *const *V,
                  const double *const *T, void *d_descs, void *h_descs);
 size_t ht_band_desc_size();
