@@ -244,7 +244,10 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool o
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
 }
 
-// smem layout (doubles): Ss [8][lds] | Yp [2][8][LDY] | Y2 [8][LDY] | Vb [2][BPW][ldr] | Tb [2][BPW][LDY]
+// double-buffered V_b/T_b staging fits in shared memory for windows of up to 256 rows
+__host__ __device__ __forceinline__ bool band_double_buffer(int p8) { return p8 <= 256; }
+
+// smem layout (doubles): Ss [8][lds] | Yp [2][8][LDY] | Y2 [8][LDY] | Vb [nbuf][BPW][ldr] | Tb [nbuf][BPW][LDY]
 // (ld == 4 mod 16 everywhere: conflict-free 64-bit fragments)
 __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, const __grid_constant__ BandDesc one)
 {
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
     double *Yp = Ss + 8 * lds;
     double *Y2 = Yp + 16 * LDY;
     double *Vb = Y2 + 8 * LDY;             // [2][BPW][ldr]
-    double *Tb = Vb + 2 * BPW * ldr;       // [2][BPW][LDY]  T_b(k, n) at Tb[n * LDY + k]
+    double *Tb = Vb + (band_double_buffer(p8) ? 2 : 1) * BPW * ldr;  // [nbuf][BPW][LDY]  T_b(k, n) at Tb[n * LDY + k]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
     const int64_t sb = A.s0 + 8 * (int64_t)blockIdx.x;
     const int ns = min(8, A.cnt - 8 * (int)blockIdx.x);
@@ -268,10 +271,11 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         return A.left ? A.X + (sb + s) * A.ld + A.o + c : A.X + (A.o + c) * A.ld + sb + s;
     };
     const int nblk = (q + BPW - 1) / BPW;
-    // stage V_b (p x 32, rows contiguous) and T_b (32 x 32) of block b into buffer b & 1
+    const bool dbl = band_double_buffer(p8);  // windows of <= 256 rows: prefetch the next block
+    // stage V_b (p x 32, rows contiguous) and T_b (32 x 32) of block b into its buffer
     auto stage = [&](int b) {
-        const int j0 = b * BPW, nc = min(BPW, q - j0);
-        double *vb = Vb + (b & 1) * BPW * ldr, *tb = Tb + (b & 1) * BPW * LDY;
+        const int j0 = b * BPW, nc = min(BPW, q - j0), bf = dbl ? (b & 1) : 0;
+        double *vb = Vb + bf * BPW * ldr, *tb = Tb + bf * BPW * LDY;
         for (int i = tid; i < BPW * p8; i += 256) {
             const int j = i / p8, r = i % p8;
             const bool ok = j < nc && r < p;
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    stage(0);
+    if (dbl) stage(0);
     for (int i = tid; i < 8 * p8; i += 256) {
         int s, c;
         if (A.left) { s = i / p8; c = i % p8; }  // contiguous along c
@@ -294,15 +298,19 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         Ss[s * lds + c] = v;
     }
     for (int b = 0; b < nblk; ++b) {
-        if (b > 0) __syncthreads();  // pass b-1 has finished reading buffer (b+1) & 1
-        if (b + 1 < nblk) {
+        if (b > 0) __syncthreads();  // pass b-1 has finished reading the buffer staged next
+        if (!dbl) {
+            stage(b);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        } else if (b + 1 < nblk) {
             stage(b + 1);
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        const double *vb = Vb + (b & 1) * BPW * ldr, *tb = Tb + (b & 1) * BPW * LDY;
+        const int bf = dbl ? (b & 1) : 0;
+        const double *vb = Vb + bf * BPW * ldr, *tb = Tb + bf * BPW * LDY;
         // Y = S V_b: warp = (n-tile, K half)
         {
             const int nt = warp & 3, kh = warp >> 2;
@@ -360,7 +368,8 @@ size_t band_smem(int pmax)
 {
     const int p8 = (pmax + 7) & ~7;
     const int lds = ((p8 + 31) & ~31) + 4, ldr = ((p8 + 15) & ~15) + 4, ldy = BPW + 4;
-    return (size_t)(8 * lds + 24 * ldy + 2 * BPW * ldr + 2 * BPW * ldy) * sizeof(double);
+    const int nbuf = band_double_buffer(p8) ? 2 : 1;
+    return (size_t)(8 * lds + 24 * ldy + nbuf * BPW * ldr + nbuf * BPW * ldy) * sizeof(double);
 }
 int band_init()
 {

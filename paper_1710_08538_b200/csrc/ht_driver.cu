@@ -113,6 +113,11 @@ struct Timer {
         cudaEvent_t e = get();
         cudaEventRecord(e, st);
         pending.push_back({cls, cur, e});
+        static const bool chk = getenv("HT_SYNC_CHECK") != nullptr;  // debugging: first failing launch
+        if (chk) {
+            const cudaError_t r = cudaStreamSynchronize(st);
+            if (r != cudaSuccess) fprintf(stderr, "[ht sync] launch %lld (class %d) failed: %s\n", (long long)launches, cls, cudaGetErrorString(r));
+        }
     }
     // Resolve the first `upto` pending intervals (their events must have completed); the
     // driver calls this after enqueueing the next absorption so that the host work of

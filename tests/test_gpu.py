@@ -89,6 +89,17 @@ def test_config_shapes_multi_panel(cfg, n):
     check_parity(A, B, H, T, Hr, Tr)
 
 
+@pytest.mark.parametrize("cfg,n,nb", [(5, 900, 160), (5, 1100, 256)])
+def test_windows_taller_than_256_rows(cfg, n, nb):
+    """nb > 128: staircase windows of 2nb > 256 rows take the 512-thread factorization,
+    512-column chain rings and single-buffered band/Qhat staging (cfg5 uses nb = 256)."""
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+
+
 @pytest.mark.parametrize("n,nb", [(120, 16), (300, 32), (700, 64)])
 def test_config4_singular(n, nb):
     """Config 4 (singular, graded B): the HT form of a singular pencil is not unique
