@@ -517,7 +517,14 @@ struct Run {
     // transforms to A, sQZ to Z and Q (their rows/columns never feed a factorization), so
     // those big applies overlap the one-SM factorization chains.  Both are joined before
     // the next panel.  Per matrix the paper's order of operations is kept.
-    int SIDE_GRID = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 56;  // CTAs of an A or Q/Z chain apply
+    // CTAs of an A or Q/Z chain apply on the low-priority streams (measured: 56 is best at
+    // n = 8192; at n = 16384 the side work grows as n^3 against ~n^2 for the critical
+    // factorization chains and 96 is best)
+    int side_grid() const
+    {
+        static const int env = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 0;
+        return env > 0 ? env : (n >= 12288 ? 96 : 56);
+    }
     int absorb(int64_t s0, int64_t k)
     {
         const int64_t p0 = s0 + 1, J = s0 + k, m = n - J - 1;
@@ -612,8 +619,8 @@ struct Run {
         {
             std::vector<ChainWin> wa = wl;
             for (auto &x : wa) x.hi[0] = n;  // A: all rows
-            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wa, SIDE_GRID));
-            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, SIDE_GRID));
+            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wa, side_grid()));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, side_grid()));
         }
         TRY(wupdate(wx[1]));
         TRY(gemm_on(sA, 'N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
@@ -631,8 +638,8 @@ struct Run {
             if (ws.empty()) return 0;
             TRY(dep(sA, sBq, 4));
             TRY(dep(sQ, sBq, 4));
-            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, ws, SIDE_GRID));
-            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, SIDE_GRID));
+            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, ws, side_grid()));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, side_grid()));
             ws.clear();
             return 0;
         };
@@ -704,10 +711,10 @@ struct Run {
         {
             std::vector<ChainWin> wla = wlu;
             for (auto &x : wla) x.lo[0] = J;  // A: columns J..n
-            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wla, SIDE_GRID));
+            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wla, side_grid()));
             std::vector<ChainWin> wlq = wlu;
             for (auto &x : wlq) x.lo[0] = 0;
-            if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, SIDE_GRID));
+            if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, side_grid()));
         }
         {
             // B(p0:p0+2k, J+1:n) (st) and A(p0:p0+2k, J:n) (sA):  X <- X - UR S^T (X^T UR)^T
@@ -739,11 +746,11 @@ struct Run {
             if (ws.empty()) return 0;
             TRY(dep(sA, sBq, 6));
             TRY(dep(sQ, sBq, 6));
-            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, SIDE_GRID));
+            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, side_grid()));
             if (wq) {
                 std::vector<ChainWin> wq_ = ws;
                 for (auto &x : wq_) x.lo[0] = 0;
-                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, SIDE_GRID));
+                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, side_grid()));
             }
             ws.clear();
             return 0;
