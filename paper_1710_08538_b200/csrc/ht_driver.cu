@@ -545,13 +545,20 @@ struct Run {
             return absorb_tail(s0, k);
         }
 
-        // geometry (Remark 4): right boundaries rb = {0, kt-k, kt, ..., m}
-        const int64_t rem = (m - k) % k;
-        const int64_t kt = k + (rem == 0 ? k : rem);
-        const int r = (int)((m - kt) / k + 1);
+        // staircase step ks >= k (reading R-step): windows of 2 ks x k rows stepping
+        // by ks.  The paper's ks = k keeps the same structure for any ks >= k (the rows between
+        // the carried k x k triangle and the ks new rows are zero), and R3/L3 then restore
+        // ks x 2ks blocks.  Tiny premature absorptions (k down to 1) would otherwise make
+        // ~m/k windows per chain; ks = min(32, nb) bounds that to ~m/32.
+        const int64_t kmin = std::min<int64_t>(32, nb);
+        const int64_t ks = (k < kmin && m > 2 * kmin) ? kmin : k;
+        // geometry (Remark 4): right boundaries rb = {0, kt-ks, kt, kt+ks, ..., m}
+        const int64_t rem = (m - ks) % ks;
+        const int64_t kt = ks + (rem == 0 ? ks : rem);
+        const int r = (int)((m - kt) / ks + 1);
         std::vector<int64_t> rb(r + 2), lb(r + 2);
         rb[0] = 0;
-        for (int t = 1; t <= r + 1; ++t) rb[t] = kt - k + (int64_t)(t - 1) * k;
+        for (int t = 1; t <= r + 1; ++t) rb[t] = kt - ks + (int64_t)(t - 1) * ks;
         for (int t = 0; t <= r + 1; ++t) lb[t] = m - rb[r + 1 - t];
         const int64_t ldw = n;  // VW/UW leading dimension
         TRY(copy2d(m, k, V + J + 1, n, w->VW, ldw));
@@ -569,7 +576,7 @@ struct Run {
                 const int p = (int)(bot - top);
                 Win x = add_win(winsL, p, K);
                 fl.push_back(FactorDesc{w->UW + top, 1, ldw, p, K, 0, sl.Vhat + x.ov, p, sl.tau + x.ot});
-                if (i > 0) fl.back().dense = p - K;  // [k new rows; R of the window below]
+                if (i > 0) fl.back().dense = p - (int)ks;  // [ks new rows; R of the window below; 0]
             }
             HT_CUDA_TRY(cudaEventRecord(w->ev_fork, st));
             HT_CUDA_TRY(cudaStreamWaitEvent(w->side_stream, w->ev_fork, 0));
@@ -585,7 +592,7 @@ struct Run {
             Win x = add_win(p, K);
             fds.push_back(FactorDesc{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1,
                                      w->Vhat + x.ov, p, w->tau + x.ot});
-            if (i > 0) fds.back().dense = p - K;  // view: [k new rows; L of the window above, reversed]
+            if (i > 0) fds.back().dense = p - (int)ks;  // view: [ks new rows; L of the window above, reversed; 0]
         }
         ph.mark(st, 1);
         TRY(factor_and_form(fds, 0));
