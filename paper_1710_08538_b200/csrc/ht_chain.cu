@@ -249,10 +249,21 @@ __host__ __device__ __forceinline__ bool band_double_buffer(int p8) { return p8 
 
 // smem layout (doubles): Ss [8][lds] | Yp [2][8][LDY] | Y2 [8][LDY] | Vb [nbuf][BPW][ldr] | Tb [nbuf][BPW][LDY]
 // (ld == 4 mod 16 everywhere: conflict-free 64-bit fragments)
+__device__ unsigned long long *g_bprof = nullptr;  // development: per-phase clock64 sums (thread 0, CTA 0)
+
 __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, const __grid_constant__ BandDesc one)
 {
+    unsigned long long *bprof = (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ? g_bprof : nullptr;
+    long long bck = bprof ? clock64() : 0;
+    auto BPROF = [&](int ph) {
+        if (bprof) {
+            const long long t = clock64();
+            bprof[ph] += (unsigned long long)(t - bck);
+            bck = t;
+        }
+    };
     extern __shared__ __align__(16) double bsm[];
-    const BandDesc &A = descs ? descs[blockIdx.y] : one;
+    const BandDesc A = descs ? descs[blockIdx.y] : one;  // by value: registers, not generic loads
     if (8 * (int)blockIdx.x >= A.cnt) return;
     const int p = A.p, q = A.q;
     const int p8 = (p + 7) & ~7;
@@ -272,15 +283,49 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
     };
     const int nblk = (q + BPW - 1) / BPW;
     const bool dbl = band_double_buffer(p8);  // windows of <= 256 rows: prefetch the next block
-    // stage V_b (p x 32, rows contiguous) and T_b (32 x 32) of block b into its buffer
+    // Bulk-copy path (copy engine, one cp.async.bulk per column, completion on an mbarrier):
+    // needs 16-byte aligned columns of whole 8-row multiples; else 8-byte cp.async.
+    const bool bulk = (p % 8) == 0 && (A.ldv % 2) == 0 && (A.ldt % 2) == 0 && ((uintptr_t)A.V & 15) == 0 &&
+                      ((uintptr_t)A.T & 15) == 0;
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
+    if (bulk && tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int uses[2] = {0, 0};  // completed phases per buffer (parity of the next wait)
+    // stage V_b (p x 32, rows contiguous) and T_b (32 x 32, diagonal block) of block b
     auto stage = [&](int b) {
         const int j0 = b * BPW, nc = min(BPW, q - j0), bf = dbl ? (b & 1) : 0;
         double *vb = Vb + bf * BPW * ldr, *tb = Tb + bf * BPW * LDY;
-        for (int i = tid; i < BPW * p8; i += 256) {
-            const int j = i / p8, r = i % p8;
-            const bool ok = j < nc && r < p;
-            cp_async8(vb + j * ldr + r, ok ? A.V + (int64_t)(j0 + j) * A.ldv + r : A.V, ok);
+        if (bulk) {
+            for (int j = nc; j < BPW; ++j) {  // ragged block: columns beyond nc are zeros
+                for (int r = tid; r < p8; r += 256) vb[j * ldr + r] = 0.0;
+                if (tid < BPW) tb[j * LDY + tid] = 0.0;
+            }
+            if (tid == 0) {
+                const unsigned mb = mb0 + 8 * bf;
+                const unsigned bytes = (unsigned)(nc * (p + BPW) * 8);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+                for (int j = 0; j < nc; ++j) {
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                                 ::"r"((unsigned)__cvta_generic_to_shared(vb + j * ldr)), "l"(A.V + (int64_t)(j0 + j) * A.ldv),
+                                 "r"(p * 8), "r"(mb) : "memory");
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                                 ::"r"((unsigned)__cvta_generic_to_shared(tb + j * LDY)), "l"(A.T + (int64_t)(j0 + j) * A.ldt + j0),
+                                 "r"(BPW * 8), "r"(mb) : "memory");
+                }
+            }
+            return;
         }
+        for (int j = 0; j < BPW; ++j)  // (no division by the runtime row count)
+            for (int r = tid; r < p8; r += 256) {
+                const bool ok = j < nc && r < p;
+                cp_async8(vb + j * ldr + r, ok ? A.V + (int64_t)(j0 + j) * A.ldv + r : A.V, ok);
+            }
         for (int i = tid; i < BPW * BPW; i += 256) {
             const int n = i / BPW, k = i % BPW;
             const bool ok = n < nc && k <= n;  // T_b upper: lower part read as 0
@@ -288,27 +333,48 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
+    // wait for block b's buffer (bulk: mbarrier phase; else cp.async groups, see the loop)
+    auto bulk_wait = [&](int b) {
+        const int bf = dbl ? (b & 1) : 0;
+        const unsigned mb = mb0 + 8 * bf, par = (unsigned)(uses[bf] & 1);
+        unsigned done = 0;
+        while (!done)
+            asm volatile("{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+                         : "=r"(done) : "r"(mb), "r"(par) : "memory");
+        ++uses[bf];
+    };
     if (dbl) stage(0);
-    for (int i = tid; i < 8 * p8; i += 256) {
-        int s, c;
-        if (A.left) { s = i / p8; c = i % p8; }  // contiguous along c
-        else { c = i >> 3; s = i & 7; }          // contiguous along s
-        double v = 0.0;
-        if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
-        Ss[s * lds + c] = v;
+    if (A.left) {  // contiguous along c
+        for (int s = 0; s < 8; ++s)
+            for (int c = tid; c < p8; c += 256) {
+                double v = 0.0;
+                if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
+                Ss[s * lds + c] = v;
+            }
+    } else {       // contiguous along s
+        for (int i = tid; i < 8 * p8; i += 256) {
+            const int c = i >> 3, s = i & 7;
+            double v = 0.0;
+            if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
+            Ss[s * lds + c] = v;
+        }
     }
     for (int b = 0; b < nblk; ++b) {
         if (b > 0) __syncthreads();  // pass b-1 has finished reading the buffer staged next
         if (!dbl) {
             stage(b);
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            if (bulk) bulk_wait(b);
+            else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         } else if (b + 1 < nblk) {
             stage(b + 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            if (bulk) bulk_wait(b);
+            else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            if (bulk) bulk_wait(b);
+            else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
+        BPROF(b == 0 ? 4 : 0);  // staging wait (4: first block, incl. the slab load)
         const int bf = dbl ? (b & 1) : 0;
         const double *vb = Vb + bf * BPW * ldr, *tb = Tb + bf * BPW * LDY;
         // Y = S V_b: warp = (n-tile, K half)
@@ -329,6 +395,7 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
             Yp[(kh * 8 + g) * LDY + 8 * nt + 2 * t4 + 1] = c1 + d1;
         }
         __syncthreads();
+        BPROF(1);  // S V_b
         // Y2 = Y T_b: warps 0..3, one n-tile each
         if (warp < 4) {
             const int nt = warp;
@@ -345,6 +412,7 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
             Y2[g * LDY + 8 * nt + 2 * t4 + 1] = c1;
         }
         __syncthreads();
+        BPROF(2);  // Y T_b
         // S -= Y2 V_b^T: B fragments V^T(k, n) = V_b(n, k)
         for (int nt = warp; nt < p8 / 8; nt += 8) {
             const int n = 8 * nt + g;
@@ -354,13 +422,17 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
             Ss[g * lds + 8 * nt + 2 * t4] = c0;
             Ss[g * lds + 8 * nt + 2 * t4 + 1] = c1;
         }
+        BPROF(3);  // S -= Y2 V_b^T (own warp)
     }
     __syncthreads();
-    for (int i = tid; i < 8 * p8; i += 256) {
-        int s, c;
-        if (A.left) { s = i / p8; c = i % p8; }
-        else { c = i >> 3; s = i & 7; }
-        if (s < ns && c < p) *xp(s, c) = Ss[s * lds + c];
+    if (A.left) {
+        for (int s = 0; s < ns; ++s)
+            for (int c = tid; c < p; c += 256) *xp(s, c) = Ss[s * lds + c];
+    } else {
+        for (int i = tid; i < 8 * p8; i += 256) {
+            const int c = i >> 3, s = i & 7;
+            if (s < ns && c < p) *xp(s, c) = Ss[s * lds + c];
+        }
     }
 }
 

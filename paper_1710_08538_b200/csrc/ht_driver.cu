@@ -312,9 +312,9 @@ struct Phases {
     {
         if (!on) return;
         static const char *nm[16] = {"panel", "pre-R1", "R2 B+W", "R3 rest", "L1 wait", "L2", "L3 rest", "join",
-                                     "factor", "form", "B apply", "", "", "", "", ""};
+                                     "factor", "form", "band", "sB wait", "", "", "", ""};
         fprintf(stderr, "[ht phases] critical stream (s):");
-        for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.3f", nm[i], acc[i]);
+        for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.3f", nm[i], acc[i]);
         fprintf(stderr, " | host: resolve=%.3f absorb-enqueue=%.3f\n", host[0], host[1]);
     }
     ~Phases()
@@ -520,6 +520,11 @@ struct Run {
     // CTAs of an A or Q/Z chain apply on the low-priority streams (measured: 56 is best at
     // n = 8192; at n = 16384 the side work grows as n^3 against ~n^2 for the critical
     // factorization chains and 96 is best)
+    int sb_grid() const  // CTAs of sB's full-height B updates (0: uncapped)
+    {
+        static const int env = getenv("HT_SB_GRID") ? atoi(getenv("HT_SB_GRID")) : 0;
+        return env;
+    }
     int side_grid() const
     {
         static const int env = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 0;
@@ -673,10 +678,11 @@ struct Run {
             TRY(factor_and_form(f1, std::vector<Win>{x}, sr, st, sBq));
             // sB: rows [0, C0) of the window's columns
             const ChainWin cw{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {C0, n, n}};
-            if (C0 > 0) TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, C0}}, {cw}, 0));
+            if (C0 > 0) TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, C0}}, {cw}, sb_grid()));
             // st: the band [C0, R0) after the previous window's sB update
             if (R0 > C0) {
                 if (have_e) HT_CUDA_TRY(cudaStreamWaitEvent(st, w->evE, 0));
+                ph.mark(st, 11);
                 tm.begin(st, 4);
                 TRY(ht_band_wy(st, B, ldb, 0, C0, R0 - C0, C0, (int)wdt, (int)h, sr.Vhat + x.ov, wdt, sr.Tm + x.og, h));
                 tm.end(st);
@@ -777,9 +783,10 @@ struct Run {
             TRY(factor_and_form(f1, std::vector<Win>{x}, sb, st, sBq));
             const int64_t c1 = R0 + q + qn;  // sB: columns [c1, n)
             if (c1 < n)
-                TRY(chain_on(sBq, {ChainMat{B, ldb, 1, c1, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {c1, 0, 0}, {n, n, n}}}, 0));
+                TRY(chain_on(sBq, {ChainMat{B, ldb, 1, c1, n}}, {ChainWin{sb.Qw + x.oq, R0, (int)p, {c1, 0, 0}, {n, n, n}}}, sb_grid()));
             if (qn > 0) {
                 if (have_e) HT_CUDA_TRY(cudaStreamWaitEvent(st, w->evE, 0));
+                ph.mark(st, 11);
                 tm.begin(st, 4);
                 TRY(ht_band_wy(st, B, ldb, 1, R0 + q, qn, R0, (int)p, (int)q, sb.Vhat + x.ov, p, sb.Tm + x.og, q));
                 tm.end(st);
