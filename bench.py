@@ -274,6 +274,19 @@ def main():
             "peak_source": "cuBLAS DGEMM 8192^3 measured live (FP64 tensor pipe; no FP64 entry in MEASURED_PEAKS.json)",
             "launches_per_step": agg["chain_launches"] / args.steps,
             "flops_per_launch": agg["flops_chain"] / max(agg["chain_launches"], 1)}
+    # the same kernel alone (full grid, no concurrent streams), on the shape of the first R2
+    # update of B at this (n, nb): n rows, a chain of (n - 1 - 2nb)/nb windows of width 2nb.
+    # The live figure above is lower by design: the A/Q/Z applies run on grids capped at
+    # 56 of the 148 SMs next to the one-SM factorization chains, so their launches last longer.
+    try:
+        nwin = max(1, (n - 1 - 2 * nb) // nb)
+        sec, fl = ht.ht_bench_chain_apply(n, 2 * nb, nwin, False, 5)
+        st_ach = fl / sec / 1e12
+        roof["standalone"] = {"achieved": st_ach, "frac": st_ach / fp64_peak, "unit": "TFLOP/s",
+                              "shape": f"{n} rows x chain of {nwin} windows of {2 * nb}, full grid",
+                              "seconds": sec, "flops": fl}
+    except Exception as exc:  # measurement hook only; never affects the timed result
+        roof["standalone"] = {"error": str(exc)}
     panel_ach = agg["panel_bytes"] / max(agg["t_panel"], 1e-12) / 1e9
     roof_panel = {"bound": "hbm", "kernel": "panel_kernel (persistent panel)", "achieved": panel_ach, "peak": hbm,
                   "unit": "GB/s", "frac": panel_ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}

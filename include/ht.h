@@ -144,6 +144,19 @@ HT_API int ht_version(void);
 /* Release the cached device workspace of the current device. Returns HT_OK. */
 HT_API int ht_release_workspace(void);
 
+/*
+ * Measurement hook (bench.py's standalone roofline of the WY-apply kernel): times the
+ * chained staircase-window apply alone on the current device -- one matrix of `rows`
+ * slabs (rows for left = 0, columns for left = 1), a chain of `nwin` windows of width p
+ * overlapping by p/2 (the shape of a first-absorption R2 update at n = rows, nb = p/2),
+ * full grid, no concurrent work.  Device memory is allocated and freed inside; the data
+ * are synthetic (values do not matter for timing).  On HT_OK, *seconds is the best of
+ * `reps` launches (CUDA events) and *flops the algorithmic flops of one launch
+ * (2 * rows * p^2 * nwin).  Errors: HT_EARG_N for rows < 1, p < 2, p > 512 or nwin < 1,
+ * HT_ENOMEM, HT_ECUDA.
+ */
+HT_API int ht_bench_chain_apply(int64_t rows, int p, int nwin, int left, int reps, double *seconds, double *flops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
 HT_OK = 0
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
           -8: "HT_EARG_OPT", 1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC"}
-EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release_workspace")
+EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release_workspace", "ht_bench_chain_apply")
 
 
 class HTOptions(ctypes.Structure):
@@ -78,6 +78,9 @@ def load_library():
         lib.ht_version.argtypes = []
         lib.ht_release_workspace.restype = ctypes.c_int
         lib.ht_release_workspace.argtypes = []
+        lib.ht_bench_chain_apply.restype = ctypes.c_int
+        lib.ht_bench_chain_apply.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         _lib = lib
     return _lib
 
@@ -92,6 +95,13 @@ def ht_version() -> int:
 
 def ht_release_workspace() -> int:
     return load_library().ht_release_workspace()
+
+
+def ht_bench_chain_apply(rows: int, p: int, nwin: int, left: bool = False, reps: int = 5):
+    """Measurement hook: (best seconds, flops) of one standalone chained window apply."""
+    sec, fl = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(load_library().ht_bench_chain_apply(rows, p, nwin, int(bool(left)), reps, ctypes.byref(sec), ctypes.byref(fl)))
+    return sec.value, fl.value
 
 
 def _check(rc: int):

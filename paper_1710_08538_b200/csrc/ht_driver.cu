@@ -909,6 +909,52 @@ const char *ht_strerror(int code)
 
 int ht_version(void) { return 100; }
 
+int ht_bench_chain_apply(int64_t rows, int p, int nwin, int left, int reps, double *seconds, double *flops)
+{
+    if (rows < 1 || p < 2 || p > 512 || nwin < 1) return HT_EARG_N;
+    if (reps < 1) reps = 1;
+    const int64_t half = p / 2, width = (int64_t)(nwin - 1) * half + p;
+    double *X = nullptr, *Qw = nullptr;
+    ChainWin *dw = nullptr;
+    int rc = HT_OK;
+    if (cudaMalloc((void **)&X, (size_t)rows * width * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void **)&Qw, (size_t)p * p * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void **)&dw, (size_t)nwin * sizeof(ChainWin)) != cudaSuccess)
+        rc = HT_ENOMEM;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (rc == HT_OK) {
+        std::vector<ChainWin> hw(nwin);
+        for (int i = 0; i < nwin; ++i) hw[i] = ChainWin{Qw, (int64_t)i * half, p, {0, 0, 0}, {rows, rows, rows}};
+        const int64_t ld = left ? width : rows;
+        ChainMat m{X, ld, left, 0, rows};
+        if (cudaMemset(X, 0, (size_t)rows * width * sizeof(double)) != cudaSuccess ||
+            cudaMemset(Qw, 0, (size_t)p * p * sizeof(double)) != cudaSuccess ||
+            cudaMemcpy(dw, hw.data(), nwin * sizeof(ChainWin), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+            rc = HT_ECUDA;
+        float best = 1e30f;
+        for (int it = 0; it <= reps && rc == HT_OK; ++it) {  // first launch: warm-up
+            cudaEventRecord(e0, 0);
+            rc = ht_chain_apply(0, &m, 1, dw, nwin, p, 0);
+            cudaEventRecord(e1, 0);
+            if (cudaEventSynchronize(e1) != cudaSuccess) rc = HT_ECUDA;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it > 0 && ms < best) best = ms;
+        }
+        if (rc == HT_OK) {
+            if (seconds) *seconds = best * 1e-3;
+            if (flops) *flops = 2.0 * (double)rows * p * (double)p * nwin;
+        }
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(X);
+    cudaFree(Qw);
+    cudaFree(dw);
+    return rc;
+}
+
 int ht_release_workspace(void)
 {
     std::lock_guard<std::mutex> lk(g_mu);
