@@ -378,8 +378,6 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     const int rmax = dense + dr;      // last row that can be nonzero in column jj
                     const bool act = warp >= bw && warp * RPT <= rmax, own = warp == bw;
                     double xr[RPT];
-                    const bool cp = fprof && lane == 0 && warp == FNW - 1;
-                    long long ck0 = cp ? clock64() : 0, ck1 = 0, ck2 = 0, ck3 = 0, ck4 = 0;
                     if (act) {
                         double sa[4] = {0.0, 0.0, 0.0, 0.0};
                         const double2 *src = reinterpret_cast<const double2 *>(pivs + buf * L::MAXP + w0);
@@ -396,10 +394,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                         }
                         part[(buf * FNW + warp) * PBW + lane] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
                         if (own) rowc[buf * PBW + lane] = val[eo];
-                        if (cp) ck1 = clock64() + (sa[0] != sa[0] ? 1 : 0);
                     }
                     __syncthreads();
-                    if (cp) ck2 = clock64();
                     if (act) {
                         double pr[FNW];
 #pragma unroll
@@ -413,12 +409,10 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                         const double alpha = rowc[buf * PBW + jj];
                         const double myrow = rowc[buf * PBW + lane];
                         double tau = 0.0, scal = 0.0, beta = alpha;
-                        if (cp) ck3 = clock64() + (ss != ss ? 1 : 0) + (myrow != myrow ? 1 : 0);
                         if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
                         const double zc = myrow + scal * S;  // lanes < jj: v_lane^T v_jj = G_b(lane, jj)
                         const double wj = tau * zc;
                         if (own && lane < jj) Xs[jj * LDX + lane] = zc;
-                        if (cp) ck4 = clock64() + (wj != wj ? 1 : 0);
                         // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
                         const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
 #pragma unroll
@@ -431,14 +425,6 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     }
                     // next step's pivot slices (a warp may become active at the next step)
                     if (jj + 1 < nc && warp >= (dr + 1) / RPT && warp * RPT <= rmax + 1) put_pivot(jj + 1, buf ^ 1);
-                    if (cp) {
-                        const long long ck5 = clock64() + (val[RPT - 1] != val[RPT - 1] ? 1 : 0);
-                        atomicAdd(&fprof[12], (unsigned long long)(ck1 - ck0));
-                        atomicAdd(&fprof[13], (unsigned long long)(ck2 - ck1));
-                        atomicAdd(&fprof[14], (unsigned long long)(ck3 - ck2));
-                        atomicAdd(&fprof[15], (unsigned long long)(ck4 - ck3));
-                        atomicAdd(&fprof[16], (unsigned long long)(ck5 - ck4));
-                    }
                 }
                 FPROF(2);
                 __syncthreads();
