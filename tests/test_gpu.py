@@ -117,6 +117,27 @@ def test_config4_singular(n, nb):
           f"IR failures {rep['ir_failed_columns']}, rescales {rep['solve_rescales']}")
 
 
+def test_staircase_step_wider_than_pending_reflectors():
+    """Reading R-step: a premature absorption with k < min(32, nb) pending reflectors uses
+    windows of 2*32 x k rows stepping by 32.  Forced IR failures one, two and three
+    columns into panels (nb = 64) make k = 1, 2, 3; B is nonsingular, so the HT form is
+    unique up to signs and must match the oracle like any other blocking."""
+    A, B = ht_inputs.pencil("shifted", 400, 31)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=64, force_ir_fail=(1, 3, 7, 100, 170))
+    assert rep["premature_absorptions"] >= 4
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr, _, _ = oracle.ht_T(A, B)
+    check_parity(A, B, H, T, Hr, Tr)
+
+
+def test_chain_apply_measurement_hook():
+    """ht_bench_chain_apply (bench.py's standalone roofline) runs the product kernel."""
+    sec, fl = ht.ht_bench_chain_apply(1024, 128, 6, False, 2)
+    assert sec > 0 and fl == 2.0 * 1024 * 128 * 128 * 6
+    sec, fl = ht.ht_bench_chain_apply(512, 96, 4, True, 1)
+    assert sec > 0 and fl == 2.0 * 512 * 96 * 96 * 4
+
+
 def test_forced_ir_failures_premature_absorption():
     """IR-failure fallback (Algorithm 1): forced failures make
     the panel stop early (k < nb) and restart at the failed column."""
