@@ -590,29 +590,42 @@ struct Run {
         }
 
         // ===== R1: QL staircase of V2, top -> bottom (sec. 3.3.1b) =====
+        // + R2 on B, pipelined: st factors the windows one by one; sB forms each window's
+        // Qhat and applies it to B at once (R2's chain order), so B's R2 update ends one
+        // window apply after the last factorization instead of a whole chain later.
+        // (Rows of the R2 chain are independent, so its critical time is the chain length,
+        // not the number of rows: splitting rows off does not help.)
+        // Small k (premature absorptions): many small windows, launch-bound -> one factor launch
+        // for all windows and one chain launch on st instead.
+        cudaStream_t sBq = serial ? st : w->sB;
+        const bool pipelined = k >= 64;
         wins_reset();
+        std::vector<ChainWin> wl;
         std::vector<FactorDesc> fds;
+        ph.mark(st, 1);
         for (int i = 0; i < r; ++i) {
             const int p = (int)(rb[i + 2] - rb[i]);
             Win x = add_win(p, K);
-            fds.push_back(FactorDesc{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1,
-                                     w->Vhat + x.ov, p, w->tau + x.ot});
-            if (i > 0) fds.back().dense = p - (int)ks;  // view: [ks new rows; L of the window above, reversed; 0]
-        }
-        ph.mark(st, 1);
-        TRY(factor_and_form(fds, 0));
-        // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e, P:819-825, P:886-890, P:929-932) =====
-        // B (critical) first with the whole GPU; A (sA) and Z (sQZ) start after it.
-        const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
-        std::vector<ChainWin> wl;
-        for (int i = 0; i < r; ++i) {
-            const Win &x = wins[i];
+            FactorDesc fd{w->VW + (rb[i + 2] - 1) + (int64_t)(K - 1) * ldw, -1, -ldw, p, K, 1, w->Vhat + x.ov, p,
+                          w->tau + x.ot};
+            if (i > 0) fd.dense = p - (int)ks;  // view: [ks new rows; L of the window above, reversed; 0]
             wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
+            if (pipelined) {
+                TRY(factor_and_form(std::vector<FactorDesc>{fd}, std::vector<Win>{x}, main_store(), st, sBq));
+                TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, n}}, {wl.back()}, 0));
+            } else {
+                fds.push_back(fd);
+            }
         }
-        // (Deferring part of this B update to sB does not pay: the next R3 band update would
-        // wait for all of it.)
-        cudaStream_t sBq = serial ? st : w->sB;
-        TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
+        if (pipelined) {
+            TRY(dep(st, sBq, 11));  // B's R2 chain done, all R1 windows formed
+        } else {
+            TRY(factor_and_form(fds, 0));
+            TRY(chain_on(st, {ChainMat{B, ldb, 0, 0, n}}, wl, 0));
+        }
+        // ===== R2: B, Z, A <- . * RV_1 ... RV_r (sec. 3.3.1c-e, P:819-825, P:886-890, P:929-932) =====
+        // B above; A (sA) and Z (sQZ) take the whole chain after B's W-update.
+        const double *L1 = w->VW + (m - k);  // L^_1 (k x k lower), ld ldw
         // W-updates: B on st (+ sB), Z on sQZ, A on sA
         struct WX { double *X; int64_t ld, rows; cudaStream_t s; double *W1, *W2; } wx[2] = {
             {B, ldb, n, st, w->W1, w->W2}, {wz ? Z + qz0 : nullptr, ldz, qz1 - qz0, sQ, w->W1Q, w->W2Q}};
