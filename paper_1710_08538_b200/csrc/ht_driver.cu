@@ -668,6 +668,31 @@ struct Run {
             ws.clear();
             return 0;
         };
+        // L2's chain on B (the L1 windows from the left, bottom -> top) only touches rows the R3
+        // chain (also bottom -> top) has finished, and left and right transforms commute, so
+        // with k >= 64 each L2 window goes to B on the L1 side stream as soon as R3 has moved
+        // above its rows (overlapping the rest of R3).
+        std::vector<ChainWin> wlu;
+        for (int i = 0; i < r; ++i) {
+            const Win &x = winsL[i];
+            const int64_t R0 = J + 1 + lb[r - 1 - i];
+            wlu.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, 0, 0}, {n, n, n}});
+        }
+        cudaStream_t sLq = serial ? st : w->side_stream;
+        int nl2 = 0;  // L2 windows issued
+        auto issue_l2 = [&](int64_t row_final) -> int {  // rows >= row_final are final for R3
+            if (!pipelined) return 0;
+            bool waited = false;
+            while (nl2 < r && wlu[nl2].o >= row_final) {
+                if (!waited) {
+                    TRY(dep(sLq, st, 11));
+                    waited = true;
+                }
+                TRY(chain_on(sLq, {ChainMat{B, ldb, 1, J + 1, n}}, {wlu[nl2]}, 0));
+                ++nl2;
+            }
+            return 0;
+        };
         std::vector<Win> winsR;
         std::vector<ChainWin> wr;
         bool have_e = false;
@@ -706,9 +731,11 @@ struct Run {
                 have_e = true;
             }
             ph.mark(st, 10);
+            TRY(issue_l2(R0));
             wr.push_back(ChainWin{sr.Qw + x.oq, C0, (int)wdt, {0, 0, 0}, {n, n, n}});
             if ((int)wr.size() == BATCH || t == 0) TRY(flush_right(wr));  // A, Z take the windows in batches
         }
+        TRY(issue_l2(J + 1));
         TRY(flush_right(wr));
         TRY(dep(st, sBq, 10));  // B complete
         ph.mark(st, 3);
@@ -719,13 +746,8 @@ struct Run {
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
         TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
         TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));
-        std::vector<ChainWin> wlu;
-        for (int i = 0; i < r; ++i) {
-            const Win &x = winsL[i];
-            const int64_t R0 = J + 1 + lb[r - 1 - i];
-            wlu.push_back(ChainWin{w->QwL + x.oq, R0, x.p, {R0, 0, 0}, {n, n, n}});
-        }
-        TRY(chain_on(st, {ChainMat{B, ldb, 1, J + 1, n}}, wlu, 0));
+        if (pipelined) TRY(dep(st, sLq, 11));  // L2's B chain (issued during R3) done
+        else TRY(chain_on(st, {ChainMat{B, ldb, 1, J + 1, n}}, wlu, 0));
         // UR = [U1; R~1]  (2k x k)
         const int64_t ldur = 2 * k;
         TRY(copy2d(k, k, U + p0, n, w->UR, ldur));
