@@ -790,15 +790,15 @@ struct Run {
         // (V, T), sB forms Qhat and updates the columns to their right.
         const Store sb{w->VhatB, w->QwB, w->TmB, w->tauB, w->WtB, w->fscr};
         TRY(dep(sBq, st, 9));
-        auto flush_left = [&](std::vector<ChainWin> &ws) -> int {
+        auto flush_left = [&](std::vector<ChainWin> &ws, int grid) -> int {
             if (ws.empty()) return 0;
             TRY(dep(sA, sBq, 6));
             TRY(dep(sQ, sBq, 6));
-            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, side_grid()));
+            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, grid));
             if (wq) {
                 std::vector<ChainWin> wq_ = ws;
                 for (auto &x : wq_) x.lo[0] = 0;
-                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, side_grid()));
+                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, grid));
             }
             ws.clear();
             return 0;
@@ -833,9 +833,9 @@ struct Run {
             }
             ph.mark(st, 10);
             wb.push_back(ChainWin{sb.Qw + x.oq, R0, (int)p, {J, 0, 0}, {n, n, n}});
-            if ((int)wb.size() == BATCH) TRY(flush_left(wb));
+            if ((int)wb.size() == BATCH) TRY(flush_left(wb, side_grid()));
         }
-        TRY(flush_left(wb));
+        TRY(flush_left(wb, 0));  // the last batch: the critical stream is done, full grid
         TRY(dep(st, sBq, 10));
         ph.mark(st, 6);
         // join: the next panel reads A and B; U, V, S, T, Y, the window stores are reused
