@@ -74,6 +74,35 @@ __device__ __forceinline__ void house_scalars(double alpha, double ss, double &b
     scal = alpha >= 0.0 ? sc : -sc;
 }
 
+// Column-step scalars of the wide layout (one out-of-line copy shared by the 32 unrolled
+// steps: the unrolled loop otherwise misses in the instruction cache).  Sums the active
+// warps' partial dot products in a fixed order, then forms the reflector of column jj.
+struct StepScalars {
+    double S, tau, scal, beta, myrow;
+};
+template <int FNW>
+__device__ __noinline__ StepScalars step_scalars(const double *part, const double *rowc, int buf, int bw, int rmax,
+                                                 int rpt, int lane, int jj)
+{
+    double pr[FNW];
+#pragma unroll
+    for (int w = 0; w < FNW; ++w) pr[w] = (w >= bw && w * rpt <= rmax) ? part[(buf * FNW + w) * 32 + lane] : 0.0;
+#pragma unroll
+    for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
+#pragma unroll
+        for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
+    StepScalars r;
+    r.S = pr[0];
+    const double ss = __shfl_sync(0xffffffffu, r.S, jj);  // squared tail norm
+    const double alpha = rowc[buf * 32 + jj];
+    r.myrow = rowc[buf * 32 + lane];
+    r.tau = 0.0;
+    r.scal = 0.0;
+    r.beta = alpha;
+    if (ss > 0.0) house_scalars(alpha, ss, r.beta, r.tau, r.scal);
+    return r;
+}
+
 // Layout of one factor CTA.  Two register layouts of the 32-column panel:
 //  * leaf layout (WIDE = false, 512 threads): a warp holds 4 row groups x 8 leaf columns,
 //    RPT rows per thread and leaf, MAXP = 16 warps * 4 * RPT rows;
@@ -397,19 +426,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     }
                     __syncthreads();
                     if (act) {
-                        double pr[FNW];
-#pragma unroll
-                        for (int w = 0; w < FNW; ++w) pr[w] = (w >= bw && w * RPT <= rmax) ? part[(buf * FNW + w) * PBW + lane] : 0.0;
-#pragma unroll
-                        for (int hh = FNW / 2; hh >= 1; hh >>= 1)  // tree sum (fixed order: deterministic)
-#pragma unroll
-                            for (int w = 0; w < hh; ++w) pr[w] += pr[w + hh];
-                        const double S = pr[0];                              // v_jj-tail . column lane
-                        const double ss = __shfl_sync(0xffffffffu, S, jj);   // squared tail norm
-                        const double alpha = rowc[buf * PBW + jj];
-                        const double myrow = rowc[buf * PBW + lane];
-                        double tau = 0.0, scal = 0.0, beta = alpha;
-                        if (ss > 0.0) house_scalars(alpha, ss, beta, tau, scal);
+                        const StepScalars sc = step_scalars<FNW>(part, rowc, buf, bw, rmax, RPT, lane, jj);
+                        const double S = sc.S, myrow = sc.myrow, tau = sc.tau, scal = sc.scal, beta = sc.beta;
                         const double zc = myrow + scal * S;  // lanes < jj: v_lane^T v_jj = G_b(lane, jj)
                         const double wj = tau * zc;
                         if (own && lane < jj) Xs[jj * LDX + lane] = zc;
