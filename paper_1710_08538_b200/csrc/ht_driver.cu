@@ -517,8 +517,9 @@ struct Run {
     // transforms to A, sQZ to Z and Q (their rows/columns never feed a factorization), so
     // those big applies overlap the one-SM factorization chains.  Both are joined before
     // the next panel.  Per matrix the paper's order of operations is kept.
-    // CTAs of an A or Q/Z chain apply on the low-priority streams (measured: 56 is best at
-    // n = 8192; at n = 16384 the side work grows as n^3 against ~n^2 for the critical
+    // CTAs of an A or Q/Z chain apply on the low-priority streams (measured: 64 is best at
+    // n = 8192 -- 56 leaves the side streams as the tail of each absorption, 72+ starves the
+    // B stream; at n = 16384 the side work grows as n^3 against ~n^2 for the critical
     // factorization chains and 96 is best)
     int sb_grid() const  // CTAs of sB's full-height B updates (0: uncapped)
     {
@@ -528,7 +529,7 @@ struct Run {
     int side_grid() const
     {
         static const int env = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 0;
-        return env > 0 ? env : (n >= 12288 ? 96 : 56);
+        return env > 0 ? env : (n >= 12288 ? 96 : 64);
     }
     int absorb(int64_t s0, int64_t k)
     {

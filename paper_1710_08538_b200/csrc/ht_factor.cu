@@ -388,11 +388,21 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 // the pivot column of the next step goes through shared memory: its owner lane
                 // stores the warp's rows, the warp reads them back as broadcasts (a 64-bit
                 // shuffle per element would cost two SHFL per row and lane)
+                // The warp owning the next diagonal row writes zeros at rows <= that row, so the
+                // dot products and updates below need no per-element masks (the index bound
+                // jn % RPT is a compile-time constant of the unrolled step).
                 auto put_pivot = [&](int jn, int bn) {
                     if (lane == jn) {
                         double2 *dst = reinterpret_cast<double2 *>(pivs + bn * L::MAXP + w0);
+                        if (warp == (c0 + jn) / RPT) {
+                            const int eon = jn % RPT;  // (c0 % RPT == 0)
 #pragma unroll
-                        for (int e = 0; e < RPT; e += 2) dst[e / 2] = make_double2(val[e], val[e + 1]);
+                            for (int e = 0; e < RPT; e += 2)
+                                dst[e / 2] = make_double2(e > eon ? val[e] : 0.0, e + 1 > eon ? val[e + 1] : 0.0);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < RPT; e += 2) dst[e / 2] = make_double2(val[e], val[e + 1]);
+                        }
                     }
                     __syncwarp();
                 };
@@ -417,10 +427,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                             xr[e + 1] = t.y;
                         }
 #pragma unroll
-                        for (int e = 0; e < RPT; ++e) {
-                            const bool on = !own || e > eo;
-                            sa[e & 3] = fma(on ? xr[e] : 0.0, val[e], sa[e & 3]);
-                        }
+                        for (int e = 0; e < RPT; ++e) sa[e & 3] = fma(xr[e], val[e], sa[e & 3]);  // xr = 0 at rows <= dr
                         part[(buf * FNW + warp) * PBW + lane] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
                         if (own) rowc[buf * PBW + lane] = val[eo];
                     }
@@ -434,8 +441,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                         // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
                         const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
 #pragma unroll
-                        for (int e = 0; e < RPT; ++e)
-                            if (!own || e > eo) val[e] = fma(mx, xr[e], val[e]);
+                        for (int e = 0; e < RPT; ++e) val[e] = fma(mx, xr[e], val[e]);  // rows <= dr: xr = 0
                         if (own) {
                             val[eo] = lane > jj ? val[eo] - wj : (lane == jj ? beta : val[eo]);
                             if (lane == jj) taus[jj] = tau;
