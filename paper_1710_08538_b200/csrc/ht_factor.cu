@@ -452,34 +452,31 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 }
                 FPROF(2);
                 __syncthreads();
-                {
+                {   // the raw panel once; R (view) and V (natural order) are both stored from it
                     double2 *dst = reinterpret_cast<double2 *>(Ps + lane * L::LDP + w0);
 #pragma unroll
                     for (int e = 0; e < RPT; e += 2) {
-                        const int r = w0 + e, col = c0 + lane;
-                        const double a0 = (r <= col && r < p && lane < nc) ? val[e] : 0.0;
-                        const double a1 = (r + 1 <= col && r + 1 < p && lane < nc) ? val[e + 1] : 0.0;
+                        const int r = w0 + e;
+                        const double a0 = (r < p && lane < nc) ? val[e] : 0.0;
+                        const double a1 = (r + 1 < p && lane < nc) ? val[e + 1] : 0.0;
                         dst[e / 2] = make_double2(a0, a1);
                     }
                 }
-                store_R();
-                {
-                    double2 *dst = reinterpret_cast<double2 *>(Ps + lane * L::LDP + w0);
-                    const double tv = taus[lane < nc ? lane : 0];
-                    const int col = c0 + lane;
-#pragma unroll
-                    for (int e = 0; e < RPT; e += 2) {
-                        double a[2];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int r = w0 + e + h;
-                            const double v = (lane >= nc || r < col) ? 0.0 : (r == col ? 1.0 : (tv == 0.0 ? 0.0 : val[e + h]));
-                            a[h] = (r < p) ? v : 0.0;
-                        }
-                        dst[e / 2] = make_double2(a[0], a[1]);
-                    }
+                __syncthreads();
+                if (rs == 1 || rs == -1) {  // R: contiguous along rows: lanes over rows
+                    for (int j = warp; j < nc; j += FNW)
+                        for (int r = lane; r < p; r += 32)
+                            d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = (r <= c0 + j) ? Ps[j * L::LDP + r] : 0.0;
+                } else {                     // R: contiguous along columns: lanes over columns
+                    for (int r = warp; r < p; r += FNW)
+                        if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = (r <= c0 + lane) ? Ps[lane * L::LDP + r] : 0.0;
                 }
-                store_V();
+                for (int j = warp; j < nc; j += FNW) {  // V: unit diagonal, zeros above (and for tau = 0)
+                    const int col = c0 + j;
+                    const bool t0 = taus[j] == 0.0;
+                    for (int r = lane; r < p; r += 32)
+                        d.V[(int64_t)col * d.ldv + nat(r)] = (r < col) ? 0.0 : (r == col ? 1.0 : (t0 ? 0.0 : Ps[j * L::LDP + r]));
+                }
             } else {
             // ---- the panel in registers: val[l][e] = P(rw0 + e, 8l + c8) ----
             double val[NLF][RPT];
