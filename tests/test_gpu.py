@@ -130,6 +130,21 @@ def test_staircase_step_wider_than_pending_reflectors():
     check_parity(A, B, H, T, Hr, Tr)
 
 
+def test_streams_and_pipelining_match_one_stream_bitwise(monkeypatch):
+    """The absorption runs on five streams with cross-phase pipelining (R1/R2, R3/L2;
+    readings R-commute and R-win).  Every element must receive the same transforms in the
+    same order as on one stream (HT_SERIAL=1), so the outputs are bitwise identical;
+    forced IR failures add premature absorptions (batched, small-k path) to the run."""
+    A, B, _ = ht_inputs.config_pencil(3, n=1100)
+    out = []
+    for serial in (False, True):
+        if serial:
+            monkeypatch.setenv("HT_SERIAL", "1")
+        out.append(gpu_reduce(A, B, nb=128, force_ir_fail=(300, 301))[:4])
+    for M1, M2 in zip(*out):
+        assert np.array_equal(M1, M2)
+
+
 def test_chain_apply_measurement_hook():
     """ht_bench_chain_apply (bench.py's standalone roofline) runs the product kernel."""
     sec, fl = ht.ht_bench_chain_apply(1024, 128, 6, False, 2)
