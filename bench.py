@@ -11,9 +11,13 @@ seed 2), with A, B restored from a pristine device copy at the start of each ste
 N > 1 is launched with torch.distributed.run (one process per GPU, NCCL): all ranks
 reduce ONE pencil together (paper_1710_08538_b200/mg.py): A, B replicated, Q and Z split
 into row slabs and all-gathered at the end (strong scaling).
-Prints ONE JSON line on rank 0.  `value` is GFLOP/s counted with the fixed
-App.-A model flop count F_model(n, nb) (DESIGN.md), so both arms are comparable;
-`ms_per_step` is the wall time of one reduction (max over ranks).
+Prints ONE JSON line on rank 0.  `value` is GFLOP/s on the instrumented EXECUTED flop
+count F_exec (per-launch formulas, the paper's interposition convention P:2161-2162;
+SURVEY §8(d)); F_model (App. A) and GFLOP/s on it are in `detail`.  `ms_per_step` is the
+wall time of one reduction (max over ranks).  `roofline_e2e` is T_roof / t with
+T_roof = F_L3,exec / P64 + B_L2,exec / BW.  `configs` carries the other BASELINE.json
+configs (1, 2, 4, 5) measured in the same run (fewer steps; --also none skips them).
+`--gpus N` without WORLD_SIZE re-launches itself under torch.distributed.run.
 """
 from __future__ import annotations
 
@@ -43,24 +47,10 @@ WORKLOAD = {
 }
 
 
-def model_flops(n: int, nb: int) -> float:
-    """F_model: SURVEY App. A flop model of basic (l=2) HouseHT with Q and Z, no IR,
-    panels of nb columns: panel solves/residuals/A*v + Remark-2 GEMM + absorption
-    72 n k m + 18 k m^2 per panel.  Fixed per (n, nb); used for `value` of both arms."""
-    tot = 0.0
-    s0 = 0
-    while s0 <= n - 3:
-        k = min(nb, n - 2 - s0)
-        p0 = s0 + 1
-        M = n - p0
-        J = s0 + k
-        m = n - J - 1
-        for i in range(k):
-            tot += M * M + (M * M if i > 0 else 0.0) + 2.0 * M * (n - s0 - i - 1)
-        tot += 2.0 * p0 * M * k + 4.0 * p0 * k * k
-        tot += 72.0 * n * k * m + 18.0 * k * m * m
-        s0 = J
-    return tot
+from paper_1710_08538_b200.model import model_flops, roofline_seconds  # noqa: E402  (measurement logic)
+
+ENV_KNOBS = ("HT_SERIAL", "HT_BATCH", "HT_SIDE_GRID", "HT_SB_GRID", "HT_PANEL_NOCLUSTER", "HT_PHASES",
+             "HT_PROFILE", "HT_DEBUG_IR", "HT_TRACE_COL", "HT_FPROF", "HT_SYNC_CHECK")
 
 
 class ClockSampler:
@@ -182,6 +172,95 @@ def run_reference(args, cfg, n, nb, rank, world):
     return 0
 
 
+def relaunch_distributed(args) -> int:
+    """`--gpus N` (N > 1) without a torch.distributed environment: run this script under
+    torch.distributed.run, one process per GPU (the driver's own launch line)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def env_knobs():
+    """HT_* development switches present in the environment (recorded in the line)."""
+    return {k: os.environ[k] for k in ENV_KNOBS if k in os.environ}
+
+
+def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank, dist, want_e2e=False, A_h=None, B_h=None):
+    """Time `steps` full reductions of config `cfg` after `warmup` untimed ones (device
+    events on the caller's stream, max over ranks).  Returns a dict of measurements."""
+    if A_h is None:
+        A_h, B_h, _ = ht_inputs.config_pencil(cfg, n=n)
+    to_dev = lambda M: torch.from_numpy(np.ascontiguousarray(M.T)).cuda()
+    A0, B0 = to_dev(A_h), to_dev(B_h)
+    A, B = torch.empty_like(A0), torch.empty_like(B0)
+    Q, Z = torch.empty_like(A0), torch.empty_like(A0)
+
+    def step():
+        A.copy_(A0)  # pristine inputs each step (inputs larger than L2 at n >= 2048)
+        B.copy_(B0)
+        return mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(stream)
+    for _ in range(steps):
+        reps.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    if dist:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    out = {"elapsed": elapsed, "t_step": elapsed / steps, "reps": reps}
+    if want_e2e:
+        # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host
+        ts = []
+        for _ in range(max(1, min(steps, 2))):
+            if dist:
+                dist.barrier()
+            t0 = time.time()
+            if world == 1:
+                ht.ht_reduce(A_h, B_h, nb=nb)
+            else:
+                hA = torch.from_numpy(np.ascontiguousarray(A_h.T)).pin_memory()
+                hB = torch.from_numpy(np.ascontiguousarray(B_h.T)).pin_memory()
+                A.copy_(hA, non_blocking=True)
+                B.copy_(hB, non_blocking=True)
+                mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+                [M.cpu() for M in (A, B, Q, Z)]
+                torch.cuda.synchronize()
+            te_ = time.time() - t0
+            if dist:
+                tt = torch.tensor([te_], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te_ = float(tt.item())
+            ts.append(te_)
+        out["e2e_s"] = float(np.mean(ts))
+    del A0, B0, A, B, Q, Z
+    torch.cuda.empty_cache()
+    return out
+
+
+def summarize(reps, steps):
+    keys = ("t_panel", "t_gemm", "t_factor", "t_other", "panel_bytes", "flops", "flops_level3", "launches",
+            "t_chain", "flops_chain", "chain_launches", "t_absorb_right", "t_absorb_left", "t_factor_exposed")
+    return {k: float(np.sum([r[k] for r in reps])) / steps for k in keys}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,10 +270,13 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--nb", type=int, default=0)
+    ap.add_argument("--also", default="1,2,4,5", help="other configs measured in the same run ('none' to skip)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -213,53 +295,21 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1710_08538_b200 as ht
-
-    A_h, B_h, _ = ht_inputs.config_pencil(cfg, n=n)
-    to_dev = lambda M: torch.from_numpy(np.ascontiguousarray(M.T)).cuda()
-    A0, B0 = to_dev(A_h), to_dev(B_h)
-    A, B = torch.empty_like(A0), torch.empty_like(B0)
-    Q, Z = torch.empty_like(A0), torch.empty_like(A0)
-    stream = torch.cuda.current_stream()
-
     from paper_1710_08538_b200 import mg
 
-    def step():
-        A.copy_(A0)
-        B.copy_(B0)
-        return mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
+    stream = torch.cuda.current_stream()
+    A_h, B_h, _ = ht_inputs.config_pencil(cfg, n=n)
     clocks = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = []
-    e0.record(stream)
-    for _ in range(args.steps):
-        reps.append(step())
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    m = measure_config(torch, ht, mg, cfg, n, nb, args.steps, args.warmup, stream, world, rank, dist,
+                       want_e2e=not args.no_e2e, A_h=A_h, B_h=B_h)
     clk = clocks.stop()
-    elapsed = e0.elapsed_time(e1) * 1e-3
-    if dist:
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-    t_step = elapsed / args.steps
-    Fm = model_flops(n, nb)
-    value = Fm / t_step / 1e9  # one pencil per step, whatever the number of GPUs
-
-    agg = {k: float(np.sum([r[k] for r in reps])) for k in
-           ("t_panel", "t_gemm", "t_factor", "t_other", "panel_bytes", "flops", "flops_level3", "launches",
-            "t_chain", "flops_chain", "chain_launches")}
+    elapsed, t_step, reps = m["elapsed"], m["t_step"], m["reps"]
+    agg = summarize(reps, args.steps)
     rep0 = reps[-1]
+    Fm = model_flops(n, nb)
+    Fx = agg["flops"]
+    value = Fx / t_step / 1e9  # executed flops of one pencil per second, whatever the number of GPUs
 
     # roofline of the dominant kernel class
     peaks = measured_peaks()
@@ -272,12 +322,10 @@ def main():
     roof = {"bound": "tensor", "kernel": "chain_apply_kernel (FP64 DMMA window applies, K8/K9)", "achieved": ach,
             "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": None,
             "peak_source": "cuBLAS DGEMM 8192^3 measured live (FP64 tensor pipe; no FP64 entry in MEASURED_PEAKS.json)",
-            "launches_per_step": agg["chain_launches"] / args.steps,
+            "launches_per_step": agg["chain_launches"],
             "flops_per_launch": agg["flops_chain"] / max(agg["chain_launches"], 1)}
     # the same kernel alone (full grid, no concurrent streams), on the shape of the first R2
     # update of B at this (n, nb): n rows, a chain of (n - 1 - 2nb)/nb windows of width 2nb.
-    # The live figure above is lower by design: the A/Q/Z applies run on grids capped at
-    # 56 of the 148 SMs next to the one-SM factorization chains, so their launches last longer.
     try:
         nwin = max(1, (n - 1 - 2 * nb) // nb)
         sec, fl = ht.ht_bench_chain_apply(n, 2 * nb, nwin, False, 5)
@@ -290,42 +338,52 @@ def main():
     panel_ach = agg["panel_bytes"] / max(agg["t_panel"], 1e-12) / 1e9
     roof_panel = {"bound": "hbm", "kernel": "panel_kernel (persistent panel)", "achieved": panel_ach, "peak": hbm,
                   "unit": "GB/s", "frac": panel_ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    # whole-path roofline: level-3 flops at the FP64 tensor peak + panel bytes at HBM
+    t_roof = roofline_seconds(agg["flops_level3"], agg["panel_bytes"], fp64_peak, hbm)
+    roof_e2e = {"t_roof_s": t_roof, "t_s": t_step, "frac": t_roof / t_step,
+                "flops_level3_exec": agg["flops_level3"], "panel_bytes_exec": agg["panel_bytes"],
+                "p64_tflops": fp64_peak, "hbm_gbs": hbm}
+    # WY-apply phase (SURVEY §8(d) "Phase definitions"): all chain applies + DMMA GEMMs
+    wy_t = agg["t_chain"] + agg["t_gemm"]
+    wy = {"tflops": agg["flops_level3"] / max(wy_t, 1e-12) / 1e12, "frac": agg["flops_level3"] / max(wy_t, 1e-12) / 1e12 / fp64_peak,
+          "note": "sum of launch durations on concurrent streams (a per-launch rate while sharing the GPU)"}
 
     e2e = None
-    if not args.no_e2e:
-        # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host
-        ts = []
-        for _ in range(max(1, min(args.steps, 2))):
-            if dist:
-                dist.barrier()
-            t0 = time.time()
-            if world == 1:
-                ht.ht_reduce(A_h, B_h, nb=nb)
-            else:
-                hA = torch.from_numpy(np.ascontiguousarray(A_h.T)).pin_memory()
-                hB = torch.from_numpy(np.ascontiguousarray(B_h.T)).pin_memory()
-                A.copy_(hA, non_blocking=True)
-                B.copy_(hB, non_blocking=True)
-                mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
-                outs = [M.cpu() for M in (A, B, Q, Z)]
-                torch.cuda.synchronize()
-            te_ = time.time() - t0
-            if dist:
-                tt = torch.tensor([te_], dtype=torch.float64, device="cuda")
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                te_ = float(tt.item())
-            ts.append(te_)
-        te = float(np.mean(ts))
-        e2e = {"value": Fm / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
+    if "e2e_s" in m:
+        te = m["e2e_s"]
+        e2e = {"value": Fx / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
                "d2h_bytes_per_step": 4 * n * n * 8, "s_per_step": te}
+
+    # the other BASELINE.json configs, same binary, fewer steps (parity-tested sizes)
+    others = {}
+    if args.also != "none" and world >= 1:
+        for c in [int(x) for x in args.also.split(",") if x.strip()]:
+            if c == cfg or c not in ht_inputs.CONFIGS:
+                continue
+            nc, nbc = ht_inputs.CONFIGS[c]["n"], ht_inputs.CONFIGS[c]["nb"]
+            st_, wu_ = (10, 3) if nc <= 2048 else (2, 1)
+            mc = measure_config(torch, ht, mg, c, nc, nbc, st_, wu_, stream, world, rank, dist)
+            ac = summarize(mc["reps"], st_)
+            rc0 = mc["reps"][-1]
+            others[f"cfg{c}"] = {"workload": WORKLOAD[c], "n": nc, "nb": nbc, "steps": st_, "warmup": wu_,
+                                 "ms_per_step": mc["t_step"] * 1e3, "gflops_exec": ac["flops"] / mc["t_step"] / 1e9,
+                                 "gflops_model": model_flops(nc, nbc) / mc["t_step"] / 1e9,
+                                 "roofline_e2e_frac": roofline_seconds(ac["flops_level3"], ac["panel_bytes"], fp64_peak, hbm) / mc["t_step"],
+                                 "t_panel_s": ac["t_panel"], "t_absorb_right_s": ac["t_absorb_right"],
+                                 "t_absorb_left_s": ac["t_absorb_left"], "t_factor_exposed_s": ac["t_factor_exposed"],
+                                 "ir_extra_columns": rc0["ir_extra_columns"], "ir_steps": rc0["ir_steps_total"],
+                                 "ir_failed_columns": rc0["ir_failed_columns"],
+                                 "premature_absorptions": rc0["premature_absorptions"],
+                                 "desingularizations": rc0["desingularizations"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_oracle_sample(A_h, B_h, budget_s=15.0)
-        cpu = {"value": Fm / s["t_full_est"] / 1e9, "unit": "GFLOP/s", "cores": s["cores"], "kind": "oracle",
+        cpu = {"value": Fx / s["t_full_est"] / 1e9, "unit": "GFLOP/s", "cores": s["cores"], "kind": "oracle",
                "sample": f"Oracle-T (oracle/ht_oracle.c, as it stands) on columns 0..{s['cols'] - 1} of the same "
                          f"n={n} pencil ({s['t_sample']:.1f} s), extrapolated by its flop model to "
-                         f"{s['t_full_est']:.0f} s per full reduction"}
+                         f"{s['t_full_est']:.0f} s per full reduction",
+               "full_run": full_oracle_run(cfg, n)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -334,17 +392,19 @@ def main():
                 "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
                            "n": n, "nb": nb, "seed": ht_inputs.CONFIGS[cfg]["seed"],
                            "l2": "inputs larger than L2 (A,B,Q,Z = 4 x %.0f MB)" % (n * n * 8 / 1e6),
-                           "parallelism": (f"AB-replicated, QZ-rowslab{world}" if world > 1 else "single")},
-                "roofline": roof, "roofline_panel": roof_panel, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(agg["launches"]), "clocks": clk,
-                "detail": {"gflops_executed": agg["flops"] / elapsed / 1e9, "model_flops": Fm,
-                           "executed_flops_per_step": agg["flops"] / args.steps,
-                           "t_panel_s": agg["t_panel"] / args.steps, "t_gemm_s": agg["t_gemm"] / args.steps,
-                           "t_factor_s": agg["t_factor"] / args.steps, "t_other_s": agg["t_other"] / args.steps,
-                           "t_chain_s": agg["t_chain"] / args.steps,
+                           "parallelism": (f"mg{world}" if world > 1 else "single"),
+                           "value_flops": "executed (instrumented per launch)", "env_knobs": env_knobs()},
+                "roofline": roof, "roofline_panel": roof_panel, "roofline_e2e": roof_e2e, "wy_apply_phase": wy,
+                "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(agg["launches"] * args.steps), "clocks": clk, "configs": others,
+                "detail": {"gflops_model": Fm / t_step / 1e9, "model_flops": Fm,
+                           "executed_flops_per_step": Fx, "exec_over_model": Fx / Fm,
+                           "t_panel_s": agg["t_panel"], "t_gemm_s": agg["t_gemm"],
+                           "t_factor_s": agg["t_factor"], "t_factor_exposed_s": agg["t_factor_exposed"],
+                           "t_absorb_right_s": agg["t_absorb_right"], "t_absorb_left_s": agg["t_absorb_left"],
+                           "t_other_s": agg["t_other"], "t_chain_s": agg["t_chain"],
                            "gemm_tflops": (agg["flops_level3"] - agg["flops_chain"]) / max(agg["t_gemm"], 1e-9) / 1e12,
-                           "panel_gbs": agg["panel_bytes"] / max(agg["t_panel"], 1e-9) / 1e9,
-                           "fp64_dgemm_probe_tflops": fp64_peak,
+                           "panel_gbs": panel_ach, "fp64_dgemm_probe_tflops": fp64_peak,
                            "ir_steps": rep0["ir_steps_total"], "ir_extra_columns": rep0["ir_extra_columns"],
                            "ir_failed_columns": rep0["ir_failed_columns"],
                            "desingularizations": rep0["desingularizations"], "panels": rep0["panels"]}}
@@ -353,6 +413,19 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def full_oracle_run(cfg, n):
+    """A full (not sampled) oracle run on this pencil, if one was recorded (tests/golden/, written by
+    scripts/make_fullsize_golden.py on the build container's host: say so, it is another machine)."""
+    for w in ("T", "G"):
+        p = os.path.join(ROOT, "tests", "golden", f"fullsize_cfg{cfg}_{w}.npz")
+        if os.path.exists(p):
+            g = np.load(p)
+            if int(g["n"]) == n:
+                return {"oracle": f"Oracle-{w}", "seconds": float(g["seconds"]), "threads": int(g["threads"]),
+                        "host": "build container (8 vCPU), not the GPU box"}
+    return None
 
 
 if __name__ == "__main__":

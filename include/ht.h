@@ -30,12 +30,20 @@
  * Error behaviour: arguments are validated before any write -- on a negative
  * return code every buffer is untouched.  Positive codes are runtime errors
  * after which buffer contents are unspecified (except HT_ENONFINITE and
- * HT_EARG_B, detected before any write).
+ * HT_EARG_B, detected before any write).  On every return the library's
+ * internal streams have finished all work of the call (nothing keeps writing the
+ * caller's buffers), and the caller's stream is ordered after the call.
+ *
+ * Range: inputs are scaled by exact powers of two at entry when max|A| or max|B|
+ * lies outside [2^-100, 2^100] (undone on H, T at exit; Q, Z are invariant), so
+ * any finite pencil is accepted; a non-finite entry in the result is reported as
+ * HT_ENUMERIC.
  *
  * Ownership: the caller owns A, B, Q, Z (host memory for ht_reduce, device
  * memory for ht_reduce_ex).  The library owns its device workspace (cached per
  * device, reused across calls) and keeps no caller pointer after returning.
- * Calls on the same device are serialised by an internal mutex.
+ * Calls on the same device are serialised by an internal per-device mutex;
+ * calls on different devices (e.g. one host thread per GPU) run concurrently.
  *
  * No CPU fallback exists: without a CUDA device every entry point returns
  * HT_ECUDA.
@@ -62,11 +70,15 @@ enum {
     HT_EARG_B = -3,     /* B == NULL, ldb < n, or B not upper triangular        */
     HT_EARG_Q = -4,     /* wantq and (Q == NULL or ldq < n)                     */
     HT_EARG_Z = -5,     /* wantz and (Z == NULL or ldz < n)                     */
-    HT_EARG_OPT = -8,   /* invalid ht_options                                   */
+    HT_EARG_WANTQ = -6, /* wantq not 0 or 1                                     */
+    HT_EARG_WANTZ = -7, /* wantz not 0 or 1                                     */
+    HT_EARG_NB = -8,    /* nb > 2^20 (absurd; nb <= 0 selects the default)      */
+    HT_EARG_OPT = -9,   /* invalid ht_options                                   */
     HT_ENONFINITE = 1,  /* A or B holds Inf/NaN (detected before any write)     */
     HT_ECUDA = 2,       /* CUDA runtime error / no device                       */
     HT_ENOMEM = 3,      /* device allocation failed                             */
-    HT_ENUMERIC = 4     /* internal numerical guard tripped (non-finite result) */
+    HT_ENUMERIC = 4,    /* internal numerical guard tripped: a non-finite entry in H, T, Q or Z */
+    HT_ENCCL = 5        /* NCCL error (ht_reduce_mg)                                            */
 };
 
 /* Options for ht_reduce_ex (zero-initialise, then set what you need). */
@@ -117,6 +129,18 @@ typedef struct {
                                /* launches; launches on concurrent streams overlap)     */
     double flops_chain;        /* FP64 flops executed by the chained window applies     */
     int64_t chain_launches;    /* chained window-apply launches                         */
+    /* critical-stream phase times (device seconds, CUDA events on the library's high-
+       priority stream): absorb-right = R1..R3 (sec. 3.3.1), absorb-left = L1..L3 (sec.
+       3.3.2); factor_exposed = factorization launches on that stream (the staircase chains
+       the critical path waits for)                                                      */
+    double t_absorb_right;
+    double t_absorb_left;
+    double t_factor_exposed;
+    /* exact power-of-two scalings applied at entry (and undone on H, T at exit) so that
+       squared norms cannot overflow or underflow: A <- scale_a A, B <- scale_b B (1 = none;
+       Q and Z are invariant under such scalings)                                       */
+    double scale_a;
+    double scale_b;
 } ht_report;
 
 /*

@@ -24,7 +24,8 @@ LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
 
 HT_OK = 0
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
-          -8: "HT_EARG_OPT", 1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC"}
+          -6: "HT_EARG_WANTQ", -7: "HT_EARG_WANTZ", -8: "HT_EARG_NB", -9: "HT_EARG_OPT",
+          1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC", 5: "HT_ENCCL"}
 EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release_workspace", "ht_bench_chain_apply")
 
 
@@ -44,7 +45,9 @@ class HTReport(ctypes.Structure):
                 ("desingularizations", ctypes.c_int64), ("solve_rescales", ctypes.c_int64),
                 ("t_panel", ctypes.c_double), ("t_gemm", ctypes.c_double), ("t_factor", ctypes.c_double),
                 ("t_other", ctypes.c_double), ("panel_bytes", ctypes.c_double), ("launches", ctypes.c_int64),
-                ("t_chain", ctypes.c_double), ("flops_chain", ctypes.c_double), ("chain_launches", ctypes.c_int64)]
+                ("t_chain", ctypes.c_double), ("flops_chain", ctypes.c_double), ("chain_launches", ctypes.c_int64),
+                ("t_absorb_right", ctypes.c_double), ("t_absorb_left", ctypes.c_double),
+                ("t_factor_exposed", ctypes.c_double), ("scale_a", ctypes.c_double), ("scale_b", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

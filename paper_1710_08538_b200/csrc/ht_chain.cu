@@ -445,12 +445,12 @@ size_t band_smem(int pmax)
 }
 int band_init()
 {
-    static bool init = false;
-    if (!init) {
+    static std::mutex mu;
+    static unsigned long long done = 0;
+    return ht_once_per_device(mu, done, [] {
         HT_CUDA_TRY(cudaFuncSetAttribute(band_wy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        init = true;
-    }
-    return 0;
+        return 0;
+    });
 }
 
 }  // namespace
@@ -507,13 +507,15 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
     if (nblk == 0) return 0;
     const int kc = P.cap <= 256 ? 16 : 8;
     const size_t smem = ((size_t)P.cap * (P.h + CHAIN_PAD) + 2 * (size_t)kc * (P.cap + CHAIN_PAD)) * sizeof(double);
-    static bool init = false;
-    if (!init) {
+    static std::mutex mu;
+    static unsigned long long done = 0;
+    const int rc = ht_once_per_device(mu, done, [] {
         const int mx = (int)(SLAB_ELEMS + CHAIN_PAD * 512 + 2 * 16 * (256 + CHAIN_PAD)) * 8;
         HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         HT_CUDA_TRY(cudaFuncSetAttribute(chain_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        init = true;
-    }
+        return 0;
+    });
+    if (rc) return rc;
     const unsigned grid = (unsigned)(maxgrid > 0 && nblk > maxgrid ? maxgrid : nblk);
     if (kc == 16) chain_apply_kernel<16><<<grid, CNT, smem, st>>>(P);
     else chain_apply_kernel<8><<<grid, CNT, smem, st>>>(P);

@@ -77,4 +77,21 @@ int ht_fill2d(cudaStream_t st, int64_t rows, int64_t cols, double *dst, int64_t 
               double diag);
 
 // running flop counter (instrumentation, paper convention P:2161-2162)
-extern double g_ht_flops;
+extern thread_local double g_ht_flops;
+
+// Per-device one-time setup (function attributes such as the dynamic shared-memory
+// opt-in apply per device context): runs `f` once for each device it is called on.
+// `done` is a bitmask over device ordinals, guarded by `mu`.
+#include <mutex>
+template <class F>
+int ht_once_per_device(std::mutex &mu, unsigned long long &done, F f)
+{
+    int dev = 0;
+    HT_CUDA_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done & bit) return 0;
+    const int rc = f();
+    if (rc == 0) done |= bit;
+    return rc;
+}

@@ -70,22 +70,26 @@ struct Work {
     int *d_irtrace = nullptr;
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
     int *dsafe = nullptr;
+    double *fro_part = nullptr;  // fixed-order partial sums of ||B||_F^2
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // timing events of one call
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     void *d_bd = nullptr, *h_bd = nullptr;  // band/Qhat-formation descriptors (one per factor descriptor)
     ChainWin *d_cw = nullptr, *h_cw = nullptr;
     int64_t ndesc = 0, ncw = 0, fd_cur = 0, ld_cur = 0, cw_cur = 0;
 };
 
-std::mutex g_mu;
+std::mutex g_mu[16];  // one per device: calls on different devices run concurrently
 Work g_work[16];
 
 // Per-kernel-class device time from CUDA events recorded on the launch stream.
-// Classes: 0 panel, 1 DMMA GEMM, 2 factorizations, 3 other, 4 chained window applies.
+// Classes: 0 panel, 1 DMMA GEMM, 2 factorizations (side streams), 3 other, 4 chained window
+// applies, 5 absorb-right span and 6 absorb-left span (critical stream), 7 factorizations on
+// the critical stream.
 struct Timer {
     std::vector<cudaEvent_t> all, free_;
     struct Pend { int cls; cudaEvent_t a, b; };
     std::vector<Pend> pending;
-    double acc[5] = {0, 0, 0, 0, 0};
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int64_t launches = 0;
     int cls = 0;
     cudaEvent_t cur = nullptr;
@@ -118,6 +122,19 @@ struct Timer {
             const cudaError_t r = cudaStreamSynchronize(st);
             if (r != cudaSuccess) fprintf(stderr, "[ht sync] launch %lld (class %d) failed: %s\n", (long long)launches, cls, cudaGetErrorString(r));
         }
+    }
+    // an interval on `st` that is not a launch (phase spans): begin with span_begin, end with span_end
+    cudaEvent_t span_begin(cudaStream_t st)
+    {
+        cudaEvent_t e = get();
+        cudaEventRecord(e, st);
+        return e;
+    }
+    void span_end(cudaStream_t st, int c, cudaEvent_t a)
+    {
+        cudaEvent_t e = get();
+        cudaEventRecord(e, st);
+        pending.push_back({c, a, e});
     }
     // Resolve the first `upto` pending intervals (their events must have completed); the
     // driver calls this after enqueueing the next absorption so that the host work of
@@ -158,6 +175,8 @@ void work_free(Work &w)
     if (w.d_force) cudaFree(w.d_force);
     if (w.d_irtrace) cudaFree(w.d_irtrace);
     w.d_irtrace = nullptr;
+    if (w.fro_part) cudaFree(w.fro_part);
+    w.fro_part = nullptr;
     if (w.Dinv) cudaFree(w.Dinv);
     if (w.Bt) cudaFree(w.Bt);
     w.Bt = nullptr;
@@ -260,6 +279,9 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     }
     if (cudaMalloc((void **)&w.d_force, (size_t)N * sizeof(int64_t)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMalloc((void **)&w.d_irtrace, (size_t)N * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    TRY(dalloc(&w.fro_part, (size_t)ht_fro_scratch_size()));
+    if (!w.ev_t0 && (cudaEventCreate(&w.ev_t0) != cudaSuccess || cudaEventCreate(&w.ev_t1) != cudaSuccess))
+        return HT_ECUDA;
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
     TRY(dalloc(&w.Bt, (size_t)N * (size_t)N));
     TRY(dalloc(&w.ypart, (size_t)(N / 256 + 2) * (size_t)N));
@@ -444,7 +466,7 @@ struct Run {
             extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
-        tm.begin(s, 2);
+        tm.begin(s, s == st ? 7 : 2);
         TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
         tm.end(s);
         if (s == st) ph.mark(st, 8);
@@ -484,7 +506,6 @@ struct Run {
     int chain(const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl) { return chain_on(st, mats, wl, 0); }
     int chain_on(cudaStream_t s, const std::vector<ChainMat> &mats, const std::vector<ChainWin> &wl, int maxgrid)
     {
-        if (s != st && getenv("HT_SKIP_SIDE")) return 0;  // debug timing experiment only (wrong results)
         if (wl.empty() || mats.empty()) return 0;
         const int nw = (int)wl.size();
         if (w->cw_cur + nw > w->ncw) return HT_ENUMERIC;
@@ -570,6 +591,7 @@ struct Run {
         TRY(copy2d(m, k, V + J + 1, n, w->VW, ldw));
         TRY(copy2d(m, k, U + J + 1, n, w->UW, ldw));
         const int K = (int)k;
+        cudaEvent_t span_r = tm.span_begin(st);
 
         // ===== L1: QR staircase of U2, bottom -> top (sec. 3.3.2b) =====
         // It depends only on U2, so it is factored on the side stream while R1-R3 run.
@@ -740,6 +762,8 @@ struct Run {
         TRY(flush_right(wr));
         TRY(dep(st, sBq, 10));  // B complete
         ph.mark(st, 3);
+        tm.span_end(st, 5, span_r);
+        cudaEvent_t span_l = tm.span_begin(st);
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
         ph.mark(st, 4);
         // ===== L2: spike, chain on B, A, Q, W-updates =====
@@ -843,6 +867,7 @@ struct Run {
         TRY(dep(st, sA, 7));
         TRY(dep(st, sQ, 8));
         ph.mark(st, 7);
+        tm.span_end(st, 6, span_l);
         return 0;
     }
 
@@ -883,7 +908,10 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     if (n > 0 && (!B || ldb < n)) return HT_EARG_B;
     if (n > 0 && wantq && (!Q || ldq < n)) return HT_EARG_Q;
     if (n > 0 && wantz && (!Z || ldz < n)) return HT_EARG_Z;
-    if (opt && opt->n_force_ir_fail > 0 && !opt->force_ir_fail) return HT_EARG_OPT;
+    if (wantq != 0 && wantq != 1) return HT_EARG_WANTQ;
+    if (wantz != 0 && wantz != 1) return HT_EARG_WANTZ;
+    if (opt && opt->nb > ((int64_t)1 << 20)) return HT_EARG_NB;
+    if (opt && (opt->n_force_ir_fail < 0 || (opt->n_force_ir_fail > 0 && !opt->force_ir_fail))) return HT_EARG_OPT;
     if (opt && (opt->row_begin != 0 || opt->row_end != 0) &&
         (opt->row_begin < 0 || opt->row_end > n || opt->row_begin > opt->row_end))
         return HT_EARG_OPT;
@@ -993,65 +1021,52 @@ int ht_bench_chain_apply(int64_t rows, int p, int nwin, int left, int reps, doub
 
 int ht_release_workspace(void)
 {
-    std::lock_guard<std::mutex> lk(g_mu);
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HT_ECUDA;
-    if (dev >= 0 && dev < 16) work_free(g_work[dev]);
+    if (dev < 0 || dev >= 16) return HT_OK;
+    std::lock_guard<std::mutex> lk(g_mu[dev]);
+    work_free(g_work[dev]);
     return HT_OK;
 }
 
-int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
-                 int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep)
+// Everything of one reduction after the caller's stream has forked into R.st.  Any error
+// return leaves work queued on the library streams; ht_reduce_ex drains them.
+int reduce_body(Run &R, const ht_options *opt)
 {
-    int rc = validate(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt);
-    if (rc) return rc;
-    if (n == 0) {
-        if (rep) memset(rep, 0, sizeof(*rep));
-        return HT_OK;
-    }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
-    std::lock_guard<std::mutex> lk(g_mu);
-    int dev = 0;
-    HT_CUDA_TRY(cudaGetDevice(&dev));
-    int64_t nb = (opt && opt->nb > 0) ? opt->nb : 128;
-    nb = std::max<int64_t>(1, std::min<int64_t>({nb, 256, std::max<int64_t>(1, n - 2)}));
-    Work *w = nullptr;
-    TRY(work_get(dev, n, nb, &w));
-    Run R;
-    memset(&R.rep, 0, sizeof(R.rep));
-    R.w = w;
-    // the caller's stream forks into the library's high-priority stream and joins it at the end
-    // (NULL is the legacy default stream, exactly as in the CUDA runtime: work the caller
-    //  queued there, e.g. the copies that produced A and B, is ordered before the reduction)
-    const cudaStream_t user_st = opt ? (cudaStream_t)opt->stream : (cudaStream_t)0;
-    R.st = w->hp_stream;
-    HT_CUDA_TRY(cudaEventRecord(w->ev[9], user_st));
-    HT_CUDA_TRY(cudaStreamWaitEvent(R.st, w->ev[9], 0));
-    R.n = n; R.nb = nb;
-    R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
-    R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
-    R.wq = wantq != 0; R.wz = wantz != 0;
-    R.qz0 = 0; R.qz1 = n;
-    if (opt && (opt->row_begin != 0 || opt->row_end != 0)) { R.qz0 = opt->row_begin; R.qz1 = opt->row_end; }
+    Work *w = R.w;
     cudaStream_t st = R.st;
-    g_ht_flops = 0.0;
+    const int64_t n = R.n, nb = R.nb;
+    double *dA = R.A, *dB = R.B, *dQ = R.Q, *dZ = R.Z;
+    const int64_t ldda = R.lda, lddb = R.ldb, lddq = R.ldq, lddz = R.ldz;
+    unsigned long long *d_max = reinterpret_cast<unsigned long long *>(w->d_scal + 4);
 
-    // validation that needs the data: finite entries, B upper triangular (before any write)
-    TRY(ht_check_input(st, n, dA, ldda, dB, lddb, w->d_iflags));
+    // validation that needs the data: finite entries, B upper triangular (before any write);
+    // the same pass finds max|A|, max|B| for the range scaling below
+    TRY(ht_check_input(st, n, dA, ldda, dB, lddb, w->d_iflags, d_max));
     HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    HT_CUDA_TRY(cudaMemcpyAsync(w->h_scal + 4, d_max, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     HT_CUDA_TRY(cudaStreamSynchronize(st));
     if (w->h_iflags[0]) return HT_ENONFINITE;
     if (w->h_iflags[1]) return HT_EARG_B;
+    // exact power-of-two range scaling (include/ht.h "Range"): squared norms of columns,
+    // reflectors and ||B||_F stay finite and normal; no rounding is introduced, and the
+    // result is bitwise that of the unscaled computation whenever no scaling is needed
+    auto pick = [](double mx) -> double {
+        if (!(mx > 0.0) || (mx >= 0x1p-100 && mx <= 0x1p100)) return 1.0;
+        return ldexp(1.0, -ilogb(mx));
+    };
+    const double sa = pick(w->h_scal[4]), sb = pick(w->h_scal[5]);
+    R.rep.scale_a = sa;
+    R.rep.scale_b = sb;
+    TRY(ht_scale(st, n, n, dA, ldda, sa));
+    TRY(ht_scale(st, n, n, dB, lddb, sb));
 
-    cudaEvent_t e0, e1;
-    HT_CUDA_TRY(cudaEventCreate(&e0));
-    HT_CUDA_TRY(cudaEventCreate(&e1));
-    HT_CUDA_TRY(cudaEventRecord(e0, st));
+    HT_CUDA_TRY(cudaEventRecord(w->ev_t0, st));
     if (R.wq) TRY(ht_fill2d(st, n, n, dQ, lddq, 0.0, 1.0));
     if (R.wz) TRY(ht_fill2d(st, n, n, dZ, lddz, 0.0, 1.0));
+    int64_t ndesing = 0;
     if (n > 2) {
-        TRY(ht_fro_norm_sq(st, n, n, dB, lddb, w->d_scal));
+        TRY(ht_fro_norm_sq(st, n, n, dB, lddb, w->d_scal, w->fro_part));
         HT_CUDA_TRY(cudaMemcpyAsync(w->h_scal, w->d_scal, sizeof(double), cudaMemcpyDeviceToHost, st));
         HT_CUDA_TRY(cudaStreamSynchronize(st));
         const double nB = sqrt(w->h_scal[0]);
@@ -1063,31 +1078,42 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             std::vector<int64_t> fl(opt->force_ir_fail, opt->force_ir_fail + opt->n_force_ir_fail);
             std::sort(fl.begin(), fl.end());
             nforce = (int)std::min<int64_t>((int64_t)fl.size(), w->ncap);
-            HT_CUDA_TRY(cudaMemcpy(w->d_force, fl.data(), nforce * sizeof(int64_t), cudaMemcpyHostToDevice));
+            HT_CUDA_TRY(cudaMemcpyAsync(w->d_force, fl.data(), nforce * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
         }
         HT_CUDA_TRY(cudaMemsetAsync(w->d_iflags, 0, sizeof(int), st));
         HT_CUDA_TRY(cudaMemsetAsync(w->d_irtrace, 0, (size_t)n * sizeof(int), st));
+        // development switches (HT_DEBUG_IR, HT_PROFILE, HT_TRACE_COL, HT_FPROF): diagnostics
+        // printed to stderr; they add instrumentation but never change the arithmetic
+        struct DevBuf {
+            void *p = nullptr;
+            ~DevBuf() { if (p) cudaFree(p); }
+        } dbg_buf, prof_buf, ttr_buf, fprof_buf;
         double *dbg = nullptr;
         const bool dbg_on = getenv("HT_DEBUG_IR") != nullptr;
         double *ptime = nullptr;
         const bool prof_on = getenv("HT_PROFILE") != nullptr;
         if (prof_on) {
-            HT_CUDA_TRY(cudaMalloc((void **)&ptime, 16 * sizeof(double)));
+            HT_CUDA_TRY(cudaMalloc(&prof_buf.p, 16 * sizeof(double)));
+            ptime = (double *)prof_buf.p;
             HT_CUDA_TRY(cudaMemset(ptime, 0, 16 * sizeof(double)));
         }
         if (dbg_on) {
-            HT_CUDA_TRY(cudaMalloc((void **)&dbg, (size_t)n * 12 * sizeof(double)));
+            HT_CUDA_TRY(cudaMalloc(&dbg_buf.p, (size_t)n * 12 * sizeof(double)));
+            dbg = (double *)dbg_buf.p;
             HT_CUDA_TRY(cudaMemset(dbg, 0, (size_t)n * 12 * sizeof(double)));
         }
         unsigned long long *ttr = nullptr;
         const int64_t tcol = getenv("HT_TRACE_COL") ? atoll(getenv("HT_TRACE_COL")) : -1;
         if (tcol >= 0) {
-            HT_CUDA_TRY(cudaMalloc((void **)&ttr, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+            HT_CUDA_TRY(cudaMalloc(&ttr_buf.p, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+            ttr = (unsigned long long *)ttr_buf.p;
             HT_CUDA_TRY(cudaMemset(ttr, 0, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
         }
         unsigned long long *fprof = nullptr;
         if (getenv("HT_FPROF")) {
-            HT_CUDA_TRY(cudaMalloc((void **)&fprof, 32 * sizeof(unsigned long long)));
+            HT_CUDA_TRY(cudaMalloc(&fprof_buf.p, 32 * sizeof(unsigned long long)));
+            fprof = (unsigned long long *)fprof_buf.p;
             HT_CUDA_TRY(cudaMemset(fprof, 0, 32 * sizeof(unsigned long long)));
             TRY(ht_factor_set_prof(fprof));
         }
@@ -1153,15 +1179,15 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
             if (opt && opt->max_panels > 0 && R.rep.panels >= opt->max_panels) break;
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        HT_CUDA_TRY(cudaStreamSynchronize(st));
+        ndesing = w->h_iflags[0];
         if (prof_on) {
-            HT_CUDA_TRY(cudaStreamSynchronize(st));
             double hp[16];
             HT_CUDA_TRY(cudaMemcpy(hp, ptime, sizeof(hp), cudaMemcpyDeviceToHost));
             const char *names[8] = {"P1", "P2+trsv", "P3 rest", "P4 r+IR", "P5 A*v", "P5 Y", "P4 w", "P4 B*w"};
             fprintf(stderr, "[ht profile] panel phases (s):");
             for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.3f", names[i], hp[i]);
             fprintf(stderr, "\n");
-            cudaFree(ptime);
         }
         if (fprof) {
             HT_CUDA_TRY(cudaDeviceSynchronize());
@@ -1173,10 +1199,8 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
                     hp[11] * 1e-9, hp[5] * 1e-9, hp[6] * 1e-9, hp[7] * 1e-9, hp[26], hp[24] / (double)(hp[26] ? hp[26] : 1),
                     hp[25] / (double)(hp[26] ? hp[26] : 1));
             TRY(ht_factor_set_prof(nullptr));
-            cudaFree(fprof);
         }
         if (ttr) {
-            HT_CUDA_TRY(cudaStreamSynchronize(st));
             const int nbk = (int)((n - 1 + 127) / 128) + 2;
             std::vector<unsigned long long> h((size_t)nbk * 4);
             HT_CUDA_TRY(cudaMemcpy(h.data(), ttr, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -1189,10 +1213,8 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
                     fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f %8.2f\n", b, h[4 * b] ? (h[4 * b] - t0) * 1e-3 : -1.0,
                             h[4 * b + 1] ? (h[4 * b + 1] - t0) * 1e-3 : -1.0, h[4 * b + 3] ? (h[4 * b + 3] - t0) * 1e-3 : -1.0,
                             (h[4 * b + 2] - t0) * 1e-3);
-            cudaFree(ttr);
         }
         if (dbg_on) {
-            HT_CUDA_TRY(cudaStreamSynchronize(st));
             std::vector<double> hd((size_t)n * 12);
             HT_CUDA_TRY(cudaMemcpy(hd.data(), dbg, hd.size() * sizeof(double), cudaMemcpyDeviceToHost));
             for (int64_t j = 0; j < n; ++j) {
@@ -1201,23 +1223,21 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
                 for (int it = 0; it < 12 && hd[j * 12 + it] != 0.0; ++it) fprintf(stderr, " %.3g", hd[j * 12 + it]);
                 fprintf(stderr, "\n");
             }
-            cudaFree(dbg);
         }
         if (opt && opt->ir_trace) {
-            HT_CUDA_TRY(cudaStreamSynchronize(st));
             std::vector<int> tr(n);
             HT_CUDA_TRY(cudaMemcpy(tr.data(), w->d_irtrace, n * sizeof(int), cudaMemcpyDeviceToHost));
             for (int64_t j = 0; j < n; ++j) opt->ir_trace[j] = tr[j];
         }
     }
-    // exact structural zeros of H and T (Alg. 2 "Set ... <- 0")
-    if (!(opt && opt->max_panels > 0)) {
-        TRY(R.zero_lower(n, n, dA, ldda, 1));
-        TRY(R.zero_lower(n, n, dB, lddb, 0));
-    }
-    HT_CUDA_TRY(cudaEventRecord(e1, st));
-    HT_CUDA_TRY(cudaStreamWaitEvent(user_st, e1, 0));
-    HT_CUDA_TRY(cudaEventSynchronize(e1));
+    // exact structural zeros of H and T (Alg. 2 "Set ... <- 0"), undo the
+    // range scaling, and check the result for non-finite entries -- one pass
+    TRY(ht_finish(st, n, dA, ldda, dB, lddb, R.wq ? dQ : nullptr, lddq, R.wz ? dZ : nullptr, lddz, 1.0 / sa, 1.0 / sb,
+                  (opt && opt->max_panels > 0) ? 1 : 0, w->d_iflags + 4));
+    R.tm.launches++;
+    HT_CUDA_TRY(cudaEventRecord(w->ev_t1, st));
+    HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags + 4, w->d_iflags + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HT_CUDA_TRY(cudaStreamSynchronize(st));
     R.tm.resolve();
     R.ph.mark(st, 7);
     HT_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1225,23 +1245,78 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     R.ph.print();
     R.rep.t_panel = R.tm.acc[0];
     R.rep.t_gemm = R.tm.acc[1];
-    R.rep.t_factor = R.tm.acc[2];
+    R.rep.t_factor = R.tm.acc[2] + R.tm.acc[7];
     R.rep.t_other = R.tm.acc[3];
     R.rep.t_chain = R.tm.acc[4];
+    R.rep.t_absorb_right = R.tm.acc[5];
+    R.rep.t_absorb_left = R.tm.acc[6];
+    R.rep.t_factor_exposed = R.tm.acc[7];
     R.rep.flops_chain = R.chain_flops;
     R.rep.chain_launches = R.chain_launches;
     R.rep.launches = R.tm.launches;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    HT_CUDA_TRY(cudaEventElapsedTime(&ms, w->ev_t0, w->ev_t1));
     HT_CUDA_TRY(cudaGetLastError());
     R.rep.seconds = ms * 1e-3;
     R.rep.flops_level3 = g_ht_flops;
     R.rep.flops = g_ht_flops + R.extra_flops;
-    R.rep.desingularizations = (n > 2) ? w->h_iflags[0] : 0;
-    if (rep) *rep = R.rep;
+    R.rep.desingularizations = ndesing;
+    if (w->h_iflags[4]) return HT_ENUMERIC;
     return HT_OK;
+}
+
+// After an error: wait for every library stream so that no queued kernel keeps writing the
+// caller's buffers or the workspace once we return (errors are ignored: a sticky CUDA error
+// makes every call fail).
+void drain(Work *w)
+{
+    cudaStream_t ss[] = {w->hp_stream, w->sA, w->sQZ, w->sB, w->side_stream};
+    for (cudaStream_t s : ss)
+        if (s) cudaStreamSynchronize(s);
+}
+
+int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
+                 int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep)
+{
+    int rc = validate(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt);
+    if (rc) return rc;
+    if (n == 0) {
+        if (rep) memset(rep, 0, sizeof(*rep));
+        return HT_OK;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
+    int dev = 0;
+    HT_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return HT_ECUDA;
+    std::lock_guard<std::mutex> lk(g_mu[dev]);
+    int64_t nb = (opt && opt->nb > 0) ? opt->nb : 128;
+    nb = std::max<int64_t>(1, std::min<int64_t>({nb, 256, std::max<int64_t>(1, n - 2)}));
+    Work *w = nullptr;
+    TRY(work_get(dev, n, nb, &w));
+    Run R;
+    memset(&R.rep, 0, sizeof(R.rep));
+    R.w = w;
+    // the caller's stream forks into the library's high-priority stream and joins it at the end
+    // (NULL is the legacy default stream, exactly as in the CUDA runtime: work the caller
+    //  queued there, e.g. the copies that produced A and B, is ordered before the reduction)
+    const cudaStream_t user_st = opt ? (cudaStream_t)opt->stream : (cudaStream_t)0;
+    R.st = w->hp_stream;
+    HT_CUDA_TRY(cudaEventRecord(w->ev[9], user_st));
+    HT_CUDA_TRY(cudaStreamWaitEvent(R.st, w->ev[9], 0));
+    R.n = n; R.nb = nb;
+    R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
+    R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
+    R.wq = wantq != 0; R.wz = wantz != 0;
+    R.qz0 = 0; R.qz1 = n;
+    if (opt && (opt->row_begin != 0 || opt->row_end != 0)) { R.qz0 = opt->row_begin; R.qz1 = opt->row_end; }
+    g_ht_flops = 0.0;
+    rc = reduce_body(R, opt);
+    if (rc != HT_OK) drain(w);
+    // join: the caller's stream is ordered after everything the call queued
+    if (cudaEventRecord(w->ev[10], R.st) == cudaSuccess) cudaStreamWaitEvent(user_st, w->ev[10], 0);
+    if (rep && (rc == HT_OK || rc == HT_ENUMERIC)) *rep = R.rep;
+    return rc;
 }
 
 int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb)

@@ -767,11 +767,13 @@ template <class L>
 int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch)
 {
     const int smem = L::DOUBLES * (int)sizeof(double);
-    static bool init = false;
-    if (!init) {
+    static std::mutex mu;
+    static unsigned long long done = 0;
+    const int rc = ht_once_per_device(mu, done, [smem] {
         HT_CUDA_TRY(cudaFuncSetAttribute(factor_qr_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        init = true;
-    }
+        return 0;
+    });
+    if (rc) return rc;
     factor_qr_kernel<L><<<1, L::NT, smem, st>>>(d_descs, nd, gscratch);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;

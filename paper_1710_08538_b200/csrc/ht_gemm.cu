@@ -7,7 +7,7 @@
 #include "ht_common.cuh"
 #include <stdio.h>
 
-double g_ht_flops = 0.0;
+thread_local double g_ht_flops = 0.0;  // per calling thread: concurrent calls on different devices
 
 namespace {
 

@@ -93,9 +93,14 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);
 int ht_panel_max_blocks(int *nblocks_out);
 
 // misc kernels (ht_util.cu)
-int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out);
+int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out,
+                   double *d_part);  // d_part: ht_fro_scratch_size() doubles
+int ht_fro_scratch_size();
 int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
-                   int *d_flags);
+                   int *d_flags, unsigned long long *d_maxbits);
+int ht_scale(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, double s);
+int ht_finish(cudaStream_t st, int64_t n, double *A, int64_t lda, double *B, int64_t ldb, const double *Q, int64_t ldq,
+              const double *Z, int64_t ldz, double sa, double sb, int partial, int *d_flag);
 int ht_desingularize(cudaStream_t st, int64_t n, double *B, int64_t ldb, int64_t r0, double thresh, double repl,
                      uint64_t seed, int64_t key, int *d_count);
 int ht_zero_lower(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, int64_t diag_offset);

@@ -5,36 +5,92 @@
 
 namespace {
 
-__global__ void fro_kernel(int64_t rows, int64_t cols, const double *M, int64_t ld, double *out)
+// ||M||_F^2 in a fixed order (bitwise reproducible run to run and rank to rank): block b
+// sums columns b, b + FRO_BLOCKS, ... (each thread a fixed row stride, then a fixed tree),
+// the partials are added by one block in index order (fro_final_kernel).
+constexpr int FRO_BLOCKS = 592;  // 4 x 148 SMs
+__global__ void fro_kernel(int64_t rows, int64_t cols, const double *M, int64_t ld, double *part)
 {
     __shared__ double red[32];
     double s = 0.0;
-    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
-            double v = M[j * ld + i];
-            s += v * v;
+    for (int64_t j = blockIdx.x; j < cols; j += gridDim.x)
+        for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+            const double v = M[j * ld + i];
+            s = fma(v, v, s);
         }
     s = block_sum(s, red);
-    if (threadIdx.x == 0) atomicAdd(out, s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void fro_final_kernel(const double *part, int np, double *out)
+{
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
 }
 
-// flags[0] |= non-finite in A or B; flags[1] |= nonzero strictly-lower entry of B
-__global__ void check_kernel(int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *flags)
+// flags[0] |= non-finite in A or B; flags[1] |= nonzero strictly-lower entry of B;
+// maxbits[0] = max |A|, maxbits[1] = max |B| (bit patterns of non-negative doubles order
+// like the values, so an integer atomicMax is exact and order-independent)
+__global__ void check_kernel(int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *flags,
+                             unsigned long long *maxbits)
 {
     int bad = 0, low = 0;
+    double ma = 0.0, mb = 0.0;
     for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
             double a = A[j * lda + i], b = B[j * ldb + i];
             if (!isfinite(a) || !isfinite(b)) bad = 1;
             if (i > j && b != 0.0) low = 1;
+            ma = fmax(ma, fabs(a));
+            mb = fmax(mb, fabs(b));
         }
     if (bad) atomicOr(&flags[0], 1);
     if (low) atomicOr(&flags[1], 1);
+    ma = warp_max(ma);
+    mb = warp_max(mb);
+    if ((threadIdx.x & 31) == 0) {
+        if (ma > 0.0) atomicMax(&maxbits[0], (unsigned long long)__double_as_longlong(ma));
+        if (mb > 0.0) atomicMax(&maxbits[1], (unsigned long long)__double_as_longlong(mb));
+    }
+}
+
+// M <- M * s (s a power of two: exact)
+__global__ void scale_kernel(int64_t rows, int64_t cols, double *M, int64_t ld, double s)
+{
+    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+            M[j * ld + i] *= s;
+}
+
+// End of a reduction: exact structural zeros of H (i > j+1) and T (i > j) (Alg. 2 "Set ... <- 0",
+// P:2378) unless `partial`, the inverse power-of-two scaling of H and T, and a scan
+// of H, T, Q, Z for non-finite entries (flag[0] |= 1).
+__global__ void finish_kernel(int64_t n, double *A, int64_t lda, double *B, int64_t ldb, const double *Q,
+                              int64_t ldq, const double *Z, int64_t ldz, double sa, double sb, int partial, int *flag)
+{
+    int bad = 0;
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            double a = A[j * lda + i], b = B[j * ldb + i];
+            if (!partial && i > j + 1) a = 0.0;
+            if (!partial && i > j) b = 0.0;
+            a *= sa;
+            b *= sb;
+            A[j * lda + i] = a;
+            B[j * ldb + i] = b;
+            bad |= !isfinite(a) || !isfinite(b);
+            if (Q) bad |= !isfinite(Q[j * ldq + i]);
+            if (Z) bad |= !isfinite(Z[j * ldz + i]);
+        }
+    if (bad) atomicOr(flag, 1);
 }
 
 // Counter-based normal draw (reading R-Z7): splitmix64 hash of (seed, key, row, ctr)
-// -> two uniforms -> Box-Muller.  Independent implementation of the same idea as the
-// oracle's (the two share no code).
+// -> two uniforms -> Box-Muller.  This generator is a shared SPEC (DESIGN.md R-Z7): the
+// oracle implements the same counter-based generator in its own file; the two share no
+// code.  The GPU keys draws by the panel start column, the oracle by the column.
 __device__ __forceinline__ uint64_t mix64(uint64_t z)
 {
     z += 0x9E3779B97F4A7C15ULL;
@@ -86,22 +142,47 @@ int ht_cuda_fail(cudaError_t e, const char *what, const char *file, int line)
     return 2;  // HT_ECUDA
 }
 
-int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out)
+int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out,
+                   double *d_part)
 {
     HT_CUDA_TRY(cudaMemsetAsync(d_out, 0, sizeof(double), st));
     if (rows <= 0 || cols <= 0) return 0;
-    dim3 grid(4, (unsigned)(cols < 2048 ? cols : 2048));
-    fro_kernel<<<grid, 256, 0, st>>>(rows, cols, M, ld, d_out);
+    fro_kernel<<<FRO_BLOCKS, 256, 0, st>>>(rows, cols, M, ld, d_part);
+    HT_CUDA_TRY(cudaGetLastError());
+    fro_final_kernel<<<1, 256, 0, st>>>(d_part, FRO_BLOCKS, d_out);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+int ht_fro_scratch_size() { return FRO_BLOCKS; }
+
+int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *d_flags,
+                   unsigned long long *d_maxbits)
+{
+    HT_CUDA_TRY(cudaMemsetAsync(d_flags, 0, 2 * sizeof(int), st));
+    HT_CUDA_TRY(cudaMemsetAsync(d_maxbits, 0, 2 * sizeof(unsigned long long), st));
+    if (n <= 0) return 0;
+    dim3 grid(4, (unsigned)(n < 2048 ? n : 2048));
+    check_kernel<<<grid, 256, 0, st>>>(n, A, lda, B, ldb, d_flags, d_maxbits);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
 
-int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb, int *d_flags)
+int ht_scale(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, double s)
 {
-    HT_CUDA_TRY(cudaMemsetAsync(d_flags, 0, 2 * sizeof(int), st));
+    if (rows <= 0 || cols <= 0 || s == 1.0) return 0;
+    dim3 grid((unsigned)((rows + 255) / 256 < 8 ? (rows + 255) / 256 : 8), (unsigned)(cols < 4096 ? cols : 4096));
+    scale_kernel<<<grid, 256, 0, st>>>(rows, cols, M, ld, s);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_finish(cudaStream_t st, int64_t n, double *A, int64_t lda, double *B, int64_t ldb, const double *Q, int64_t ldq,
+              const double *Z, int64_t ldz, double sa, double sb, int partial, int *d_flag)
+{
+    HT_CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
     if (n <= 0) return 0;
-    dim3 grid(4, (unsigned)(n < 2048 ? n : 2048));
-    check_kernel<<<grid, 256, 0, st>>>(n, A, lda, B, ldb, d_flags);
+    dim3 grid((unsigned)((n + 255) / 256 < 8 ? (n + 255) / 256 : 8), (unsigned)(n < 4096 ? n : 4096));
+    finish_kernel<<<grid, 256, 0, st>>>(n, A, lda, B, ldb, Q, ldq, Z, ldz, sa, sb, partial, d_flag);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -42,8 +42,31 @@ def test_argument_errors_before_any_write():
     assert lib.ht_reduce(4, A.ctypes.data, None, None, None, 0, 0, 0) == -3
     assert lib.ht_reduce(4, A.ctypes.data, A.ctypes.data, None, None, 1, 0, 0) == -4
     assert lib.ht_reduce(4, A.ctypes.data, A.ctypes.data, None, None, 0, 1, 0) == -5
+    assert lib.ht_reduce(4, A.ctypes.data, A.ctypes.data, A.ctypes.data, None, 2, 0, 0) == -6
+    assert lib.ht_reduce(4, A.ctypes.data, A.ctypes.data, None, A.ctypes.data, 0, 3, 0) == -7
     assert np.array_equal(A, keep)
     assert lib.ht_reduce(0, None, None, None, None, 1, 1, 0) == 0
+
+
+def test_ex_option_errors_before_any_write():
+    lib = ht.load_library()
+    A = np.asfortranarray(np.arange(16.0).reshape(4, 4))
+    keep = A.copy()
+    p = A.ctypes.data
+    rep = ht.HTReport()
+    opt = ht.make_options(nb=1 << 21)
+    assert lib.ht_reduce_ex(4, p, 4, p, 4, None, 4, None, 4, 0, 0, ctypes.byref(opt), ctypes.byref(rep)) == -8
+    opt = ht.make_options(row_range=(3, 1))
+    assert lib.ht_reduce_ex(4, p, 4, p, 4, None, 4, None, 4, 0, 0, ctypes.byref(opt), ctypes.byref(rep)) == -9
+    assert np.array_equal(A, keep)
+
+
+def test_report_layout_matches_header():
+    """ht_report / ht_options field order in the binding follows include/ht.h."""
+    txt = open(os.path.join(ROOT, "include", "ht.h")).read()
+    body = txt[txt.index("typedef struct {", txt.index("Statistics of one reduction")):txt.index("} ht_report;")]
+    names = re.findall(r"\b(?:double|int64_t)\s+(\w+)\s*;", body)
+    assert names == [f for f, _ in ht.HTReport._fields_]
 
 
 def test_no_cpu_fallback_without_gpu():

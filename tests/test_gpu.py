@@ -6,6 +6,10 @@ Tolerances are the north star's (BASELINE.json):
 Structure is checked bitwise (exact zeros).  Config-4 (singular B) parity is
 against Oracle-G (the HT form of a singular pencil is not unique).
 """
+import functools
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -17,8 +21,38 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_1710_08538_b200 as ht  # noqa: E402
+from paper_1710_08538_b200.model import model_flops  # noqa: E402
 
 PARITY = 1e-9
+# cfg 4 (singular B) vs Oracle-G: the HT form of a singular pencil is not unique (SURVEY
+# F7, reading R-F7): O(u) changes of the window transforms (tests/test_blocked_mirror.py)
+# or of the desingularisation draws (test_config4_form_depends_on_rho below) move it by
+# O(0.1).  Measured GPU distance to Oracle-G: 0.089-0.106 (gpurun_out/parity_cfg4_*.json,
+# profiles/r02_parity.md).  The hard gates are structure, backward error, orthogonality;
+# this bound only catches regressions.
+CFG4_G_GATE = 0.25
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def record(name, payload):
+    """Measured parity numbers go to gpurun_out/parity_<name>.json (copied under profiles/)."""
+    d = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, f"parity_{name}.json"), "w") as f:
+        json.dump(payload, f, indent=1)
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_T_cached(cfg, n):
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    return oracle.ht_T(A, B)[:2]
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_G_cached(cfg, n):
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    return oracle.ht_G(A, B)[:2]
 
 
 def to_dev(M):
@@ -100,7 +134,51 @@ def test_windows_taller_than_256_rows(cfg, n, nb):
     check_parity(A, B, H, T, Hr, Tr)
 
 
-@pytest.mark.parametrize("n,nb", [(120, 16), (300, 32), (700, 64)])
+@pytest.mark.parametrize("cfg,n,fails", [(3, 1300, ()), (3, 1300, (200, 201, 777)), (2, 600, ()),
+                                         (1, 700, (300,)), (5, 900, ())])
+def test_headline_nb128_vs_oracle_T(cfg, n, fails):
+    """The headline launch configuration nb = 128 (cfg 3): 256 x 128 staircase windows take
+    the FactorSmem<256,32,1> factorization, the cap-256 / h-64 chain rings, the pipelined
+    R1/R2 and R3/L2 windows (k >= 64) and the double-buffered <= 256-row band staging.
+    Forced IR failures add premature absorptions with 64 <= k < 128 and k < 64 (batched
+    path).  B is nonsingular, so the HT form is unique up to signs: gate at 1e-9."""
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    H, T, Q, Z, rep = gpu_reduce(A, B, nb=128, force_ir_fail=fails)
+    check_props(A, B, H, T, Q, Z)
+    Hr, Tr = oracle_T_cached(cfg, n)
+    dh, dt = check_parity(A, B, H, T, Hr, Tr)
+    assert rep["premature_absorptions"] == len(fails)
+    record(f"nb128_cfg{cfg}_n{n}_f{len(fails)}", {"cfg": cfg, "n": n, "nb": 128, "forced_fails": list(fails),
+                                                  "absH_vs_oracleT": dh, "absT_vs_oracleT": dt})
+
+
+def test_flop_accounting_within_15pct_of_model():
+    """SURVEY §8(c) pin: instrumented executed flops (per-launch formulas, the paper's
+    interposition convention P:2161-2162) within +-15% of the App. A model -- catches
+    missing or duplicated work.  Full size is checked in test_full_size_config_properties."""
+    for cfg, n, nb in ((3, 1300, 128), (2, 1000, 64), (5, 1100, 256)):
+        A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+        *_, rep = gpu_reduce(A, B, nb=nb)
+        ratio = rep["flops"] / model_flops(n, nb)
+        assert 0.85 <= ratio <= 1.15, (cfg, n, nb, ratio)
+
+
+@pytest.mark.parametrize("sa,sb", [(1e200, 1.0), (1.0, 1e-200), (1e-200, 1e200), (1e300, 1e300)])
+def test_extreme_scaling_is_invariant(sa, sb):
+    """Any finite pencil is accepted (include/ht.h "Range"): entries near 1e+-200 would
+    overflow or underflow squared norms; the library scales by exact powers of two and
+    undoes it on H, T.  The HT form of (sa A, sb B) is (sa H, sb T) with the same Q, Z."""
+    A, B = ht_inputs.pencil("qruniform", 300, 8)
+    H, T, Q, Z, _ = gpu_reduce(A, B, nb=32)
+    As, Bs = A * sa, B * sb
+    Hs, Ts, Qs, Zs, rep = gpu_reduce(As, Bs, nb=32)
+    assert np.all(np.isfinite(Hs)) and np.all(np.isfinite(Ts))
+    check_props(A, B, Hs / sa, Ts / sb, Qs, Zs)  # (numpy's own products would overflow at 1e300)
+    assert C.abs_diff(Hs / sa, H, C.fro(A)) <= PARITY and C.abs_diff(Ts / sb, T, C.fro(B)) <= PARITY
+    assert (rep["scale_a"] != 1.0) == (sa != 1.0) and (rep["scale_b"] != 1.0) == (sb != 1.0)
+
+
+@pytest.mark.parametrize("n,nb", [(120, 16), (300, 32), (700, 64), (700, 128)])
 def test_config4_singular(n, nb):
     """Config 4 (singular, graded B): the HT form of a singular pencil is not unique
     (tests/test_blocked_mirror.py::test_singular_ht_form_is_not_unique shows O(u)
@@ -110,11 +188,30 @@ def test_config4_singular(n, nb):
     H, T, Q, Z, rep = gpu_reduce(A, B, nb=nb)
     check_props(A, B, H, T, Q, Z)
     assert rep["desingularizations"] > 0
-    Hg, Tg, _, _ = oracle.ht_G(A, B)
+    Hg, Tg = oracle_G_cached(4, n)
     dh = C.abs_diff(H, Hg, C.fro(A))
     dt = C.abs_diff(T, Tg, C.fro(B))
-    print(f"cfg4 n={n}: |H| diff vs Oracle-G {dh:.2e}, |T| {dt:.2e} (reported, not gated); "
-          f"IR failures {rep['ir_failed_columns']}, rescales {rep['solve_rescales']}")
+    record(f"cfg4_n{n}_nb{nb}", {"cfg": 4, "n": n, "nb": nb, "absH_vs_oracleG": dh, "absT_vs_oracleG": dt,
+                                 "ir_failed_columns": rep["ir_failed_columns"],
+                                 "premature_absorptions": rep["premature_absorptions"],
+                                 "desingularizations": rep["desingularizations"],
+                                 "solve_rescales": rep["solve_rescales"]})
+    assert dh <= CFG4_G_GATE and dt <= CFG4_G_GATE, (dh, dt)
+
+
+def test_config4_form_depends_on_rho():
+    """Evidence for reading R-F7 on the product path itself: two seeds of the
+    desingularisation draws rho (perturbations of B of size 2u||B||_F) give two
+    backward-stable HT forms of the same singular pencil that differ by >> 1e-9."""
+    A, B, _ = ht_inputs.config_pencil(4, n=300)
+    H0, T0, Q0, Z0, _ = gpu_reduce(A, B, nb=32, seed=0)
+    H1, T1, Q1, Z1, _ = gpu_reduce(A, B, nb=32, seed=1)
+    check_props(A, B, H0, T0, Q0, Z0)
+    check_props(A, B, H1, T1, Q1, Z1)
+    d = C.abs_diff(H0, H1, C.fro(A))
+    record("cfg4_rho_seed", {"n": 300, "nb": 32, "absH_seed0_vs_seed1": d,
+                             "absT_seed0_vs_seed1": C.abs_diff(T0, T1, C.fro(B))})
+    assert d > 1e-9, d
 
 
 def test_staircase_step_wider_than_pending_reflectors():
@@ -267,13 +364,41 @@ def _device_backward_errors(A, B, dA, dB, dQ, dZ):
     return ra, rb, oq, oz, struct
 
 
+def _golden_gate(A, B, dA, dB, cfg):
+    """Entry-wise |H|, |T| against the full-size oracle samples written by
+    scripts/make_fullsize_golden.py (Oracle-T for cfg 3/5, Oracle-G for cfg 4), keyed by the
+    SHA-256 of the inputs.  Returns (max |d| / ||.||_F, sampled-Frobenius estimate / ||.||_F)
+    for H and T, or None if no sample file exists for this config."""
+    import hashlib
+    path = [os.path.join(GOLD, f"fullsize_cfg{cfg}_{w}.npz") for w in ("T", "G")]
+    path = [p for p in path if os.path.exists(p)]
+    if not path:
+        return None
+    g = np.load(path[0])
+    sha = lambda M: hashlib.sha256(np.asfortranarray(M).tobytes(order="F")).hexdigest()
+    assert str(g["sha_A"]) == sha(A) and str(g["sha_B"]) == sha(B), "golden samples are for other inputs"
+    n = A.shape[0]
+    out = {}
+    for name, t, rows, cols, ref, nrm, region in (
+            ("H", dA, g["h_rows"], g["h_cols"], g["h_abs"], float(g["fro_A"]), n * (n + 1) / 2 + n - 1),
+            ("T", dB, g["t_rows"], g["t_cols"], g["t_abs"], float(g["fro_B"]), n * (n + 1) / 2)):
+        # tensors hold M^T: M[i, j] = t[j, i]
+        got = t[torch.from_numpy(cols).cuda(), torch.from_numpy(rows).cuda()].abs().cpu().numpy()
+        d = got - ref
+        out[name] = (float(np.max(np.abs(d))) / nrm, float(np.sqrt(region / d.size) * np.linalg.norm(d)) / nrm)
+    out["oracle"] = str(g["oracle"])
+    return out
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [3, 4, 5])
 def test_full_size_config_properties(cfg):
     """BASELINE.json configs at full size, in the launch configuration bench.py times:
     exact structure, backward errors and orthogonality (north-star tolerances) computed on
-    the device; for the nonsingular configs the first rows of |H| are compared with a
-    column-sampled oracle-independent invariant (det identity is not feasible at this n)."""
+    the device; executed flops within +-15% of the App. A model; and |H|, |T| entry by entry
+    against the full-size oracle samples of tests/golden/ (Oracle-T for cfg 3, Oracle-G for
+    cfg 4) at the north-star 1e-9 -- both as the max entry-wise difference and as the
+    sampled estimate of || |H| - |H_oracle| ||_F, relative to ||A||_F (||B||_F for T)."""
     A, B, nb = ht_inputs.config_pencil(cfg)
     n = A.shape[0]
     dA, dB = to_dev(A), to_dev(B)
@@ -288,6 +413,18 @@ def test_full_size_config_properties(cfg):
     assert ra <= tol and rb <= tol and oq <= tol and oz <= tol, (ra, rb, oq, oz, tol)
     if cfg != 4:
         assert rep["ir_failed_columns"] == 0
+    ratio = rep["flops"] / model_flops(n, nb)
+    assert 0.85 <= ratio <= 1.15, ratio
+    gate = _golden_gate(A, B, dA, dB, cfg)
+    if gate is not None:
+        record(f"fullsize_cfg{cfg}", {"cfg": cfg, "n": n, "nb": nb, "oracle": gate["oracle"],
+                                      "absH_max_rel": gate["H"][0], "absH_fro_est_rel": gate["H"][1],
+                                      "absT_max_rel": gate["T"][0], "absT_fro_est_rel": gate["T"][1],
+                                      "flops_exec_over_model": ratio})
+        lim = PARITY if cfg != 4 else CFG4_G_GATE
+        assert max(gate["H"] + gate["T"]) <= lim, gate
+    elif cfg == 3:
+        pytest.fail("tests/golden/fullsize_cfg3_T.npz missing (scripts/make_fullsize_golden.py --config 3)")
     # Q e1 = Z e1 = e1 (every transform acts on rows/columns >= 2)
     e1 = torch.zeros(n, dtype=torch.float64, device="cuda")
     e1[0] = 1.0
