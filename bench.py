@@ -190,7 +190,8 @@ def env_knobs():
     return {k: os.environ[k] for k in ENV_KNOBS if k in os.environ}
 
 
-def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank, dist, want_e2e=False, A_h=None, B_h=None):
+def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank, dist, want_e2e=False, A_h=None, B_h=None,
+                   comm=None):
     """Time `steps` full reductions of config `cfg` after `warmup` untimed ones (device
     events on the caller's stream, max over ranks).  Returns a dict of measurements."""
     if A_h is None:
@@ -203,10 +204,17 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
     def step():
         A.copy_(A0)  # pristine inputs each step (inputs larger than L2 at n >= 2048)
         B.copy_(B0)
-        return mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+        return mg.reduce_mg(A, B, Q, Z, nb=nb, comm=comm, rank=rank, world=world, stream=stream.cuda_stream)
 
-    for _ in range(warmup):
-        step()
+    f_single = None
+    for i in range(warmup):
+        if world > 1 and i == 0:
+            # executed flops of the whole problem (F_exec of P = 1: replicated work is not credited twice)
+            A.copy_(A0)
+            B.copy_(B0)
+            f_single = ht.reduce_device(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)["flops"]
+        else:
+            step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -225,7 +233,7 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
         t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    out = {"elapsed": elapsed, "t_step": elapsed / steps, "reps": reps}
+    out = {"elapsed": elapsed, "t_step": elapsed / steps, "reps": reps, "f_single": f_single}
     if want_e2e:
         # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host
         ts = []
@@ -240,7 +248,7 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
                 hB = torch.from_numpy(np.ascontiguousarray(B_h.T)).pin_memory()
                 A.copy_(hA, non_blocking=True)
                 B.copy_(hB, non_blocking=True)
-                mg.reduce_mg(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)
+                mg.reduce_mg(A, B, Q, Z, nb=nb, comm=comm, rank=rank, world=world, stream=stream.cuda_stream)
                 [M.cpu() for M in (A, B, Q, Z)]
                 torch.cuda.synchronize()
             te_ = time.time() - t0
@@ -298,17 +306,18 @@ def main():
     from paper_1710_08538_b200 import mg
 
     stream = torch.cuda.current_stream()
+    comm = mg.init_comm()[0] if world > 1 else None
     A_h, B_h, _ = ht_inputs.config_pencil(cfg, n=n)
     clocks = ClockSampler(local)
     clocks.start()
     m = measure_config(torch, ht, mg, cfg, n, nb, args.steps, args.warmup, stream, world, rank, dist,
-                       want_e2e=not args.no_e2e, A_h=A_h, B_h=B_h)
+                       want_e2e=not args.no_e2e, A_h=A_h, B_h=B_h, comm=comm)
     clk = clocks.stop()
     elapsed, t_step, reps = m["elapsed"], m["t_step"], m["reps"]
     agg = summarize(reps, args.steps)
     rep0 = reps[-1]
     Fm = model_flops(n, nb)
-    Fx = agg["flops"]
+    Fx = m["f_single"] if m["f_single"] else agg["flops"]
     value = Fx / t_step / 1e9  # executed flops of one pencil per second, whatever the number of GPUs
 
     # roofline of the dominant kernel class
@@ -361,9 +370,11 @@ def main():
             if c == cfg or c not in ht_inputs.CONFIGS:
                 continue
             nc, nbc = ht_inputs.CONFIGS[c]["n"], ht_inputs.CONFIGS[c]["nb"]
-            st_, wu_ = (10, 3) if nc <= 2048 else (2, 1)
-            mc = measure_config(torch, ht, mg, c, nc, nbc, st_, wu_, stream, world, rank, dist)
+            st_, wu_ = (10, 3) if nc <= 2048 else (2, 1 if world == 1 else 2)
+            mc = measure_config(torch, ht, mg, c, nc, nbc, st_, wu_, stream, world, rank, dist, comm=comm)
             ac = summarize(mc["reps"], st_)
+            if mc["f_single"]:
+                ac["flops"] = mc["f_single"]
             rc0 = mc["reps"][-1]
             others[f"cfg{c}"] = {"workload": WORKLOAD[c], "n": nc, "nb": nbc, "steps": st_, "warmup": wu_,
                                  "ms_per_step": mc["t_step"] * 1e3, "gflops_exec": ac["flops"] / mc["t_step"] / 1e9,
@@ -392,7 +403,8 @@ def main():
                 "config": {"workload": WORKLOAD.get(cfg, f"cfg{cfg}") + (f" (n={n})" if n != ht_inputs.CONFIGS[cfg]["n"] else ""),
                            "n": n, "nb": nb, "seed": ht_inputs.CONFIGS[cfg]["seed"],
                            "l2": "inputs larger than L2 (A,B,Q,Z = 4 x %.0f MB)" % (n * n * 8 / 1e6),
-                           "parallelism": (f"mg{world}" if world > 1 else "single"),
+                           "parallelism": (f"mg{world}: A row/column slabs + Q,Z row slabs, B/panel/factors replicated"
+                                           if world > 1 else "single"),
                            "value_flops": "executed (instrumented per launch)", "env_knobs": env_knobs()},
                 "roofline": roof, "roofline_panel": roof_panel, "roofline_e2e": roof_e2e, "wy_apply_phase": wy,
                 "cpu_baseline": cpu, "e2e": e2e,
@@ -411,6 +423,7 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
+        ht.ht_nccl_comm_destroy(comm)
         dist.destroy_process_group()
     return 0
 

@@ -159,6 +159,48 @@ HT_API int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int 
 HT_API int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq,
                  double *dZ, int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep);
 
+/*
+ * Multi-GPU entry point: one process per GPU of one node,
+ * called collectively by every rank with its own device buffers.
+ *   Layout: A, B are n x n on every rank with identical contents (replicated); on return
+ *   every rank holds H and T.  The work is sharded: A's right-hand applies (R2, R3, the
+ *   Remark-2 rows; sec. 3.3.1) run on row slabs, its left-hand applies (L2, L3;
+ *   sec. 3.3.2) on column slabs, with one packed ncclAllGather after each phase (the
+ *   layout switch); Q and Z only receive right multiplications (P:886, P:945, P:1157,
+ *   P:1198), so each rank computes the row slab ht_mg_slab(0, n, nranks, rank) of them,
+ *   all-gathered at the end when gather_qz != 0 (else the other rows are unspecified).
+ *   The panel, B and the staircase factorizations are computed redundantly on every rank
+ *   (bitwise identical: deterministic kernels, fixed-order reductions).
+ *   nccl_comm: an ncclComm_t of nranks ranks whose rank `rank` is this process (see
+ *   ht_nccl_comm_init), ordered on opt->stream.  nccl_comm == NULL is the LOOPBACK mode: the
+ *   call plays all nranks ranks on the current device (slab launches + the pack/unpack of
+ *   every all-gather without the network) -- a single-GPU test of the sharded path.
+ *   opt->row_begin/row_end must be 0 (HT_EARG_OPT).  Errors as ht_reduce_ex, plus
+ *   HT_ENCCL for NCCL failures and HT_EARG_OPT for a communicator that does not match
+ *   (rank, nranks).
+ */
+typedef struct {
+    double *A; int64_t lda;
+    double *B; int64_t ldb;
+    double *Q; int64_t ldq;
+    double *Z; int64_t ldz;
+    int gather_qz;
+} ht_mg_layout;
+HT_API int ht_reduce_mg(int64_t n, const ht_mg_layout *layout, void *nccl_comm, int rank, int nranks, int wantq,
+                        int wantz, const ht_options *opt, ht_report *rep);
+
+/* NCCL bootstrap for ht_reduce_mg (NCCL is loaded at run time from the process's
+ * libnccl.so.2): rank 0 calls ht_nccl_unique_id (128 opaque bytes), sends them to every
+ * rank (e.g. torch.distributed), and every rank calls ht_nccl_comm_init.  HT_ENCCL if
+ * NCCL is unavailable or fails. */
+HT_API int ht_nccl_unique_id(void *id128);
+HT_API int ht_nccl_comm_init(void **comm, int nranks, const void *id128, int rank);
+HT_API int ht_nccl_comm_destroy(void *comm);
+
+/* The contiguous balanced partition used by ht_reduce_mg: part `part` of [begin, end) over
+ * `parts` parts is [*lo, *hi) (sizes differ by at most 1, lower parts larger).  Host-only. */
+HT_API int ht_mg_slab(int64_t begin, int64_t end, int parts, int part, int64_t *lo, int64_t *hi);
+
 /* Human-readable text for a return code (static storage). */
 HT_API const char *ht_strerror(int code);
 

@@ -26,7 +26,9 @@ HT_OK = 0
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
           -6: "HT_EARG_WANTQ", -7: "HT_EARG_WANTZ", -8: "HT_EARG_NB", -9: "HT_EARG_OPT",
           1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC", 5: "HT_ENCCL"}
-EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_strerror", "ht_version", "ht_release_workspace", "ht_bench_chain_apply")
+EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_reduce_mg", "ht_nccl_unique_id", "ht_nccl_comm_init",
+           "ht_nccl_comm_destroy", "ht_mg_slab", "ht_strerror", "ht_version", "ht_release_workspace",
+           "ht_bench_chain_apply")
 
 
 class HTOptions(ctypes.Structure):
@@ -51,6 +53,12 @@ class HTReport(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class HTMgLayout(ctypes.Structure):
+    _fields_ = [("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+                ("Q", ctypes.c_void_p), ("ldq", ctypes.c_int64), ("Z", ctypes.c_void_p), ("ldz", ctypes.c_int64),
+                ("gather_qz", ctypes.c_int)]
 
 
 class HTError(RuntimeError):
@@ -81,6 +89,17 @@ def load_library():
         lib.ht_version.argtypes = []
         lib.ht_release_workspace.restype = ctypes.c_int
         lib.ht_release_workspace.argtypes = []
+        lib.ht_reduce_mg.restype = ctypes.c_int
+        lib.ht_reduce_mg.argtypes = [i64, ctypes.POINTER(HTMgLayout), P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.POINTER(HTOptions), ctypes.POINTER(HTReport)]
+        lib.ht_nccl_unique_id.restype = ctypes.c_int
+        lib.ht_nccl_unique_id.argtypes = [P]
+        lib.ht_nccl_comm_init.restype = ctypes.c_int
+        lib.ht_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, P, ctypes.c_int]
+        lib.ht_nccl_comm_destroy.restype = ctypes.c_int
+        lib.ht_nccl_comm_destroy.argtypes = [P]
+        lib.ht_mg_slab.restype = ctypes.c_int
+        lib.ht_mg_slab.argtypes = [i64, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         lib.ht_bench_chain_apply.restype = ctypes.c_int
         lib.ht_bench_chain_apply.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -157,6 +176,51 @@ def ht_reduce_ex(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq=True, wantz=Tr
     _check(lib.ht_reduce_ex(int(n), dA, int(ldda), dB, int(lddb), dQ, int(lddq), dZ, int(lddz),
                             int(wantq), int(wantz), ctypes.byref(opt), ctypes.byref(rep)))
     return rep.as_dict()
+
+
+def ht_reduce_mg(n, layout, nccl_comm, rank, nranks, wantq=True, wantz=True, options=None):
+    """Multi-GPU entry point (collective; nccl_comm None = loopback). Returns the report dict."""
+    lib = load_library()
+    rep = HTReport()
+    opt = options if options is not None else make_options()
+    _check(lib.ht_reduce_mg(int(n), ctypes.byref(layout), nccl_comm, int(rank), int(nranks), int(wantq), int(wantz),
+                            ctypes.byref(opt), ctypes.byref(rep)))
+    return rep.as_dict()
+
+
+def _nccl_first():
+    """The library dlopens the libnccl.so.2 the process already mapped: import torch first so
+    that it is torch's bundled NCCL (the one torch.distributed uses)."""
+    try:
+        import torch  # noqa: F401
+        import torch.distributed  # noqa: F401
+    except ImportError:
+        pass
+
+
+def ht_nccl_unique_id() -> bytes:
+    _nccl_first()
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().ht_nccl_unique_id(buf))
+    return buf.raw
+
+
+def ht_nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    _nccl_first()
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(load_library().ht_nccl_comm_init(ctypes.byref(comm), int(nranks), buf, int(rank)))
+    return comm.value
+
+
+def ht_nccl_comm_destroy(comm) -> None:
+    _check(load_library().ht_nccl_comm_destroy(comm))
+
+
+def ht_mg_slab(begin: int, end: int, parts: int, part: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(load_library().ht_mg_slab(int(begin), int(end), int(parts), int(part), ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
 
 
 def reduce_device(A, B, Q=None, Z=None, nb=0, stream=None, **kw):

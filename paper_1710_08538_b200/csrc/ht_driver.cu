@@ -71,6 +71,8 @@ struct Work {
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
     int *dsafe = nullptr;
     double *fro_part = nullptr;  // fixed-order partial sums of ||B||_F^2
+    double *mgbuf = nullptr;     // packed all-gather staging (ht_reduce_mg)
+    size_t mgcap = 0;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // timing events of one call
     FactorDesc *d_fd = nullptr, *h_fd = nullptr;
     void *d_bd = nullptr, *h_bd = nullptr;  // band/Qhat-formation descriptors (one per factor descriptor)
@@ -177,6 +179,9 @@ void work_free(Work &w)
     w.d_irtrace = nullptr;
     if (w.fro_part) cudaFree(w.fro_part);
     w.fro_part = nullptr;
+    if (w.mgbuf) cudaFree(w.mgbuf);
+    w.mgbuf = nullptr;
+    w.mgcap = 0;
     if (w.Dinv) cudaFree(w.Dinv);
     if (w.Bt) cudaFree(w.Bt);
     w.Bt = nullptr;
@@ -356,6 +361,22 @@ struct Run {
     int64_t lda, ldb, ldq, ldz;
     bool wq, wz;
     int64_t qz0 = 0, qz1 = 0;  // rows of Q and Z this call computes (multi-GPU row slabs)
+    // Multi-GPU (ht_reduce_mg): P ranks, this is rank `me`; `comm` is the NCCL
+    // communicator, or NULL = loopback (this call plays all P ranks on one device).  A's
+    // right-hand applies (R2, R3, Remark 2) run on row slabs, its left-hand applies (L2, L3)
+    // on column slabs of [J, n); one packed all-gather after each phase switches layouts.
+    int P = 1, me = 0;
+    void *comm = nullptr;
+    int part_begin() const { return comm ? me : 0; }
+    int part_end() const { return comm ? me + 1 : P; }
+    int gather(cudaStream_t s, double *X, int64_t ldx, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int by_cols)
+    {
+        if (P <= 1) return 0;
+        tm.begin(s, 3);
+        const int rc = ht_mg_allgather(s, comm, P, me, X, ldx, r0, r1, c0, c1, by_cols, w->mgbuf, w->mgcap);
+        tm.end(s);
+        return rc;
+    }
     ht_report rep;
     double extra_flops = 0.0;
     double chain_flops = 0.0;
@@ -562,11 +583,20 @@ struct Run {
         w->fd_cur = w->ld_cur = w->cw_cur = 0;
         TRY(dep(sA, st, 0));
         TRY(dep(sQ, st, 0));
-        // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns (A: sA)
-        TRY(gemm_on(sA, 'N', 'N', p0, k, n - p0, 1.0, A + p0 * lda, lda, V + p0, n, 0.0, w->W1A, n));
-        TRY(gemm_on(sA, 'N', 'N', p0, k, k, 1.0, w->W1A, n, T, nb, 0.0, Y, n));
-        if (J > p0) TRY(gemm_on(sA, 'N', 'T', p0, J - p0, k, -1.0, Y, n, V + p0, n, 1.0, A + p0 * lda, lda));
-        if (m <= 2 * k) {
+        // Remark 2: rows 0:p0 of Y, then the deferred update of the panel columns (A: sA);
+        // row-separable, so each rank takes the rows of its A slab (all rows before the tail rule)
+        const bool tail = m <= 2 * k;
+        for (int q = tail ? 0 : part_begin(); q < (tail ? 1 : part_end()); ++q) {
+            int64_t a0 = 0, a1 = n;
+            if (!tail) ht_slab(0, n, P, q, &a0, &a1);
+            a1 = std::min(a1, p0);
+            if (a1 <= a0) continue;
+            const int64_t h = a1 - a0;
+            TRY(gemm_on(sA, 'N', 'N', h, k, n - p0, 1.0, A + a0 + p0 * lda, lda, V + p0, n, 0.0, w->W1A + a0, n));
+            TRY(gemm_on(sA, 'N', 'N', h, k, k, 1.0, w->W1A + a0, n, T, nb, 0.0, Y + a0, n));
+            if (J > p0) TRY(gemm_on(sA, 'N', 'T', h, J - p0, k, -1.0, Y + a0, n, V + p0, n, 1.0, A + a0 + p0 * lda, lda));
+        }
+        if (tail) {
             TRY(dep(st, sA, 1));
             TRY(dep(st, sQ, 2));
             return absorb_tail(s0, k);
@@ -667,12 +697,21 @@ struct Run {
         {
             std::vector<ChainWin> wa = wl;
             for (auto &x : wa) x.hi[0] = n;  // A: all rows
-            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, wa, side_grid()));
+            for (int q = part_begin(); q < part_end(); ++q) {
+                int64_t a0, a1;
+                ht_slab(0, n, P, q, &a0, &a1);
+                TRY(chain_on(sA, {ChainMat{A, lda, 0, a0, a1}}, wa, side_grid()));
+            }
             if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, side_grid()));
         }
         TRY(wupdate(wx[1]));
-        TRY(gemm_on(sA, 'N', 'T', n, 1, k, -1.0, Y, n, V + J, n, 1.0, A + J * lda, lda));
-        TRY(gemm_on(sA, 'N', 'T', n, k, k, -1.0, Y, n, L1, ldw, 1.0, A + (n - k) * lda, lda));
+        for (int q = part_begin(); q < part_end(); ++q) {
+            int64_t a0, a1;
+            ht_slab(0, n, P, q, &a0, &a1);
+            if (a1 <= a0) continue;
+            TRY(gemm_on(sA, 'N', 'T', a1 - a0, 1, k, -1.0, Y + a0, n, V + J, n, 1.0, A + a0 + J * lda, lda));
+            TRY(gemm_on(sA, 'N', 'T', a1 - a0, k, k, -1.0, Y + a0, n, L1, ldw, 1.0, A + a0 + (n - k) * lda, lda));
+        }
         ph.mark(st, 2);
         // ===== R3: RQ staircase restoring B, bottom -> top (sec. 3.3.1 second "e)") =====
         // Window t is factored on st; the next window (t-1) reads only the band of rows
@@ -686,7 +725,11 @@ struct Run {
             if (ws.empty()) return 0;
             TRY(dep(sA, sBq, 4));
             TRY(dep(sQ, sBq, 4));
-            TRY(chain_on(sA, {ChainMat{A, lda, 0, 0, n}}, ws, side_grid()));
+            for (int q = part_begin(); q < part_end(); ++q) {
+                int64_t a0, a1;
+                ht_slab(0, n, P, q, &a0, &a1);
+                TRY(chain_on(sA, {ChainMat{A, lda, 0, a0, a1}}, ws, side_grid()));
+            }
             if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, side_grid()));
             ws.clear();
             return 0;
@@ -779,20 +822,31 @@ struct Run {
         TRY(copy2d(k, k, w->UW, ldw, w->UR + k, ldur));
         TRY(zero_lower(k, k, w->UR + k, ldur, 0));
 
+        // layout switch of A: row slabs -> full rows [0, n) x columns [p0, n) on every rank
+        TRY(gather(sA, A, lda, 0, n, p0, n, 0));
         TRY(dep(sA, st, 5));  // L1 windows and UR are ready
         TRY(dep(sQ, st, 5));
         {
             std::vector<ChainWin> wla = wlu;
-            for (auto &x : wla) x.lo[0] = J;  // A: columns J..n
-            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, wla, side_grid()));
+            for (auto &x : wla) x.lo[0] = J;  // A: columns J..n (column slabs per rank)
+            for (int q = part_begin(); q < part_end(); ++q) {
+                int64_t c0, c1;
+                ht_slab(J, n, P, q, &c0, &c1);
+                TRY(chain_on(sA, {ChainMat{A, lda, 1, c0, c1}}, wla, side_grid()));
+            }
             std::vector<ChainWin> wlq = wlu;
             for (auto &x : wlq) x.lo[0] = 0;
             if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, side_grid()));
         }
         {
             // B(p0:p0+2k, J+1:n) (st) and A(p0:p0+2k, J:n) (sA):  X <- X - UR S^T (X^T UR)^T
-            struct LX { double *X; int64_t ld, c0, c1; cudaStream_t s; double *W1, *W2; } lx[2] = {
-                {B, ldb, J + 1, n, st, w->W1, w->W2}, {A, lda, J, n, sA, w->W1A, w->W2A}};
+            struct LX { double *X; int64_t ld, c0, c1; cudaStream_t s; double *W1, *W2; };
+            std::vector<LX> lx{{B, ldb, J + 1, n, st, w->W1, w->W2}};
+            for (int q = part_begin(); q < part_end(); ++q) {
+                int64_t c0, c1;
+                ht_slab(J, n, P, q, &c0, &c1);
+                lx.push_back({A, lda, c0, c1, sA, w->W1A, w->W2A});
+            }
             for (auto &e : lx) {
                 const int64_t nc = e.c1 - e.c0;
                 if (nc <= 0) continue;
@@ -819,7 +873,11 @@ struct Run {
             if (ws.empty()) return 0;
             TRY(dep(sA, sBq, 6));
             TRY(dep(sQ, sBq, 6));
-            TRY(chain_on(sA, {ChainMat{A, lda, 1, J, n}}, ws, grid));
+            for (int q = part_begin(); q < part_end(); ++q) {
+                int64_t c0, c1;
+                ht_slab(J, n, P, q, &c0, &c1);
+                TRY(chain_on(sA, {ChainMat{A, lda, 1, c0, c1}}, ws, grid));
+            }
             if (wq) {
                 std::vector<ChainWin> wq_ = ws;
                 for (auto &x : wq_) x.lo[0] = 0;
@@ -861,6 +919,8 @@ struct Run {
             if ((int)wb.size() == BATCH) TRY(flush_left(wb, side_grid()));
         }
         TRY(flush_left(wb, 0));  // the last batch: the critical stream is done, full grid
+        // layout switch back: column slabs -> the full trailing block on every rank
+        TRY(gather(sA, A, lda, p0, n, J, n, 1));
         TRY(dep(st, sBq, 10));
         ph.mark(st, 6);
         // join: the next panel reads A and B; U, V, S, T, Y, the window stores are reused
@@ -1028,6 +1088,10 @@ int ht_release_workspace(void)
     work_free(g_work[dev]);
     return HT_OK;
 }
+
+}  // extern "C"
+
+namespace {
 
 // Everything of one reduction after the caller's stream has forked into R.st.  Any error
 // return leaves work queued on the library streams; ht_reduce_ex drains them.
@@ -1275,15 +1339,12 @@ void drain(Work *w)
         if (s) cudaStreamSynchronize(s);
 }
 
-int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
-                 int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep)
+// One reduction on the current device: the single-GPU entry point (P = 1) and one rank of
+// the multi-GPU one (P > 1: rank `me` with NCCL `comm`, or every rank when comm is NULL).
+int reduce_impl(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
+                int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep, int P, int me, void *comm,
+                int gather_qz)
 {
-    int rc = validate(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt);
-    if (rc) return rc;
-    if (n == 0) {
-        if (rep) memset(rep, 0, sizeof(*rep));
-        return HT_OK;
-    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
     int dev = 0;
@@ -1294,6 +1355,16 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     nb = std::max<int64_t>(1, std::min<int64_t>({nb, 256, std::max<int64_t>(1, n - 2)}));
     Work *w = nullptr;
     TRY(work_get(dev, n, nb, &w));
+    if (P > 1) {  // packed all-gather staging: P + 1 chunks of at most ceil(n / P) x n doubles
+        const size_t need = (size_t)(P + 1) * (size_t)((n + P - 1) / P) * (size_t)n;
+        if (w->mgcap < need) {
+            if (w->mgbuf) cudaFree(w->mgbuf);
+            w->mgbuf = nullptr;
+            w->mgcap = 0;
+            if (cudaMalloc((void **)&w->mgbuf, need * sizeof(double)) != cudaSuccess) return HT_ENOMEM;
+            w->mgcap = need;
+        }
+    }
     Run R;
     memset(&R.rep, 0, sizeof(R.rep));
     R.w = w;
@@ -1308,15 +1379,58 @@ int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, 
     R.A = dA; R.B = dB; R.Q = dQ; R.Z = dZ;
     R.lda = ldda; R.ldb = lddb; R.ldq = lddq; R.ldz = lddz;
     R.wq = wantq != 0; R.wz = wantz != 0;
+    R.P = P; R.me = me; R.comm = comm;
     R.qz0 = 0; R.qz1 = n;
     if (opt && (opt->row_begin != 0 || opt->row_end != 0)) { R.qz0 = opt->row_begin; R.qz1 = opt->row_end; }
+    if (P > 1 && comm) ht_slab(0, n, P, me, &R.qz0, &R.qz1);  // Q, Z: this rank's row slab
     g_ht_flops = 0.0;
-    rc = reduce_body(R, opt);
+    int rc = reduce_body(R, opt);
+    if (rc == HT_OK && P > 1 && gather_qz) {  // C6: every rank gets the full Q, Z (not in rep.seconds)
+        if (R.wq) rc = R.gather(R.st, dQ, lddq, 0, n, 0, n, 0);
+        if (rc == HT_OK && R.wz) rc = R.gather(R.st, dZ, lddz, 0, n, 0, n, 0);
+        if (rc == HT_OK && cudaStreamSynchronize(R.st) != cudaSuccess) rc = HT_ECUDA;
+    }
     if (rc != HT_OK) drain(w);
     // join: the caller's stream is ordered after everything the call queued
     if (cudaEventRecord(w->ev[10], R.st) == cudaSuccess) cudaStreamWaitEvent(user_st, w->ev[10], 0);
     if (rep && (rc == HT_OK || rc == HT_ENUMERIC)) *rep = R.rep;
     return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ht_reduce_ex(int64_t n, double *dA, int64_t ldda, double *dB, int64_t lddb, double *dQ, int64_t lddq, double *dZ,
+                 int64_t lddz, int wantq, int wantz, const ht_options *opt, ht_report *rep)
+{
+    int rc = validate(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt);
+    if (rc) return rc;
+    if (n == 0) {
+        if (rep) memset(rep, 0, sizeof(*rep));
+        return HT_OK;
+    }
+    return reduce_impl(n, dA, ldda, dB, lddb, dQ, lddq, dZ, lddz, wantq, wantz, opt, rep, 1, 0, nullptr, 0);
+}
+
+int ht_reduce_mg(int64_t n, const ht_mg_layout *L, void *nccl_comm, int rank, int nranks, int wantq, int wantz,
+                 const ht_options *opt, ht_report *rep)
+{
+    if (!L) return HT_EARG_OPT;
+    int rc = validate(n, L->A, L->lda, L->B, L->ldb, L->Q, L->ldq, L->Z, L->ldz, wantq, wantz, opt);
+    if (rc) return rc;
+    if (nranks < 1 || (nccl_comm && (rank < 0 || rank >= nranks))) return HT_EARG_OPT;
+    if (opt && (opt->row_begin != 0 || opt->row_end != 0)) return HT_EARG_OPT;  // the layout decides the slabs
+    if (n == 0) {
+        if (rep) memset(rep, 0, sizeof(*rep));
+        return HT_OK;
+    }
+    if (nccl_comm && nranks > 1) {
+        rc = ht_mg_check_comm(nccl_comm, rank, nranks);
+        if (rc) return rc;
+    }
+    return reduce_impl(n, L->A, L->lda, L->B, L->ldb, L->Q, L->ldq, L->Z, L->ldz, wantq, wantz, opt, rep, nranks,
+                       nccl_comm ? rank : 0, nranks > 1 ? nccl_comm : nullptr, L->gather_qz);
 }
 
 int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb)

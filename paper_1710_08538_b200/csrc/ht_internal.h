@@ -92,6 +92,17 @@ struct PanelArgs {
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);
 int ht_panel_max_blocks(int *nblocks_out);
 
+// multi-GPU plumbing (ht_mg.cu)
+#define TRY_HT(x)                  \
+    do {                           \
+        int _rc = (x);             \
+        if (_rc) return _rc;       \
+    } while (0)
+void ht_slab(int64_t begin, int64_t end, int parts, int r, int64_t *lo, int64_t *hi);
+int ht_mg_allgather(cudaStream_t st, void *comm, int P, int me, double *X, int64_t ldx, int64_t r_beg, int64_t r_end,
+                    int64_t c_beg, int64_t c_end, int by_cols, double *buf, size_t buf_doubles);
+int ht_mg_check_comm(void *comm, int rank, int nranks);
+
 // misc kernels (ht_util.cu)
 int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M, int64_t ld, double *d_out,
                    double *d_part);  // d_part: ht_fro_scratch_size() doubles
