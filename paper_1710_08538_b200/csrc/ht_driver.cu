@@ -1170,9 +1170,10 @@ int reduce_body(Run &R, const ht_options *opt)
         unsigned long long *ttr = nullptr;
         const int64_t tcol = getenv("HT_TRACE_COL") ? atoll(getenv("HT_TRACE_COL")) : -1;
         if (tcol >= 0) {
-            HT_CUDA_TRY(cudaMalloc(&ttr_buf.p, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+            const size_t nt = (size_t)((n - 1 + 127) / 128 + 2) * 8;
+            HT_CUDA_TRY(cudaMalloc(&ttr_buf.p, nt * sizeof(unsigned long long)));
             ttr = (unsigned long long *)ttr_buf.p;
-            HT_CUDA_TRY(cudaMemset(ttr, 0, (size_t)(n / 128 + 2) * 4 * sizeof(unsigned long long)));
+            HT_CUDA_TRY(cudaMemset(ttr, 0, nt * sizeof(unsigned long long)));
         }
         unsigned long long *fprof = nullptr;
         if (getenv("HT_FPROF")) {
@@ -1266,17 +1267,17 @@ int reduce_body(Run &R, const ht_options *opt)
         }
         if (ttr) {
             const int nbk = (int)((n - 1 + 127) / 128) + 2;
-            std::vector<unsigned long long> h((size_t)nbk * 4);
+            std::vector<unsigned long long> h((size_t)nbk * 8);
             HT_CUDA_TRY(cudaMemcpy(h.data(), ttr, h.size() * 8, cudaMemcpyDeviceToHost));
             unsigned long long t0 = ~0ull;
             for (auto v : h)
                 if (v && v < t0) t0 = v;
-            fprintf(stderr, "[ht trace] col %lld: block: tiles_done wait_done matvec_done publish (us from first event)\n", (long long)tcol);
+            fprintf(stderr, "[ht trace] col %lld: block: start stage_done lastload lastfetch tiles_done wait_done matvec_done publish (us)\n", (long long)tcol);
+            auto us = [&](unsigned long long v) { return v ? (v - t0) * 1e-3 : -1.0; };
             for (int b = nbk - 1; b >= 0; --b)
-                if (h[4 * b + 2])
-                    fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f %8.2f\n", b, h[4 * b] ? (h[4 * b] - t0) * 1e-3 : -1.0,
-                            h[4 * b + 1] ? (h[4 * b + 1] - t0) * 1e-3 : -1.0, h[4 * b + 3] ? (h[4 * b + 3] - t0) * 1e-3 : -1.0,
-                            (h[4 * b + 2] - t0) * 1e-3);
+                if (h[8 * b + 2])
+                    fprintf(stderr, "[ht trace] %3d: %8.2f %8.2f %8.2f %8.2f %8.2f %8.2f %8.2f %8.2f\n", b, us(h[8 * b + 4]), us(h[8 * b + 5]),
+                            us(h[8 * b + 7]), us(h[8 * b + 6]), us(h[8 * b + 0]), us(h[8 * b + 1]), us(h[8 * b + 3]), us(h[8 * b + 2]));
         }
         if (dbg_on) {
             std::vector<double> hd((size_t)n * 12);

@@ -51,6 +51,7 @@ struct __align__(16) PanelSmem {
     double rhs[TB];
     double cbv[TB];
     double yrecv[TB];  // y~_{b+1} handed over by the partner CTA of the cluster (DSMEM)
+    unsigned long long mbar;  // completes when the partner has written yrecv/erecv (TB remote arrivals)
     int ival[4];
     int erecv;
 };
@@ -68,6 +69,7 @@ __device__ __forceinline__ unsigned long long gtime()
 }
 struct Ctx {
     const PanelArgs &a;
+    unsigned mbpar = 0;  // parity of the next phase of g_sm.mbar (lo CTAs of the solve clusters)
     int G, bid, tid, lane, warp;
     int64_t n, p0, M, rb0, rb1;
     int nr;
@@ -265,6 +267,25 @@ __device__ __forceinline__ void st_volatile64(unsigned long long *p, unsigned lo
 {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Solve hand-over inside a 2-CTA cluster: the hi CTA stores y~_b into the lo CTA's shared
+// memory and every storing thread arrives (release, cluster scope) on the lo CTA's mbarrier;
+// the lo CTA waits on the phase (acquire).  One-way, ~DSMEM latency: no cluster barrier.
+__device__ __forceinline__ void mbar_remote_arrive(unsigned long long *local_bar, unsigned rank)
+{
+    const unsigned la = (unsigned)__cvta_generic_to_shared(local_bar);
+    unsigned ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long *bar, unsigned parity)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred P;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, P;\n}\n"
+                     : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
 __device__ __forceinline__ void ll_put(unsigned long long *w, double x, unsigned epoch)
 {
     const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -292,6 +313,14 @@ __device__ __forceinline__ int ll_get_exp(const unsigned long long *w, unsigned 
         __nanosleep(64);
     }
     return (int)(unsigned)(v & 0xffffffffull);
+}
+// Packed layout of the pre-scaled block rows Bt = Dinv_b B(block b, blocks > b) (formed per
+// panel by ht_panel_run): block row b is a TB x W_b column-major panel with ld TB (= ldbt),
+// W_b = M - (b+1) TB columns, stored after the block rows above it -- so every TB x TB tile
+// (b, c) is one contiguous 128 KB range (DRAM-friendly streaming in the solve).
+__host__ __device__ __forceinline__ int64_t bt_row_offset(int64_t M, int64_t b)
+{
+    return (int64_t)TB * (b * M - (int64_t)TB * b * (b + 1) / 2);
 }
 // Stage block cb of the solution (w values) into ys[] and return its exponent (all threads).
 __device__ __forceinline__ int fetch_block(Ctx &C, int cb, int w, unsigned epoch, double *ys)
@@ -366,8 +395,10 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
     for (int sb = cid; sb < Nsb; sb += ncl) {
         const int b = Nb - 1 - per * sb - rank;  // hi (rank 0) or lo (rank 1)
         const bool paired_lo = pair && rank == 1;  // lo: y~_{b+1} comes from the partner
-        if (b < 0) {                               // odd Nb: the top super-block has no lo
-            cl.sync();
+        if (b < 0) {  // odd Nb: the top super-block has no lo; its hi still hands over
+            mbar_wait_parity(&g_sm.mbar, C.mbpar);
+            C.mbpar ^= 1u;
+            if (Nsb > ncl) cl.sync();
             continue;
         }
         const int64_t r0 = p0 + (int64_t)b * TB;
@@ -375,7 +406,9 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         const bool safe = a.dsafe[b] != 0;
         const bool last = (b == Nb - 1);
         const int hn = last ? 0 : (int)(n - (r0 + TB) < TB ? n - (r0 + TB) : TB);  // rows of block b+1
-        const double *Bsrc = safe ? a.Bt : a.B;  // off-diagonal tiles
+        // off-diagonal tiles: B, or the packed Bt (a.ldbt = TB), addressed like B: tile (b, c)
+        // = Bsrc + c0(c) * ldsrc + r0 with the base shifted so that tile (b, b+1) is block row b's start
+        const double *Bsrc = safe ? a.Bt + bt_row_offset(M, b) - ((r0 + TB) * a.ldbt + r0) : a.B;
         const int64_t ldsrc = safe ? a.ldbt : a.ldb;
         // (1) rhs_b (all loads of a thread first)
         {
@@ -410,7 +443,7 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
         // (2) stage Bt_{b,b+1} (safe) or D (unsafe) in shared memory; c_b = Dinv_b rhs_b (safe)
         if (safe) {
             if (!last) {
-                const double *src = a.Bt + (size_t)(r0 + TB) * a.ldbt + r0;
+                const double *src = Bsrc + (size_t)(r0 + TB) * a.ldbt + r0;
                 for (int l0 = 0; l0 < TB; l0 += 32) {  // 32 columns per round, 8 loads per thread
                     double t[8];
 #pragma unroll
@@ -468,52 +501,46 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
             acc1 = fma(t1, sc, acc1);
             __syncthreads();  // ys is reused by the next tile
         }
-        if (tt) tt[4 * b + 0] = gtime();
-        {   // fold the 8 column groups: rows 2rp, 2rp+1
-            const int rp = C.tid & 63, g8 = C.tid >> 6;
-            accg[g8 * TB + 2 * rp] = acc0;
-            accg[g8 * TB + 2 * rp + 1] = acc1;
-        }
-        __syncthreads();
-        double s8 = 0.0;
-        if (C.tid < TB) {
-#pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) s8 += accg[g8 * TB + C.tid];
-        }
-        __syncthreads();
+        if (tt) tt[8 * b + 0] = gtime();
         int e = Eacc;
+        double xv = 0.0;  // this thread's entry of the block (tid < TB), exponent e
+        const int rp = C.tid & 63, g8 = C.tid >> 6;
         if (safe) {
-            // (4) critical path: y~_b = c_b 2^(-E) - acc 2^(Eacc-E) - Bt_{b,b+1} y~_{b+1} 2^(e1-E)
-            double xv = 0.0;
+            // (4) critical path: y~_b = c_b 2^(-E) - [acc 2^(Eacc-E) + Bt_{b,b+1} y~_{b+1} 2^(e1-E)]:
+            // the tile moves from shared memory into registers before the wait, so after the
+            // hand-over the hop is 32 FMA + one 8-way fold (the off-diagonal sums ride along)
             if (!last) {
+                TileRegs ct;  // rows 2rp, 2rp+1; columns g8 + 8q
+#pragma unroll
+                for (int q = 0; q < 16; ++q) ct.x[q] = *reinterpret_cast<const double2 *>(Dsm + (g8 + 8 * q) * TB + 2 * rp);
+                const double *yb1;
                 int e1;
                 if (paired_lo) {
-                    cl.sync();  // partner wrote y~_{b+1} and its exponent into yrecv / erecv
-                    if (C.tid < TB) g_sm.rhs[C.tid] = (C.tid < hn) ? g_sm.yrecv[C.tid] : 0.0;
+                    mbar_wait_parity(&g_sm.mbar, C.mbpar);  // partner wrote y~_{b+1}, exponent
+                    yb1 = g_sm.yrecv;
                     e1 = g_sm.erecv;
-                    __syncthreads();
                 } else {
                     e1 = fetch_block(C, b + 1, hn, epoch, g_sm.rhs);
+                    yb1 = g_sm.rhs;
                 }
-                if (tt) tt[4 * b + 1] = gtime() + (g_sm.rhs[0] != g_sm.rhs[0] ? 1 : 0);  // depends on the staged data
-                double sa[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int m = 0; m < TB / 16; ++m)
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int l = grp + 16 * m + 4 * u;
-                        sa[u] = fma(Dsm[l * TB + ri], g_sm.rhs[l], sa[u]);
-                    }
-                accg[grp * TB + ri] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
-                __syncthreads();
-                if (tt) tt[4 * b + 3] = gtime() + (accg[0] != accg[0] ? 1 : 0);
+                if (tt) tt[8 * b + 1] = gtime() + (yb1[0] != yb1[0] ? 1 : 0);  // depends on the staged data
+                double t0 = 0.0, t1 = 0.0;
+                tile_fma(ct, yb1, C.tid, t0, t1);
                 const int E = max(e1, Eacc);
-                if (C.tid < TB)
-                    xv = g_sm.cbv[C.tid] * pow2i(-E) - s8 * pow2i(Eacc - E) -
-                         ((accg[C.tid] + accg[TB + C.tid]) + (accg[2 * TB + C.tid] + accg[3 * TB + C.tid])) * pow2i(e1 - E);
+                const double sa_ = pow2i(Eacc - E), sb_ = pow2i(e1 - E);
+                acc0 = fma(t0, sb_, acc0 * sa_);
+                acc1 = fma(t1, sb_, acc1 * sa_);
                 e = E;
-            } else if (C.tid < TB) {
-                xv = g_sm.cbv[C.tid] * pow2i(-Eacc) - s8;
+            }
+            accg[g8 * TB + 2 * rp] = acc0;  // fold the 8 column groups: rows 2rp, 2rp+1
+            accg[g8 * TB + 2 * rp + 1] = acc1;
+            __syncthreads();
+            if (tt) tt[8 * b + 3] = gtime() + (accg[0] != accg[0] ? 1 : 0);
+            if (C.tid < TB) {
+                double s8 = 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s8 += accg[q * TB + C.tid];
+                xv = g_sm.cbv[C.tid] * pow2i(-e) - s8;
             }
             // (5) post-hoc power-of-two rescale, only if some entry of the block is too large
             const bool big = (C.tid < h) && !(fabs(xv) <= BIG);
@@ -527,13 +554,29 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                 if (!(mx <= BIG)) frexp(mx, &ex);
                 if (!isfinite(mx)) ex = 0;
             }
-            if (C.tid < h) {
-                const double yv = ex ? ldexp(xv, -ex) : xv;
-                a.vy[r0 + C.tid] = yv;
-                ll_put(a.yll + 2 * (r0 + C.tid), yv, epoch);
-            }
+            if (ex) xv = ldexp(xv, -ex);
             e += ex;
+            if (pair && !paired_lo && C.tid < TB) {
+                // hand y~_b to the lo partner's shared memory FIRST (before the global stores)
+                PanelSmem *peer = cl.map_shared_rank(&g_sm, 1);
+                peer->yrecv[C.tid] = (C.tid < h) ? xv : 0.0;
+                if (C.tid == 0) peer->erecv = e;
+                mbar_remote_arrive(&g_sm.mbar, 1);
+            }
+            if (C.tid < h) {
+                a.vy[r0 + C.tid] = xv;
+                ll_put(a.yll + 2 * (r0 + C.tid), xv, epoch);
+            }
         } else {
+            accg[g8 * TB + 2 * rp] = acc0;  // fold the 8 column groups: rows 2rp, 2rp+1
+            accg[g8 * TB + 2 * rp + 1] = acc1;
+            __syncthreads();
+            double s8 = 0.0;
+            if (C.tid < TB) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s8 += accg[q * TB + C.tid];
+            }
+            __syncthreads();
             if (C.tid < TB) g_sm.rhs[C.tid] = (C.tid < h) ? ldexp(g_sm.rhs[C.tid], -Eacc) - s8 : 0.0;
             __syncthreads();
             if (C.warp == 0) {
@@ -551,11 +594,11 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                     const double dcc = Dsm[c * TB + c];
                     double xc = __shfl_sync(0xffffffffu, mine, own) / dcc;
                     if (!(fabs(xc) <= BIG)) {
-                        int ex;
-                        frexp(xc, &ex);
+                        int exx;
+                        frexp(xc, &exx);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) v[q] = ldexp(v[q], -ex);
-                        e += ex;
+                        for (int q = 0; q < 4; ++q) v[q] = ldexp(v[q], -exx);
+                        e += exx;
                         mine = v[0];
                         if (hq == 1) mine = v[1];
                         if (hq == 2) mine = v[2];
@@ -573,29 +616,37 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
                 for (int q = 0; q < 4; ++q)
                     if (l + 32 * q < h) {
                         a.vy[r0 + l + 32 * q] = v[q];
+                        g_sm.rhs[l + 32 * q] = v[q];
                         ll_put(a.yll + 2 * (r0 + l + 32 * q), v[q], epoch);
                     }
                 if (l == 0) g_sm.ival[3] = e;
             }
             __syncthreads();
             e = g_sm.ival[3];
+            if (C.tid < TB) xv = (C.tid < h) ? g_sm.rhs[C.tid] : 0.0;
+            if (pair && !paired_lo && C.tid < TB) {  // unsafe hi block: hand y~_b over
+                PanelSmem *peer = cl.map_shared_rank(&g_sm, 1);
+                peer->yrecv[C.tid] = (C.tid < h) ? xv : 0.0;
+                if (C.tid == 0) peer->erecv = e;
+                mbar_remote_arrive(&g_sm.mbar, 1);
+            }
         }
-        __syncthreads();
+        // the block exponent: its word carries the epoch like the value words (no ordering with them)
         if (C.tid == 0) {
             a.bexp[b] = e;
             st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
-            if (tt) tt[4 * b + 2] = gtime();
+            if (tt) tt[8 * b + 2] = gtime();
         }
-        if (!pair) {
-        } else if (!paired_lo) {
-            // hand y~_b (this CTA's values, exponent e) to the lo partner's shared memory
-            PanelSmem *peer = cl.map_shared_rank(&g_sm, 1);
-            if (C.tid < TB) peer->yrecv[C.tid] = (C.tid < h) ? a.vy[r0 + C.tid] : 0.0;
-            if (C.tid == 0) peer->erecv = e;
-            cl.sync();
-        } else if (!(safe && !last)) {
-            cl.sync();  // lo blocks that did not wait on the handoff still complete the cluster phase
+        if (paired_lo) {
+            // every phase of the mbarrier completes once per super-block (the hi partner always
+            // hands over); a lo block that did not wait on it still consumes the phase
+            if (!(safe && !last)) mbar_wait_parity(&g_sm.mbar, C.mbpar);
+            C.mbpar ^= 1u;
         }
+        // yrecv is rewritten only by the next super-block of this cluster: a cluster barrier keeps
+        // the lo CTA's reads of this one ahead of it (not needed while n <= TB * G)
+        if (pair && Nsb > ncl) cl.sync();
+        else __syncthreads();
     }
     __syncthreads();
 }
@@ -847,6 +898,12 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
 {
     cg::grid_group grid = cg::this_grid();
     Ctx C(a);
+    if (threadIdx.x == 0) {  // the solve's hand-over barrier: TB remote arrivals per phase
+        const unsigned mb = (unsigned)__cvta_generic_to_shared(&g_sm.mbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(TB) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cg::this_cluster().sync();  // the partner's barrier is initialised before any remote arrive
     const int64_t n = a.n, s0 = a.s0, p0 = C.p0, lda = a.lda;
     double *A = a.A;
     double *U = a.U, *V = a.V, *Y = a.Y, *S = a.S, *T = a.T;
@@ -1260,14 +1317,16 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb = (int)((M + TB - 1) / TB);
     inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
     HT_CUDA_TRY(cudaGetLastError());
-    // Bt(block b, blocks > b) = Dinv_b * B(block b, blocks > b): pre-scaled block rows
+    // Bt(block b, blocks > b) = Dinv_b * B(block b, blocks > b): pre-scaled block rows, packed
+    // (bt_row_offset, ld TB: every TB x TB tile contiguous)
+    a->ldbt = TB;
     if (Nb > 1) {
         std::vector<GemmBatchItem> it;
         for (int b = 0; b + 1 < Nb; ++b) {
             const int64_t r0 = a->s0 + 1 + (int64_t)b * TB, c0 = r0 + TB;
             const int w = (int)(a->n - c0);
-            it.push_back(GemmBatchItem{a->Dinv + (size_t)b * TB * TB, a->B + r0 + c0 * a->ldb, a->Bt + r0 + c0 * a->ldbt,
-                                       TB, a->ldb, a->ldbt, TB, w, TB, 1.0, 0.0, 0.0});
+            it.push_back(GemmBatchItem{a->Dinv + (size_t)b * TB * TB, a->B + r0 + c0 * a->ldb, a->Bt + bt_row_offset(M, b),
+                                       TB, a->ldb, TB, TB, w, TB, 1.0, 0.0, 0.0});
         }
         int rc = ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size());
         if (rc) return rc;
