@@ -68,7 +68,7 @@ struct Work {
     double *VhatB = nullptr, *QwB = nullptr, *TmB = nullptr, *tauB = nullptr, *WtB = nullptr;
     int64_t *d_force = nullptr;
     int *d_irtrace = nullptr;
-    double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr;
+    double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr, *ypartB = nullptr, *BV = nullptr;
     int *dsafe = nullptr;
     double *fro_part = nullptr;  // fixed-order partial sums of ||B||_F^2
     double *mgbuf = nullptr;     // packed all-gather staging (ht_reduce_mg)
@@ -187,6 +187,10 @@ void work_free(Work &w)
     w.Bt = nullptr;
     if (w.ypart) cudaFree(w.ypart);
     w.ypart = nullptr;
+    if (w.ypartB) cudaFree(w.ypartB);
+    w.ypartB = nullptr;
+    if (w.BV) cudaFree(w.BV);
+    w.BV = nullptr;
     if (w.dsafe) cudaFree(w.dsafe);
     w.Dinv = nullptr;
     w.dsafe = nullptr;
@@ -290,6 +294,8 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.Dinv, (size_t)(N / 128 + 2) * 128 * 128));
     TRY(dalloc(&w.Bt, (size_t)N * (size_t)N));
     TRY(dalloc(&w.ypart, (size_t)(N / 256 + 2) * (size_t)N));
+    TRY(dalloc(&w.ypartB, (size_t)(N / 256 + 2) * (size_t)N));
+    TRY(dalloc(&w.BV, nnb));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
@@ -978,20 +984,23 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     return 0;
 }
 
-// Algorithmic HBM bytes of one panel: the trailing B
-// triangle once per solve and per residual, the trailing A block once per A*v.
+// Algorithmic HBM bytes of one panel: per solve, the trailing B triangle
+// once (the factored solve reads the packed Bt = Dinv B, the same element count) and one fused
+// sweep over A(s+1:n, j+1:n) and the upper part of B(s+1:n, j+1:n) (P4's B w and P5's A v);
+// every IR step repeats both.
+double panel_elems_sweep(int64_t n, int64_t s0, int64_t i)
+{
+    const double M = (double)(n - s0 - 1), c = (double)(n - (s0 + i) - 1);
+    return M * c + (double)i * c + c * (c + 1) / 2.0;  // A block + B rows s+1..j + B triangle
+}
 double panel_bytes(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
 {
     const double M = (double)(n - s0 - 1);
-    const double tri = 8.0 * M * (M + 1) / 2.0;
-    double b = 0.0;
-    for (int64_t i = 0; i < k; ++i) {
-        b += tri;                                  // solve
-        if (i > 0) b += tri;                       // residual
-        b += 8.0 * M * (double)(n - (s0 + i) - 1); // A v
-    }
-    b += 2.0 * tri * (double)ir_steps;
-    return b;
+    const double tri = M * (M + 1) / 2.0;
+    double e = 0.0;
+    for (int64_t i = 0; i < k; ++i) e += tri + panel_elems_sweep(n, s0, i);
+    e += (double)ir_steps * (tri + panel_elems_sweep(n, s0, k / 2));
+    return 8.0 * e;
 }
 
 double panel_flops(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
@@ -999,13 +1008,10 @@ double panel_flops(int64_t n, int64_t s0, int64_t k, int64_t ir_steps)
     const double M = (double)(n - s0 - 1);
     double f = 0.0;
     for (int64_t i = 0; i < k; ++i) {
-        const double j0 = (double)(s0 + i);
-        f += M * M;                                 // factored solve (trsv)
-        if (i > 0) f += M * M;                      // residual (trmv)
-        f += 2.0 * M * (n - j0 - 1);                // A v
-        f += (4.0 * n + 22.0 * M) * (double)i;      // small WY terms
+        f += M * M + 2.0 * panel_elems_sweep(n, s0, i);  // factored solve (trsv) + fused sweep
+        f += (4.0 * n + 22.0 * M) * (double)i;           // small WY terms
     }
-    f += 2.0 * M * M * (double)ir_steps;            // IR: solve + residual
+    f += (double)ir_steps * (M * M + 2.0 * panel_elems_sweep(n, s0, k / 2));  // IR: solve + sweep
     return f;
 }
 
@@ -1200,6 +1206,7 @@ int reduce_body(Run &R, const ht_options *opt)
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.yll = w->yll; pa.yll_exp = w->yll_exp; pa.bexp = w->bexp; pa.epoch = w->epoch;
             pa.Dinv = w->Dinv; pa.Bt = w->Bt; pa.ldbt = n; pa.dsafe = w->dsafe; pa.ypart = w->ypart;
+            pa.ypartB = w->ypartB; pa.BV = w->BV; pa.vbx = vv + 7 * N;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;

@@ -86,7 +86,10 @@ struct PanelArgs {
     int *irtrace;       // per-column IR count (+1000 after a failed attempt)
     unsigned long long *ttrace;  // optional (HT_TRACE_COL): per-block trsv timestamps of one column
     int64_t tcol;
-    double *ypart;      // tiled mat-vec partial sums: [column chunk][row], ld = n
+    double *ypart;      // tiled mat-vec partial sums: [column chunk][row], ld = n (A x)
+    double *ypartB;     // the same for B x
+    double *BV;         // n x nb: B v_i of the panel's right reflectors (absolute row index)
+    double *vbx;        // n-vector: B x of the current solve
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
 };
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);

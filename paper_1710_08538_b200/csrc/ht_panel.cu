@@ -46,6 +46,7 @@ struct __align__(16) PanelSmem {
     double sv2[NBMAX + 2];
     double sv3[NBMAX + 2];
     double snew[NBMAX + 2];  // new column of S
+    double svx[NBMAX + 2];   // V^T x of the current solve (kept for P5's V^T v)
     double vloc[RBMAX];      // own-row vector cache
     double red[32];
     double rhs[TB];
@@ -778,7 +779,7 @@ struct TileGeom {
 };
 
 template <class VF>
-__device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf)
+__device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf, double *yp)
 {
     double *red = g_dyn;               // [NWP][TRT]
     double *vs = g_dyn + NWP * TRT;    // [TCW]
@@ -879,18 +880,18 @@ __device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_
             double t = 0.0;
 #pragma unroll
             for (int w = 0; w < NWP; ++w) t += red[w * TRT + C.tid];
-            if (r < tg.r_end) C.a.ypart[(size_t)cc * C.n + r] = t;
+            if (r < tg.r_end) yp[(size_t)cc * C.n + r] = t;
         }
     }
     __syncthreads();
 }
 
 // y(r) = sum of the item partials of row r (after a grid sync), fixed order.
-__device__ __forceinline__ double tiled_sum(const Ctx &C, const TileGeom &tg, int64_t r)
+__device__ __forceinline__ double tiled_sum(const Ctx &C, const TileGeom &tg, int64_t r, const double *yp)
 {
     const int rb = (int)((r - tg.r_al) / TRT);
     double t = 0.0;
-    for (int cc = tg.cc_min(rb); cc < tg.ncc; ++cc) t += __ldcg(C.a.ypart + (size_t)cc * C.n + r);
+    for (int cc = tg.cc_min(rb); cc < tg.ncc; ++cc) t += __ldcg(yp + (size_t)cc * C.n + r);
     return t;
 }
 
@@ -1047,32 +1048,41 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         __syncthreads();
 
         // ================= P4: residual + iterative refinement ================
+        // One HBM sweep per solve serves both P4 and P5: with x known,
+        //   A x over A(s+1:n, j+1:n)   -> P5's A v = A e_{j+1} + scal (A x - A e_{j+1} x_{j+1})
+        //   B x over B(s+1:n, j+1:n)   -> the residual's B w = B x - (B V)(T V^T x)
+        // where B V is kept column by column (B v = B e_{j+1} + scal (B x - B e_{j+1} x_{j+1})).
+        // If IR corrects x, the sweep is redone for the new x (the A half is then speculative).
         bool accepted = (k == 0);  // k = 0: stable solve, no test (reading R-Z4)
         bool forced = false;
         while (ffi < a.n_force_fail && a.force_fail[ffi] < j0) ++ffi;
         if (ffi < a.n_force_fail && a.force_fail[ffi] == j0 && k > 0) forced = true;
         int ir = 0;
         bool this_col_ir = false;
-        while (!accepted) {
-            // w = (I - V T V^T)[0; x]
-            C.gather(g_sm.sv1, k, 2);  // V^T x
+        const TileGeom tga(p0, n, j0 + 1, n, false);  // A(s+1:n, j+1:n)
+        const TileGeom tgb(p0, n, j0 + 1, n, true);   // B(s+1:n, j+1:n), upper part
+        auto Tget = [&](int i, int c) { return T[(size_t)c * nb + i]; };
+        while (true) {
+            C.gather(g_sm.svx, k, 2);  // V^T x
             __syncthreads();
-            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);  // T t
-            C.rowgemv(V, n, k, g_sm.sv2);
+            if (k > 0) C.trimv<false>(Tget, k, g_sm.svx, g_sm.sv2);  // z = T V^T x
+            mark(6);
+            tiled_matvec(C, tga, A, lda, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypart);
+            tiled_matvec(C, tgb, a.B, a.ldb, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypartB);
+            grid.sync();
+            mark(4);
+            if (k > 0) C.rowgemv(a.BV, n, k, g_sm.sv2);  // (B V) z for own rows
             for (int rl = C.tid; rl < C.nr; rl += PNT) {
                 const int64_t r = C.rb0 + rl;
-                a.vw[r] = __ldcg(&a.vx[r]) - g_dyn[rl];
+                const double bx = tiled_sum(C, tgb, r, a.ypartB);
+                a.vw[r] = tiled_sum(C, tga, r, a.ypart);
+                a.vbx[r] = bx;
+                if (k > 0) a.vw2[r] = bx - g_dyn[rl];  // w2 = B w
             }
-            grid.sync();
-            // w2 = B w over area-balanced slabs, + partial U^T w2
+            if (accepted) break;  // k = 0
+            __syncthreads();
             C.ph++;
-            mark(6);
-            const TileGeom tgb(p0, n, p0, n, true);
-            tiled_matvec(C, tgb, a.B, a.ldb, [&](int64_t c) { return __ldcg(&a.vw[c]); });
-            grid.sync();
-            {
-                for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tgb, C.rb0 + rl);
-                __syncthreads();
+            {   // partial U^T w2
                 double *stg = g_dyn;
                 for (int c = C.warp; c < ku; c += NWP) {
                     double s = 0.0;
@@ -1144,7 +1154,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             grid.sync();
             C.gather(g_sm.sv1, k, 0);
             __syncthreads();
-            C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);
+            C.trimv<true>(Tget, k, g_sm.sv1, g_sm.sv2);
             C.rowgemv(V, n, k, g_sm.sv2);
             C.ph++;
             {
@@ -1182,49 +1192,39 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             failed = 1;
             break;
         }
-        // ================= P5: right reflector, T, Y ===========================
+        // ================= P5: right reflector, T, Y (no sweep, no grid barrier) ==========
         double gam, scal_v;
+        const double x1 = __ldcg(&a.vx[j0 + 1]);
         {
-            const double alpha = __ldcg(&a.vx[j0 + 1]);
             gam = 0.0;
             scal_v = 0.0;
             if (xtail2 > 0.0) {
-                double nrm = sqrt(alpha * alpha + xtail2);
-                double bet = alpha >= 0.0 ? -nrm : nrm;
-                gam = (bet - alpha) / bet;
-                scal_v = 1.0 / (alpha - bet);
+                double nrm = sqrt(x1 * x1 + xtail2);
+                double bet = x1 >= 0.0 ? -nrm : nrm;
+                gam = (bet - x1) / bet;
+                scal_v = 1.0 / (x1 - bet);
             }
         }
-        auto vget = [&](int64_t r) -> double {
-            return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_v);
-        };
-        C.ph++;
-        for (int rl = C.tid; rl < C.nr; rl += PNT) {
-            const int64_t r = C.rb0 + rl;
-            double v = vget(r);
-            V[(size_t)k * n + r] = v;
-            g_sm.vloc[rl] = v;
+        // V^T v = V(j+1,:)^T + scal (V^T x - V(j+1,:)^T x_{j+1})   (v = [1; scal x(j+2:n)])
+        for (int c = C.tid; c < k; c += PNT) {
+            const double vj = V[(size_t)c * n + j0 + 1];
+            g_sm.sv1[c] = vj + scal_v * (g_sm.svx[c] - vj * x1);
         }
         __syncthreads();
-        C.coltdot(V, n, k, 0);
-        // A(p0:n, j0+1:n) v  (tiled, partials in ypart)
-        const TileGeom tga(p0, n, j0 + 1, n, false);
-        tiled_matvec(C, tga, A, lda, vget);
-        grid.sync();
-        mark(4);
-        for (int rl = C.tid; rl < C.nr; rl += PNT) a.vw2[C.rb0 + rl] = tiled_sum(C, tga, C.rb0 + rl);
-        __syncthreads();
-        C.gather(g_sm.sv1, k, 0);  // z = V^T v
-        __syncthreads();
         if (C.bid == 0) {
-            C.trimv<false>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2, -gam);
+            C.trimv<false>(Tget, k, g_sm.sv1, g_sm.sv2, -gam);
             for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = g_sm.sv2[i];
             if (C.tid == 0) T[(size_t)k * nb + k] = gam;
         }
         C.rowgemv(Y, n, k, g_sm.sv1);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
-            Y[(size_t)k * n + r] = gam * (a.vw2[r] - g_dyn[rl]);
+            V[(size_t)k * n + r] = (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_v);
+            const double acol = A[(size_t)(j0 + 1) * lda + r];
+            const double av = acol + scal_v * (a.vw[r] - acol * x1);                 // A v
+            const double bcol = (r <= j0 + 1) ? a.B[(size_t)(j0 + 1) * a.ldb + r] : 0.0;
+            a.BV[(size_t)k * n + r] = bcol + scal_v * (a.vbx[r] - bcol * x1);        // B v
+            Y[(size_t)k * n + r] = gam * (av - g_dyn[rl]);
         }
         ++k;
         __syncthreads();
