@@ -17,6 +17,8 @@ the BASELINE.json variants):
                           then round(0.1 n) random diagonal positions set to 0
                           (reading R-Z17)
   cfg5  n=16384, seed 4: as cfg2
+  saddle  (Test Suite 4): A = [[X, Y], [Y^T, 0]], B = diag(I_{3n/4}, 0)
+  general A, B ~ N(0,1), B not triangular (QZ step-1 front end)
 
 The generators also accept any n so that tests can draw the same distributions
 at sizes the oracle finishes in seconds.
@@ -62,6 +64,26 @@ def pencil(kind: str, n: int, seed: int):
             nz = int(round(0.1 * n))
             idx = rng.choice(n, nz, replace=False)
             B[idx, idx] = 0.0
+    elif kind == "saddle":
+        # Test Suite 4: A = [[X, Y], [Y^T, 0]], B = diag(I, 0) with X
+        # symmetric positive definite of 3/4 the dimension and Y random full-rank; X = G^T G + n I
+        # (SPEC S:612's documented construction of "random SPD").  n must be divisible by 4.
+        if n % 4:
+            raise ValueError("saddle pencils need n divisible by 4")
+        m1 = 3 * n // 4
+        G = rng.standard_normal((m1, m1))
+        X = G.T @ G + n * np.eye(m1)
+        Y = rng.standard_normal((m1, n - m1))
+        A = np.zeros((n, n))
+        A[:m1, :m1] = X
+        A[:m1, m1:] = Y
+        A[m1:, :m1] = Y.T
+        B = np.zeros((n, n))
+        B[np.arange(m1), np.arange(m1)] = 1.0
+    elif kind == "general":
+        # a general (not triangular) B: the QZ step-1 front end (HT_FLAG_GENERAL_B)
+        A = rng.standard_normal((n, n))
+        B = rng.standard_normal((n, n))
     elif kind == "ht":
         # already in Hessenberg-triangular form: the degenerate case where
         # every reflector is the identity (SURVEY §8(c) special cases)

@@ -104,7 +104,22 @@ typedef struct {
        0, 0 = all rows.  Requires 0 <= row_begin <= row_end <= n, else HT_EARG_OPT. */
     int64_t row_begin;
     int64_t row_end;
+    /* HT_FLAG_* below (0 = the plain reduction of a triangular B) */
+    uint32_t flags;
 } ht_options;
+
+/* ht_options.flags */
+/* QZ step 1 front end: B may be a general square matrix; the library
+   first computes B = Q0 R (Householder QR by panels, each panel reduced by a staircase of
+   2k x k window QRs as in sec. 3.3.2b), A <- Q0^T A, B <- R, and the returned Q includes Q0.
+   (Q e1 = e1 then no longer holds.)  Without the flag B must be upper triangular. */
+#define HT_FLAG_GENERAL_B 1u
+/* Preprocessing of sec. 3.5.1: if B (upper triangular) has l > 0 exactly-zero
+   columns, a permutation Z0 moves them first (Q0 = Z0 if B is diagonal, else I), a QR of
+   the first l columns of Q0^T A Z0 gives A(:, 1:l) = [A11; 0], the trailing block of B is
+   re-triangularised (QR), and only the trailing (n-l) x (n-l) pencil is reduced to HT form.
+   The leading l x l part is already in generalised Schur form (T's first l columns are 0). */
+#define HT_FLAG_DEFLATE_ZERO_COLUMNS 2u
 
 /* Statistics of one reduction (the paper's Table 3/4 columns). */
 typedef struct {
@@ -141,6 +156,8 @@ typedef struct {
        Q and Z are invariant under such scalings)                                       */
     double scale_a;
     double scale_b;
+    int64_t deflated_columns;  /* l of HT_FLAG_DEFLATE_ZERO_COLUMNS (sec. 3.5.1)             */
+    double t_front;            /* device seconds of the front end (GENERAL_B / DEFLATE)      */
 } ht_report;
 
 /*

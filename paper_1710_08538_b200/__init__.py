@@ -23,6 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
 
 HT_OK = 0
+HT_FLAG_GENERAL_B = 1
+HT_FLAG_DEFLATE_ZERO_COLUMNS = 2
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
           -6: "HT_EARG_WANTQ", -7: "HT_EARG_WANTZ", -8: "HT_EARG_NB", -9: "HT_EARG_OPT",
           1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC", 5: "HT_ENCCL"}
@@ -36,7 +38,7 @@ class HTOptions(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p),
                 ("force_ir_fail", ctypes.POINTER(ctypes.c_int64)), ("n_force_ir_fail", ctypes.c_int64),
                 ("ir_trace", ctypes.POINTER(ctypes.c_int32)), ("max_panels", ctypes.c_int64),
-                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64)]
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64), ("flags", ctypes.c_uint32)]
 
 
 class HTReport(ctypes.Structure):
@@ -49,7 +51,8 @@ class HTReport(ctypes.Structure):
                 ("t_other", ctypes.c_double), ("panel_bytes", ctypes.c_double), ("launches", ctypes.c_int64),
                 ("t_chain", ctypes.c_double), ("flops_chain", ctypes.c_double), ("chain_launches", ctypes.c_int64),
                 ("t_absorb_right", ctypes.c_double), ("t_absorb_left", ctypes.c_double),
-                ("t_factor_exposed", ctypes.c_double), ("scale_a", ctypes.c_double), ("scale_b", ctypes.c_double)]
+                ("t_factor_exposed", ctypes.c_double), ("scale_a", ctypes.c_double), ("scale_b", ctypes.c_double),
+                ("deflated_columns", ctypes.c_int64), ("t_front", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -147,8 +150,9 @@ def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True):
 
 
 def make_options(nb=0, max_ir=0, tol_factor=0.0, seed=0, stream=None, force_ir_fail=(), ir_trace=None, max_panels=0,
-                 row_range=None):
+                 row_range=None, flags=0):
     opt = HTOptions()
+    opt.flags = int(flags)
     if row_range is not None:
         opt.row_begin, opt.row_end = int(row_range[0]), int(row_range[1])
     opt.nb = int(nb)

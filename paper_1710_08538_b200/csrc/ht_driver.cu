@@ -559,6 +559,108 @@ struct Run {
         return rc;
     }
 
+    // ---------------- front end: Householder QR by staircase panels ---------------------
+    // X(r0:n, c0:c0+c) <- R (upper trapezoidal, exact zeros below) in place, by panels of q <= nq
+    // columns.  A panel (rows rt:n) is reduced bottom -> top by a staircase of window QRs,
+    // exactly the chain structure of sec. 3.3.2b (eq. qrdecomposition): the first
+    // window is the bottom kt rows (q < kt <= 2q, q | (m - kt), Remark 4), every next one is
+    // [q new rows; R of the window below].  The window transforms are then applied from the
+    // left to X's columns [c0+p+q, x_end) and to Y(rt:n, y_c0:y_c1), and from the right to
+    // Q(:, rt:n) -- the panel's Q factor is exactly the product of its windows (Q <- Q W1 W2 ...).
+    int qr_left(double *X, int64_t ldx, int64_t r0, int64_t c0, int64_t c, int64_t x_end, double *Y, int64_t ldy,
+                int64_t y_c0, int64_t y_c1, int64_t nq)
+    {
+        const Store sto = main_store();
+        for (int64_t p = 0; p < c; p += nq) {
+            const int64_t rt = r0 + p, m = n - rt, q = std::min<int64_t>(nq, c - p);
+            if (m <= 1 || q <= 0) break;
+            const int64_t q1 = std::min<int64_t>(q, m);
+            w->fd_cur = w->ld_cur = w->cw_cur = 0;
+            wins_reset();
+            std::vector<FactorDesc> fds;
+            std::vector<int64_t> tops;
+            auto window = [&](int64_t a, int64_t b, bool stair) {
+                Win x = add_win((int)(b - a), (int)q1);
+                FactorDesc fd{X + (rt + a) + (c0 + p) * ldx, 1, ldx, (int)(b - a), (int)q1, 0, sto.Vhat + x.ov, b - a,
+                              sto.tau + x.ot};
+                if (stair) fd.dense = (int)(b - a - q1);  // [q new rows; R of the window below]
+                fds.push_back(fd);
+                tops.push_back(a);
+            };
+            if (m <= 2 * q1) {
+                window(0, m, false);
+            } else {
+                const int64_t rem = (m - q1) % q1, kt = q1 + (rem == 0 ? q1 : rem);
+                window(m - kt, m, false);
+                for (int64_t top = m - kt; top > 0; top -= q1) window(top - q1, top + q1, true);
+            }
+            TRY(factor_and_form(fds, 0));
+            std::vector<ChainWin> wl;
+            const int64_t xs = c0 + p + q1;
+            for (size_t i = 0; i < fds.size(); ++i)
+                wl.push_back(ChainWin{sto.Qw + wins[i].oq, rt + tops[i], wins[i].p, {xs, y_c0, qz0}, {x_end, y_c1, qz1}});
+            std::vector<ChainMat> mats;
+            mats.push_back(ChainMat{X, ldx, 1, xs, x_end});
+            mats.push_back(ChainMat{Y, ldy, 1, y_c0, y_c1});
+            if (wq) mats.push_back(ChainMat{Q, ldq, 0, qz0, qz1});
+            TRY(chain(mats, wl));
+            // the descriptors live in pinned host buffers read by the queued copies: drain before
+            // the next panel rewrites them
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        return 0;
+    }
+
+    // Front end (ht_options.flags).  HT_FLAG_DEFLATE_ZERO_COLUMNS: sec. 3.5.1 --
+    // zero columns of B first (Z0; Q0 = Z0 if B is diagonal), QR of A's first l columns, QR of
+    // the trailing block of B; *s_begin = l.  HT_FLAG_GENERAL_B: QR of B (QZ step 1).
+    int front_end(uint32_t flags, int64_t *s_begin)
+    {
+        *s_begin = 0;
+        const int64_t nq = std::min<int64_t>(nb, 128);
+        if (flags & HT_FLAG_DEFLATE_ZERO_COLUMNS) {
+            int *zc = reinterpret_cast<int *>(w->d_irtrace);  // n ints of scratch (the IR trace is set later)
+            TRY(ht_zero_columns(st, n, B, ldb, zc, w->d_iflags + 2));
+            std::vector<int> hz(n);
+            HT_CUDA_TRY(cudaMemcpyAsync(hz.data(), zc, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+            HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags + 2, w->d_iflags + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+            HT_CUDA_TRY(cudaStreamSynchronize(st));
+            const bool diagonal = w->h_iflags[2] == 0;
+            std::vector<int64_t> perm;  // zero columns first, stable (SPEC's determinism)
+            for (int64_t j = 0; j < n; ++j)
+                if (hz[j]) perm.push_back(j);
+            const int64_t l = (int64_t)perm.size();
+            for (int64_t j = 0; j < n; ++j)
+                if (!hz[j]) perm.push_back(j);
+            if (l > 0 && l < n) {
+                int64_t *dp = w->d_force;  // n int64 of scratch (the forced-failure list is uploaded later)
+                HT_CUDA_TRY(cudaMemcpyAsync(dp, perm.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+                double *tmp = w->Bt;       // n x n scratch (used by the panels only)
+                const int64_t *pr = diagonal ? dp : nullptr;
+                // A0 = Q0^T A Z0, B0 = Q0^T B Z0 (Q0 = Z0 for diagonal B): rows and columns gathered
+                TRY(ht_permute(st, n, n, A, lda, tmp, n, pr, dp));
+                TRY(ht_copy2d(st, n, n, tmp, n, A, lda));
+                TRY(ht_permute(st, n, n, B, ldb, tmp, n, pr, dp));
+                TRY(ht_copy2d(st, n, n, tmp, n, B, ldb));
+                if (wz) TRY(ht_perm_matrix(st, n, Z, ldz, dp));
+                if (wq && diagonal) TRY(ht_perm_matrix(st, n, Q, ldq, dp));
+                HT_CUDA_TRY(cudaStreamSynchronize(st));  // dp is reused as the forced-failure list
+                // A0(:, 1:l) = Q1 [A11; 0]: Q1^T on A's other columns and on B (its first l columns are 0)
+                TRY(qr_left(A, lda, 0, 0, l, n, B, ldb, l, n, nq));
+                // the trailing block B(l:n, l:n) back to triangular form; A(l:n, 1:l) = 0 stays 0
+                TRY(qr_left(B, ldb, l, l, n - l, n, A, lda, l, n, nq));
+                TRY(zero_lower(n - l, n - l, B + l + l * ldb, ldb, 0));
+                TRY(zero_lower(n, l, A, lda, 0));  // A11 upper triangular, zeros below (exact)
+                *s_begin = l;
+            }
+        }
+        if ((flags & HT_FLAG_GENERAL_B) && *s_begin == 0) {
+            TRY(qr_left(B, ldb, 0, 0, n, n, A, lda, 0, n, nq));  // B = Q0 R; A <- Q0^T A; Q <- Q0
+            TRY(zero_lower(n, n, B, ldb, 0));
+        }
+        return 0;
+    }
+
     // ---------------- absorption (sec. 3.3) ---------------------------------
     // Streams: st (high priority) carries the critical path -- the staircase factorization
     // chains and every update of B (the chains read B's band); sA applies the same window
@@ -978,6 +1080,7 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     if (wantz != 0 && wantz != 1) return HT_EARG_WANTZ;
     if (opt && opt->nb > ((int64_t)1 << 20)) return HT_EARG_NB;
     if (opt && (opt->n_force_ir_fail < 0 || (opt->n_force_ir_fail > 0 && !opt->force_ir_fail))) return HT_EARG_OPT;
+    if (opt && (opt->flags & ~(HT_FLAG_GENERAL_B | HT_FLAG_DEFLATE_ZERO_COLUMNS))) return HT_EARG_OPT;
     if (opt && (opt->row_begin != 0 || opt->row_end != 0) &&
         (opt->row_begin < 0 || opt->row_end > n || opt->row_begin > opt->row_end))
         return HT_EARG_OPT;
@@ -1116,8 +1219,9 @@ int reduce_body(Run &R, const ht_options *opt)
     HT_CUDA_TRY(cudaMemcpyAsync(w->h_iflags, w->d_iflags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     HT_CUDA_TRY(cudaMemcpyAsync(w->h_scal + 4, d_max, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     HT_CUDA_TRY(cudaStreamSynchronize(st));
+    const uint32_t flags = opt ? opt->flags : 0u;
     if (w->h_iflags[0]) return HT_ENONFINITE;
-    if (w->h_iflags[1]) return HT_EARG_B;
+    if (w->h_iflags[1] && !(flags & HT_FLAG_GENERAL_B)) return HT_EARG_B;
     // exact power-of-two range scaling (include/ht.h "Range"): squared norms of columns,
     // reflectors and ||B||_F stay finite and normal; no rounding is introduced, and the
     // result is bitwise that of the unscaled computation whenever no scaling is needed
@@ -1134,6 +1238,14 @@ int reduce_body(Run &R, const ht_options *opt)
     HT_CUDA_TRY(cudaEventRecord(w->ev_t0, st));
     if (R.wq) TRY(ht_fill2d(st, n, n, dQ, lddq, 0.0, 1.0));
     if (R.wz) TRY(ht_fill2d(st, n, n, dZ, lddz, 0.0, 1.0));
+    int64_t s_begin = 0;
+    if (n > 2 && (flags & (HT_FLAG_GENERAL_B | HT_FLAG_DEFLATE_ZERO_COLUMNS))) {
+        const auto f0 = std::chrono::steady_clock::now();
+        TRY(R.front_end(flags, &s_begin));
+        HT_CUDA_TRY(cudaStreamSynchronize(st));
+        R.rep.t_front = std::chrono::duration<double>(std::chrono::steady_clock::now() - f0).count();
+        R.rep.deflated_columns = s_begin;
+    }
     int64_t ndesing = 0;
     if (n > 2) {
         TRY(ht_fro_norm_sq(st, n, n, dB, lddb, w->d_scal, w->fro_part));
@@ -1188,7 +1300,7 @@ int reduce_body(Run &R, const ht_options *opt)
             HT_CUDA_TRY(cudaMemset(fprof, 0, 32 * sizeof(unsigned long long)));
             TRY(ht_factor_set_prof(fprof));
         }
-        int64_t s0 = 0;
+        int64_t s0 = s_begin;  // > 0 after the sec. 3.5.1 preprocessing: only the trailing pencil
         while (s0 <= n - 3) {
             const int64_t kmax = std::min<int64_t>(nb, n - 2 - s0);
             TRY(ht_desingularize(st, n, dB, lddb, s0 + 1, HT_U * nB, 2.0 * HT_U * nB, seed, s0, w->d_iflags));

@@ -112,6 +112,10 @@ int ht_fro_norm_sq(cudaStream_t st, int64_t rows, int64_t cols, const double *M,
 int ht_fro_scratch_size();
 int ht_check_input(cudaStream_t st, int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
                    int *d_flags, unsigned long long *d_maxbits);
+int ht_zero_columns(cudaStream_t st, int64_t n, const double *B, int64_t ldb, int *d_zc, int *d_flags);
+int ht_permute(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+               const int64_t *d_perm_r, const int64_t *d_perm_c);
+int ht_perm_matrix(cudaStream_t st, int64_t n, double *M, int64_t ld, const int64_t *d_perm);
 int ht_scale(cudaStream_t st, int64_t rows, int64_t cols, double *M, int64_t ld, double s);
 int ht_finish(cudaStream_t st, int64_t n, double *A, int64_t lda, double *B, int64_t ldb, const double *Q, int64_t ldq,
               const double *Z, int64_t ldz, double sa, double sb, int partial, int *d_flag);

@@ -133,7 +133,78 @@ __global__ void zero_lower_kernel(int64_t rows, int64_t cols, double *M, int64_t
             if (i >= 0) M[j * ld + i] = 0.0;
 }
 
+// Column j of B exactly zero -> zc[j] = 1 (bitwise-zero test; sec. 3.5.1 deflates structural
+// zeros only); any nonzero off-diagonal entry -> flags[0] |= 1 (B not diagonal)
+__global__ void zero_cols_kernel(int64_t n, const double *B, int64_t ldb, int *zc, int *flags)
+{
+    __shared__ int any;
+    for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+        if (threadIdx.x == 0) any = 0;
+        __syncthreads();
+        int nz = 0, off = 0;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double v = B[j * ldb + i];
+            if (v != 0.0) {
+                nz = 1;
+                if (i != j) off = 1;
+            }
+        }
+        if (nz) atomicOr(&any, 1);
+        if (off) atomicOr(&flags[0], 1);
+        __syncthreads();
+        if (threadIdx.x == 0) zc[j] = any ? 0 : 1;
+        __syncthreads();
+    }
+}
+
+// dst(i, j) = src(perm_r[i], perm_c[j]) (perm_* null: identity)
+__global__ void permute_kernel(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+                               const int64_t *perm_r, const int64_t *perm_c)
+{
+    for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+        const int64_t sj = perm_c ? perm_c[j] : j;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+            dst[j * ldd + i] = src[sj * lds + (perm_r ? perm_r[i] : i)];
+    }
+}
+
+// M = the permutation matrix with columns e_{perm[j]} (M(perm[j], j) = 1)
+__global__ void perm_matrix_kernel(int64_t n, double *M, int64_t ld, const int64_t *perm)
+{
+    for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            M[j * ld + i] = (i == perm[j]) ? 1.0 : 0.0;
+}
+
 }  // namespace
+
+int ht_zero_columns(cudaStream_t st, int64_t n, const double *B, int64_t ldb, int *d_zc, int *d_flags)
+{
+    HT_CUDA_TRY(cudaMemsetAsync(d_flags, 0, sizeof(int), st));
+    if (n <= 0) return 0;
+    zero_cols_kernel<<<(unsigned)(n < 4096 ? n : 4096), 256, 0, st>>>(n, B, ldb, d_zc, d_flags);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_permute(cudaStream_t st, int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+               const int64_t *d_perm_r, const int64_t *d_perm_c)
+{
+    if (rows <= 0 || cols <= 0) return 0;
+    dim3 grid((unsigned)((rows + 255) / 256 < 16 ? (rows + 255) / 256 : 16), (unsigned)(cols < 4096 ? cols : 4096));
+    permute_kernel<<<grid, 256, 0, st>>>(rows, cols, src, lds, dst, ldd, d_perm_r, d_perm_c);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_perm_matrix(cudaStream_t st, int64_t n, double *M, int64_t ld, const int64_t *d_perm)
+{
+    if (n <= 0) return 0;
+    dim3 grid((unsigned)((n + 255) / 256 < 16 ? (n + 255) / 256 : 16), (unsigned)(n < 4096 ? n : 4096));
+    perm_matrix_kernel<<<grid, 256, 0, st>>>(n, M, ld, d_perm);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
 
 int ht_cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 {
