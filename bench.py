@@ -191,7 +191,7 @@ def env_knobs():
 
 
 def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank, dist, want_e2e=False, A_h=None, B_h=None,
-                   comm=None):
+                   comm=None, flags=0):
     """Time `steps` full reductions of config `cfg` after `warmup` untimed ones (device
     events on the caller's stream, max over ranks).  Returns a dict of measurements."""
     if A_h is None:
@@ -204,7 +204,8 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
     def step():
         A.copy_(A0)  # pristine inputs each step (inputs larger than L2 at n >= 2048)
         B.copy_(B0)
-        return mg.reduce_mg(A, B, Q, Z, nb=nb, comm=comm, rank=rank, world=world, stream=stream.cuda_stream)
+        return mg.reduce_mg(A, B, Q, Z, nb=nb, comm=comm, rank=rank, world=world, stream=stream.cuda_stream,
+                            flags=flags)
 
     f_single = None
     for i in range(warmup):
@@ -212,7 +213,7 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
             # executed flops of the whole problem (F_exec of P = 1: replicated work is not credited twice)
             A.copy_(A0)
             B.copy_(B0)
-            f_single = ht.reduce_device(A, B, Q, Z, nb=nb, stream=stream.cuda_stream)["flops"]
+            f_single = ht.reduce_device(A, B, Q, Z, nb=nb, stream=stream.cuda_stream, flags=flags)["flops"]
         else:
             step()
     torch.cuda.synchronize()
@@ -387,6 +388,27 @@ def main():
                                  "premature_absorptions": rc0["premature_absorptions"],
                                  "desingularizations": rc0["desingularizations"]}
 
+    # the paper's Test Suite 4 (saddle-point pencils, Table 4) at n = 4000, with and
+    # without the sec. 3.5.1 preprocessing, and the QZ step-1 front end (general B) at this n
+    extra = {}
+    if args.also != "none":
+        As, Bs = ht_inputs.pencil("saddle", 4000, 40)
+        for tag, fl in (("suite4_saddle_n4000", 0), ("suite4_saddle_n4000_preprocessed", ht.HT_FLAG_DEFLATE_ZERO_COLUMNS)):
+            me = measure_config(torch, ht, mg, 0, 4000, 128, 2, 1, stream, world, rank, dist, A_h=As, B_h=Bs,
+                                comm=comm, flags=fl)
+            r0 = me["reps"][-1]
+            extra[tag] = {"n": 4000, "nb": 128, "ms_per_step": me["t_step"] * 1e3,
+                          "pct_columns_extra_ir": 100.0 * r0["ir_extra_columns"] / 4000,
+                          "pct_columns_failed_ir": 100.0 * r0["ir_failed_columns"] / 4000,
+                          "avg_ir_steps_per_column": r0["ir_steps_total"] / 4000,
+                          "premature_absorptions": r0["premature_absorptions"],
+                          "deflated_columns": r0["deflated_columns"], "t_front_s": r0["t_front"]}
+        Ag, Bg = ht_inputs.pencil("general", n, 41)
+        me = measure_config(torch, ht, mg, 0, n, nb, 1, 1, stream, world, rank, dist, A_h=Ag, B_h=Bg, comm=comm,
+                            flags=ht.HT_FLAG_GENERAL_B)
+        extra[f"general_b_n{n}"] = {"n": n, "nb": nb, "ms_per_step": me["t_step"] * 1e3,
+                                    "t_front_s": me["reps"][-1]["t_front"]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_oracle_sample(A_h, B_h, budget_s=15.0)
@@ -409,6 +431,7 @@ def main():
                 "roofline": roof, "roofline_panel": roof_panel, "roofline_e2e": roof_e2e, "wy_apply_phase": wy,
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(agg["launches"] * args.steps), "clocks": clk, "configs": others,
+                "front_ends": extra,
                 "detail": {"gflops_model": Fm / t_step / 1e9, "model_flops": Fm,
                            "executed_flops_per_step": Fx, "exec_over_model": Fx / Fm,
                            "t_panel_s": agg["t_panel"], "t_gemm_s": agg["t_gemm"],
