@@ -81,7 +81,7 @@ struct StepScalars {
     double S, tau, scal, beta, myrow;
 };
 template <int FNW>
-__device__ __noinline__ StepScalars step_scalars(const double *part, const double *rowc, int buf, int bw, int rmax,
+__device__ __forceinline__ StepScalars step_scalars(const double *part, const double *rowc, int buf, int bw, int rmax,
                                                  int rpt, int lane, int jj)
 {
     double pr[FNW];
@@ -385,81 +385,137 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                         val[e + 1] = t.y;
                     }
                 }
-                // the pivot column of the next step goes through shared memory: its owner lane
+                // The pivot column of the next step goes through shared memory: its owner lane
                 // stores the warp's rows, the warp reads them back as broadcasts (a 64-bit
-                // shuffle per element would cost two SHFL per row and lane)
-                // The warp owning the next diagonal row writes zeros at rows <= that row, so the
-                // dot products and updates below need no per-element masks (the index bound
-                // jn % RPT is a compile-time constant of the unrolled step).
-                auto put_pivot = [&](int jn, int bn) {
+                // shuffle per element would cost two SHFL per row and lane).  The warp owning
+                // the next diagonal row writes zeros at rows <= that row, so the dot products and
+                // updates need no per-element masks.
+                // Column steps run in groups of 8 (unrolled: static register indices) inside a
+                // rolled loop over the groups (the fully unrolled 32-step loop missed in the
+                // instruction cache).  The warp owning a group's 8 diagonal rows keeps them in
+                // val[0..7]: after the group they are final, go to Ps, and the warp shifts its
+                // rows up by 8 (zeros enter at the bottom).  A warp that has shifted sh rows holds
+                // row w0 + sh + e in val[e].
+                int sh = 0;
+                auto put_pivot = [&](int jn, int bn, int eon) {  // eon: local diagonal index, -1: not own
+#ifdef HT_FACTOR_SHFL_PIVOT
+                    return;
+#endif
                     if (lane == jn) {
                         double2 *dst = reinterpret_cast<double2 *>(pivs + bn * L::MAXP + w0);
-                        if (warp == (c0 + jn) / RPT) {
-                            const int eon = jn % RPT;  // (c0 % RPT == 0)
 #pragma unroll
-                            for (int e = 0; e < RPT; e += 2)
-                                dst[e / 2] = make_double2(e > eon ? val[e] : 0.0, e + 1 > eon ? val[e + 1] : 0.0);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < RPT; e += 2) dst[e / 2] = make_double2(val[e], val[e + 1]);
-                        }
+                        for (int e = 0; e < RPT; e += 2)
+                            dst[e / 2] = make_double2(e > eon ? val[e] : 0.0, e + 1 > eon ? val[e + 1] : 0.0);
                     }
                     __syncwarp();
                 };
-                put_pivot(0, 0);
+                put_pivot(0, 0, warp == c0 / RPT ? 0 : -1);
+#pragma unroll 1
+                for (int g = 0; 8 * g < nc; ++g) {
+                    const bool gown = warp == (c0 + 8 * g) / RPT;  // owns this group's diagonal rows
 #pragma unroll
-                for (int jj = 0; jj < PBW; ++jj) {
-                    if (jj >= nc) break;
-                    const int buf = jj & 1;
-                    const int dr = c0 + jj;           // diagonal row of column jj
-                    const int bw = dr / RPT;          // warp holding row dr
-                    const int eo = jj % RPT;          // its element index (c0 % RPT == 0 or RPT % 32 == 0)
-                    const int rmax = dense + dr;      // last row that can be nonzero in column jj
-                    const bool act = warp >= bw && warp * RPT <= rmax, own = warp == bw;
-                    double xr[RPT];
-                    if (act) {
-                        double sa[4] = {0.0, 0.0, 0.0, 0.0};
-                        const double2 *src = reinterpret_cast<const double2 *>(pivs + buf * L::MAXP + w0);
+                    for (int jj8 = 0; jj8 < 8; ++jj8) {
+                        const int jj = 8 * g + jj8;
+                        if (jj >= nc) break;
+                        const int buf = jj & 1;
+                        const int dr = c0 + jj;           // diagonal row of column jj
+                        const int bw = dr / RPT;          // warp holding row dr (in val[jj8])
+                        const int rmax = dense + dr;      // last row that can be nonzero in column jj
+                        const bool act = warp >= bw && warp * RPT <= rmax, own = gown;
+                        double xr[RPT];
+#ifdef HT_FACTOR_STEP_PROF
+                        const bool cpw = fprof && lane == 0 && warp == FNW - 1;
+                        long long ck0 = cpw ? clock64() : 0;
+#endif
+                        if (act) {
+                            double sa[4] = {0.0, 0.0, 0.0, 0.0};
+#ifdef HT_FACTOR_SHFL_PIVOT
+                            // pivot column jj by shuffles from its lane (own warp: rows <= dr read as 0)
 #pragma unroll
-                        for (int e = 0; e < RPT; e += 2) {
-                            const double2 t = src[e / 2];
-                            xr[e] = t.x;
-                            xr[e + 1] = t.y;
+                            for (int e = 0; e < RPT; ++e) {
+                                const double t = __shfl_sync(0xffffffffu, val[e], jj);
+                                xr[e] = (own && e <= jj8) ? 0.0 : t;
+                            }
+#else
+                            const double2 *src = reinterpret_cast<const double2 *>(pivs + buf * L::MAXP + w0);
+#pragma unroll
+                            for (int e = 0; e < RPT; e += 2) {
+                                const double2 t = src[e / 2];
+                                xr[e] = t.x;
+                                xr[e + 1] = t.y;
+                            }
+#endif
+#pragma unroll
+                            for (int e = 0; e < RPT; ++e) sa[e & 3] = fma(xr[e], val[e], sa[e & 3]);  // xr = 0 at rows <= dr
+                            part[(buf * FNW + warp) * PBW + lane] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+                            if (own) rowc[buf * PBW + lane] = val[jj8];
+                        }
+#ifdef HT_FACTOR_STEP_PROF
+                        long long ck1 = cpw ? clock64() + (int)(part[0] != part[0]) : 0;
+#endif
+                        __syncthreads();
+#ifdef HT_FACTOR_STEP_PROF
+                        long long ck2 = cpw ? clock64() : 0, ck3 = 0;
+#endif
+                        if (act) {
+                            const StepScalars sc = step_scalars<FNW>(part, rowc, buf, bw, rmax, RPT, lane, jj);
+#ifdef HT_FACTOR_STEP_PROF
+                            if (cpw) ck3 = clock64() + (int)(sc.tau != sc.tau);
+#endif
+                            const double S = sc.S, myrow = sc.myrow, tau = sc.tau, scal = sc.scal, beta = sc.beta;
+                            const double zc = myrow + scal * S;  // lanes < jj: v_lane^T v_jj = G_b(lane, jj)
+                            const double wj = tau * zc;
+                            if (own && lane < jj) Xs[jj * LDX + lane] = zc;
+                            // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
+                            const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
+#pragma unroll
+                            for (int e = 0; e < RPT; ++e) val[e] = fma(mx, xr[e], val[e]);  // rows <= dr: xr = 0
+                            if (own) {
+                                val[jj8] = lane > jj ? val[jj8] - wj : (lane == jj ? beta : val[jj8]);
+                                if (lane == jj) taus[jj] = tau;
+                            }
+                        }
+#ifdef HT_FACTOR_STEP_PROF
+                        long long ck4 = cpw ? clock64() + (int)(val[RPT - 1] != val[RPT - 1]) : 0;
+#endif
+                        // next step's pivot slices inside the group (a warp may become active)
+                        if (jj8 < 7 && jj + 1 < nc && warp >= (dr + 1) / RPT && warp * RPT <= rmax + 1)
+                            put_pivot(jj + 1, buf ^ 1, gown ? jj8 + 1 : -1);
+#ifdef HT_FACTOR_STEP_PROF
+                        if (cpw) {
+                            const long long ck5 = clock64();
+                            atomicAdd(&fprof[12], (unsigned long long)(ck1 - ck0));
+                            atomicAdd(&fprof[13], (unsigned long long)(ck2 - ck1));
+                            atomicAdd(&fprof[14], (unsigned long long)(ck3 - ck2));
+                            atomicAdd(&fprof[15], (unsigned long long)(ck4 - ck3));
+                            atomicAdd(&fprof[16], (unsigned long long)(ck5 - ck4));
+                        }
+#endif
+                    }
+                    if (gown) {  // this group's diagonal rows are final: to Ps, shift up by 8
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int r = w0 + sh + e;
+                            Ps[lane * L::LDP + r] = (r < p && lane < nc) ? val[e] : 0.0;
                         }
 #pragma unroll
-                        for (int e = 0; e < RPT; ++e) sa[e & 3] = fma(xr[e], val[e], sa[e & 3]);  // xr = 0 at rows <= dr
-                        part[(buf * FNW + warp) * PBW + lane] = (sa[0] + sa[1]) + (sa[2] + sa[3]);
-                        if (own) rowc[buf * PBW + lane] = val[eo];
-                    }
-                    __syncthreads();
-                    if (act) {
-                        const StepScalars sc = step_scalars<FNW>(part, rowc, buf, bw, rmax, RPT, lane, jj);
-                        const double S = sc.S, myrow = sc.myrow, tau = sc.tau, scal = sc.scal, beta = sc.beta;
-                        const double zc = myrow + scal * S;  // lanes < jj: v_lane^T v_jj = G_b(lane, jj)
-                        const double wj = tau * zc;
-                        if (own && lane < jj) Xs[jj * LDX + lane] = zc;
-                        // rows > dr: column jj -> scal * x (its tail of v); later columns -= w_j v
-                        const double mx = lane > jj ? -wj * scal : (lane == jj ? scal - 1.0 : 0.0);
+                        for (int e = 0; e + 8 < RPT; ++e) val[e] = val[e + 8];
 #pragma unroll
-                        for (int e = 0; e < RPT; ++e) val[e] = fma(mx, xr[e], val[e]);  // rows <= dr: xr = 0
-                        if (own) {
-                            val[eo] = lane > jj ? val[eo] - wj : (lane == jj ? beta : val[eo]);
-                            if (lane == jj) taus[jj] = tau;
-                        }
+                        for (int e = RPT - 8; e < RPT; ++e) val[e] = 0.0;
+                        sh += 8;
                     }
-                    // next step's pivot slices (a warp may become active at the next step)
-                    if (jj + 1 < nc && warp >= (dr + 1) / RPT && warp * RPT <= rmax + 1) put_pivot(jj + 1, buf ^ 1);
+                    const int jn = 8 * (g + 1);  // first column of the next group
+                    if (jn < nc && warp >= (c0 + jn) / RPT && warp * RPT <= dense + c0 + jn)
+                        put_pivot(jn, jn & 1, warp == (c0 + jn) / RPT ? 0 : -1);
                 }
                 FPROF(2);
                 __syncthreads();
-                {   // the raw panel once; R (view) and V (natural order) are both stored from it
-                    double2 *dst = reinterpret_cast<double2 *>(Ps + lane * L::LDP + w0);
+                {   // the rows still in registers (row w0 + sh + e in val[e]); R (view) and V (natural
+                    // order) are both stored from Ps
 #pragma unroll
-                    for (int e = 0; e < RPT; e += 2) {
-                        const int r = w0 + e;
-                        const double a0 = (r < p && lane < nc) ? val[e] : 0.0;
-                        const double a1 = (r + 1 < p && lane < nc) ? val[e + 1] : 0.0;
-                        dst[e / 2] = make_double2(a0, a1);
+                    for (int e = 0; e < RPT; ++e) {
+                        const int r = w0 + sh + e;
+                        if (e < RPT - sh) Ps[lane * L::LDP + r] = (r < p && lane < nc) ? val[e] : 0.0;
                     }
                 }
                 __syncthreads();

@@ -2,6 +2,9 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_1710_08538_b200/csrc
 //        factor_bench.cu -o factor_bench
 // Usage: ./factor_bench p q [reps] [rev] [transposed]
+#ifndef HT_NO_STEP_PROF
+#define HT_FACTOR_STEP_PROF 1
+#endif
 #include "../../paper_1710_08538_b200/csrc/ht_factor.cu"
 #include <cstdio>
 #include <cstdlib>
