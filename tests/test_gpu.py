@@ -376,7 +376,14 @@ def _golden_gate(A, B, dA, dB, cfg):
         return None
     g = np.load(path[0])
     sha = lambda M: hashlib.sha256(np.asfortranarray(M).tobytes(order="F")).hexdigest()
-    assert str(g["sha_A"]) == sha(A) and str(g["sha_B"]) == sha(B), "golden samples are for other inputs"
+    # A (plain draws) must be bitwise the same; B = R of numpy's QR (LAPACK/OpenBLAS) may differ
+    # in the last bits between the box that wrote the samples and this one (CPU-specific kernels):
+    # then it must agree in ||B||_F to 1e-13 -- a u-level input perturbation, which moves |H|, |T|
+    # of a pencil with nonsingular B by ~1e-12, far inside the 1e-9 gate
+    assert str(g["sha_A"]) == sha(A), "golden samples are for other inputs"
+    b_exact = str(g["sha_B"]) == sha(B)
+    if not b_exact:
+        assert abs(np.linalg.norm(B) - float(g["fro_B"])) <= 1e-13 * float(g["fro_B"]), "B differs beyond rounding"
     n = A.shape[0]
     out = {}
     for name, t, rows, cols, ref, nrm, region in (
@@ -387,6 +394,7 @@ def _golden_gate(A, B, dA, dB, cfg):
         d = got - ref
         out[name] = (float(np.max(np.abs(d))) / nrm, float(np.sqrt(region / d.size) * np.linalg.norm(d)) / nrm)
     out["oracle"] = str(g["oracle"])
+    out["b_sha_match"] = b_exact
     return out
 
 
@@ -420,9 +428,10 @@ def test_full_size_config_properties(cfg):
         record(f"fullsize_cfg{cfg}", {"cfg": cfg, "n": n, "nb": nb, "oracle": gate["oracle"],
                                       "absH_max_rel": gate["H"][0], "absH_fro_est_rel": gate["H"][1],
                                       "absT_max_rel": gate["T"][0], "absT_fro_est_rel": gate["T"][1],
-                                      "flops_exec_over_model": ratio})
+                                      "b_sha_match": gate["b_sha_match"], "flops_exec_over_model": ratio,
+                                      "backward": {"resA": ra, "resB": rb, "orthQ": oq, "orthZ": oz}})
         lim = PARITY if cfg != 4 else CFG4_G_GATE
-        assert max(gate["H"] + gate["T"]) <= lim, gate
+        assert max(list(gate["H"]) + list(gate["T"])) <= lim, gate
     elif cfg == 3:
         pytest.fail("tests/golden/fullsize_cfg3_T.npz missing (scripts/make_fullsize_golden.py --config 3)")
     # Q e1 = Z e1 = e1 (every transform acts on rows/columns >= 2)
