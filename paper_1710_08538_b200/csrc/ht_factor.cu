@@ -519,6 +519,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     }
                 }
                 __syncthreads();
+#ifdef HT_FACTOR_STEP_PROF
+                FPROF(28);
+#endif
                 if (rs == 1 || rs == -1) {  // R: contiguous along rows: lanes over rows
                     for (int j = warp; j < nc; j += FNW)
                         for (int r = lane; r < p; r += 32)
@@ -527,6 +530,9 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                     for (int r = warp; r < p; r += FNW)
                         if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = (r <= c0 + lane) ? Ps[lane * L::LDP + r] : 0.0;
                 }
+#ifdef HT_FACTOR_STEP_PROF
+                FPROF(29);
+#endif
                 for (int j = warp; j < nc; j += FNW) {  // V: unit diagonal, zeros above (and for tau = 0)
                     const int col = c0 + j;
                     const bool t0 = taus[j] == 0.0;

@@ -59,6 +59,7 @@ int main(int argc, char **argv)
     printf("column step cycles/col: warp0 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]  warp15 [A %.0f bar1 %.0f B %.0f bar2 %.0f C %.0f]\n",
            hp[12] / (double)q, hp[13] / (double)q, hp[14] / (double)q, hp[15] / (double)q, hp[16] / (double)q,
            hp[17] / (double)q, hp[18] / (double)q, hp[19] / (double)q, hp[20] / (double)q, hp[21] / (double)q);
+    printf("write split (us): stage %.1f R %.1f V+tau %.1f\n", hp[28] * 1e-3, hp[29] * 1e-3, hp[4] * 1e-3);
     printf("T recurrence: %.0f cycles per panel\n", (double)(long long)hp[27] / ((q + 31) / 32));
     printf("vt_times_panel: %llu calls, stage %.0f cycles/call, dmma %.0f cycles/call\n", hp[26], hp[24] / (double)(hp[26] ? hp[26] : 1), hp[25] / (double)(hp[26] ? hp[26] : 1));
     printf("p=%d q=%d rev=%d: best %.1f us | phases(us): load %.1f left[X %.1f TX %.1f upd %.1f] leafsteps %.1f leafupd %.1f write %.1f G %.1f T %.1f offT %.1f zero %.1f\n",
