@@ -33,6 +33,15 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool ok)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 struct ChainParams {
     ChainMat m[3];
     int nm;
@@ -40,6 +49,17 @@ struct ChainParams {
     const ChainWin *wins;
     int nw;
 };
+
+#ifdef CHAIN_PROF
+// development instrumentation (scripts/micro/chain_prof.py): per-CTA cycles in
+// [0] first-window load, [1] k-chunk loop, [2] whole window product incl. epilogue, [3] transition, [4] barrier waits in the loop
+__device__ unsigned long long g_chain_prof[256][8];
+#define CPROF_T(v) const long long v = clock64()
+#define CPROF_ADD(i, a, b) if (tid == 0) g_chain_prof[blockIdx.x][i] += (unsigned long long)((b) - (a))
+#else
+#define CPROF_T(v)
+#define CPROF_ADD(i, a, b)
+#endif
 
 template <int KC>
 __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_constant__ ChainParams P)
@@ -52,6 +72,22 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     double *Xs = csm;               // [cap][ldh]  ring of slab columns
     double *Qs = Xs + (size_t)cap * ldh;  // [2][kc][ldq]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+
+    // Qhat chunks arrive by bulk copy (cp.async.bulk, one per Qhat row, completion counted on
+    // the buffer's mbarrier) when the window's rows are 16-byte aligned; else by 8-byte cp.async
+    __shared__ __align__(8) unsigned long long qbar[2];
+    const unsigned qb0 = (unsigned)__cvta_generic_to_shared(&qbar[0]);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(qb0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(qb0 + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // rows k >= p of a ragged last chunk are not rewritten: they meet zero slab columns, so
+    // they must hold finite values -- zeros at start, earlier Qhat rows later
+    for (int i = tid; i < 2 * KC * (cap + CHAIN_PAD); i += CNT) Qs[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    unsigned qpar = 0;  // bit b: parity of the next wait on Qhat buffer b
 
     // slab tasks over all matrices; a capped grid loops over them (persistent style), so that
     // concurrent streams keep SMs free for the factorization chain
@@ -77,17 +113,47 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     auto slot = [&](int64_t c) -> int { return (int)c & capm; };
     // move columns [c_lo, c_hi) between HBM and the ring (coalesced along the contiguous
     // direction: rows of a column for right applies, columns of a row for left applies)
+    // (all loads of a thread are issued before its shared-memory stores: the entering columns of
+    // a transition are ~16 independent HBM loads per thread, one latency instead of 16)
     auto load_cols = [&](int64_t c_lo, int64_t c_hi) {
         const int nc = (int)(c_hi - c_lo);
         if (nc <= 0) return;
+        const int total = nc * h;
+        constexpr int LB = 16;
+        for (int base = 0; base < total; base += CNT * LB) {
+            double v[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int idx = base + tid + q * CNT;
+                v[q] = 0.0;
+                if (idx < total) {
+                    // right applies: rows fastest (a column is contiguous); left: columns fastest
+                    const int s = M.left ? idx / nc : idx % h, c = M.left ? idx % nc : idx / h;
+                    if (s < hs) v[q] = *gaddr(s, c_lo + c);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int idx = base + tid + q * CNT;
+                if (idx < total) {
+                    const int s = M.left ? idx / nc : idx % h, c = M.left ? idx % nc : idx / h;
+                    Xs[slot(c_lo + c) * ldh + s] = v[q];
+                }
+            }
+        }
+    };
+    // the same movement issued as cp.async (no register staging; completes behind later work);
+    // a handful of columns per call, so plain warp/lane loops (no division by runtime sizes)
+    auto load_cols_async = [&](int64_t c_lo, int64_t c_hi) {
+        const int nc = (int)(c_hi - c_lo);
         if (M.left) {
             for (int s = warp; s < h; s += CNT / 32)
                 for (int c = lane; c < nc; c += 32)
-                    Xs[slot(c_lo + c) * ldh + s] = (s < hs) ? *gaddr(s, c_lo + c) : 0.0;
+                    cp_async8(&Xs[slot(c_lo + c) * ldh + s], s < hs ? gaddr(s, c_lo + c) : M.X, s < hs);
         } else {
             for (int c = warp; c < nc; c += CNT / 32)
                 for (int s = lane; s < h; s += 32)
-                    Xs[slot(c_lo + c) * ldh + s] = (s < hs) ? *gaddr(s, c_lo + c) : 0.0;
+                    cp_async8(&Xs[slot(c_lo + c) * ldh + s], s < hs ? gaddr(s, c_lo + c) : M.X, s < hs);
         }
     };
     auto store_cols = [&](int64_t c_lo, int64_t c_hi) {
@@ -109,15 +175,39 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     };
 
     {
+        CPROF_T(t0);
         const ChainWin w0 = P.wins[0];
         load_cols(w0.o, (int64_t)w0.o + w0.p);
         zero_pad(w0.o, w0.p);
+        CPROF_T(t1);
+        CPROF_ADD(0, t0, t1);
     }
     for (int wi = 0; wi < P.nw; ++wi) {
         const ChainWin W = P.wins[wi];
         const int p = W.p, pp = (p + 31) & ~31;
         const int64_t lo = W.lo[mi], hi = W.hi[mi];
         const bool active = (s0 < hi) && (s0 + hs > lo) && p > 0;
+        const bool last = wi + 1 == P.nw;
+        const int64_t a0 = W.o, a1 = (int64_t)W.o + W.p;
+        int64_t b0 = a1, b1 = a1;
+        if (!last) {
+            const ChainWin N = P.wins[wi + 1];
+            b0 = N.o;
+            b1 = (int64_t)N.o + N.p;
+        }
+        // Overlapped transition (forward chains, slab entirely inside the window's row range):
+        // the leaving columns [a0, b0) are written to HBM straight from the accumulators, and
+        // the entering columns are prefetched with cp.async into the ring slots of leaving
+        // columns as soon as the k-loop has consumed them (slot(c) = slot(c - cap)), so the
+        // slab's HBM traffic streams behind the DMMA work instead of stalling between windows.
+        // Entering columns that overlap this window's zero padding [a1, a0 + pp) wait for the
+        // transition (the padding must read as zeros until the window is done).
+        const bool inside = active && s0 >= lo && s0 + hs <= hi;
+        const bool early = inside && !last && b0 >= a0 && b1 >= a1 && b1 - b0 <= cap;
+        const int direct = !inside ? 0 : last ? p : early ? (int)(b0 - a0 < p ? b0 - a0 : p) : 0;
+        const int64_t e_beg = a0 + pp > a1 ? a0 + pp : a1;  // first early-prefetchable entering column
+        int64_t e_cur = e_beg;
+        CPROF_T(tw0);
         __syncthreads();
         if (active) {
             const int nwr = h / 32, nwc = pp / 32;
@@ -128,37 +218,67 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-            // k-chunk of Qhat (row-major, Qhat(k, c) at Qw[k p + c]): lanes run along c for
-            // both the global read and the shared store (conflict-free)
-            const int lcap = __ffs(cap) - 1;            // cap is a power of two
-            const int per = (kc * cap) >> 9;            // staged elements per thread (<= 8; CNT = 512)
-            double rq[8];
-            auto fetch = [&](int k0) {
+            // k-chunk of Qhat (row-major, Qhat(k, c) at Qw[k p + c]) staged by cp.async into the
+            // other buffer while this chunk computes; lanes run along c (coalesced, conflict-free)
+            const int lcap = __ffs(cap) - 1;  // cap is a power of two
+            const int per = (kc * cap) >> 9;  // staged elements per thread (<= 8; CNT = 512)
+            const bool qbulk = (p % 2) == 0 && ((uintptr_t)W.Qw & 15) == 0;
+            auto fetch = [&](int k0, int buf) {
+                double *qd = Qs + (size_t)buf * kc * ldq;
+                if (qbulk) {
+                    if (tid == 0) {
+                        const int nr = p - k0 < kc ? p - k0 : kc;
+                        const unsigned mb = qb0 + 8 * buf;
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                                     "r"((unsigned)(nr > 0 ? nr * p * 8 : 0)) : "memory");
+                        for (int r = 0; r < nr; ++r)
+                            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                                         ::"r"((unsigned)__cvta_generic_to_shared(qd + r * ldq)),
+                                         "l"(W.Qw + (size_t)(k0 + r) * p), "r"(p * 8), "r"(mb) : "memory");
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     if (e >= per) break;
                     const int idx = tid + e * CNT;
                     const int kr = idx >> lcap, c = idx & (cap - 1);
-                    double v = 0.0;
-                    if (c < p && k0 + kr < p) v = W.Qw[(size_t)(k0 + kr) * p + c];
-                    rq[e] = v;
+                    const bool ok = c < p && k0 + kr < p;
+                    cp_async8(qd + kr * ldq + c, ok ? W.Qw + (size_t)(k0 + kr) * p + c : W.Qw, ok);
                 }
+                cp_async_commit();
             };
-            auto put = [&](int buf) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if (e >= per) break;
-                    const int idx = tid + e * CNT;
-                    Qs[(size_t)buf * kc * ldq + (idx >> lcap) * ldq + (idx & (cap - 1))] = rq[e];
+            // wait for the chunk staged in `buf` (bulk: mbarrier phase; else cp.async groups)
+            auto qwait = [&](int buf, bool pending_enter) {
+                if (qbulk) {
+                    const unsigned mb = qb0 + 8 * buf, par = (qpar >> buf) & 1u;
+                    unsigned done = 0;
+                    while (!done)
+                        asm volatile("{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+                                     : "=r"(done) : "r"(mb), "r"(par) : "memory");
+                    qpar ^= 1u << buf;
                 }
+                // entering-column groups: the newest may stay in flight
+                if (pending_enter) cp_async_wait<1>(); else cp_async_wait<0>();
             };
             const int nk = pp / kc + (pp % kc ? 1 : 0);
-            fetch(0);
-            put(0);
+            CPROF_T(tl0);
+            fetch(0, 0);
+            qwait(0, false);
             __syncthreads();
             for (int kt = 0; kt < nk; ++kt) {
                 const int buf = kt & 1;
-                if (kt + 1 < nk) fetch((kt + 1) * kc);
+                if (kt + 1 < nk) fetch((kt + 1) * kc, buf ^ 1);
+                if (early) {  // entering columns whose ring slots the k-loop has released
+                    int64_t lim = a0 + (int64_t)kt * kc + cap;
+                    if (lim > b1) lim = b1;
+                    if (lim > e_cur) {
+                        load_cols_async(e_cur, lim);
+                        e_cur = lim;
+                    }
+                    cp_async_commit();
+                }
                 if (wact) {
                     const double *qb = Qs + (size_t)buf * kc * ldq;
 #pragma unroll
@@ -176,10 +296,18 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                             for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
                     }
                 }
-                if (kt + 1 < nk) put(buf ^ 1);
+                // the next Qhat chunk has landed; this chunk's entering columns may still fly
+                if (kt + 1 < nk) qwait(buf ^ 1, early);
+                else if (early) cp_async_wait<1>();
+                CPROF_T(tb0);
                 __syncthreads();
+                CPROF_T(tb1);
+                CPROF_ADD(4, tb0, tb1);
             }
-            // epilogue: slab(s, o + c) <- acc for s in [lo, hi), c < p
+            CPROF_T(tl1);
+            CPROF_ADD(1, tl0, tl1);
+            // epilogue: slab(s, o + c) <- acc for s in [lo, hi), c < p; the first `direct`
+            // columns leave the chain here and go straight to HBM
             if (wact) {
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
@@ -190,28 +318,40 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                             const int s = wr * 32 + 8 * a + g;
                             const int c = wc * 32 + 8 * b + 2 * t4 + hh;
                             const int64_t sg = s0 + s;
-                            if (c < p && sg >= lo && sg < hi && s < hs)
-                                Xs[slot((int64_t)W.o + c) * ldh + s] = acc[a][b][hh];
+                            if (c < p && sg >= lo && sg < hi && s < hs) {
+                                if (c < direct)
+                                    *gaddr(s, (int64_t)W.o + c) = acc[a][b][hh];
+                                else
+                                    Xs[slot((int64_t)W.o + c) * ldh + s] = acc[a][b][hh];
+                            }
                         }
             }
         }
+        cp_async_wait<0>();
         __syncthreads();
+        CPROF_T(tt0);
+        CPROF_ADD(2, tw0, tt0);
         // transition: flush columns leaving the chain, load columns entering it
-        const int64_t a0 = W.o, a1 = (int64_t)W.o + W.p;
-        if (wi + 1 < P.nw) {
-            const ChainWin N = P.wins[wi + 1];
-            const int64_t b0 = N.o, b1 = (int64_t)N.o + N.p;
+        if (!last) {
             // leaving: [a0, a1) \ [b0, b1); entering: [b0, b1) \ [a0, a1)  (monotone chains)
-            store_cols(a0, a1 < b0 ? a1 : b0);
+            store_cols(a0 + direct, a1 < b0 ? a1 : b0);
             store_cols(a0 > b1 ? a0 : b1, a1);
             __syncthreads();
-            load_cols(b0, b1 < a0 ? b1 : a0);
-            load_cols(b0 > a1 ? b0 : a1, b1);
+            if (early) {
+                load_cols(a1, e_beg < b1 ? e_beg : b1);  // entering columns under the zero padding
+                load_cols(e_cur, b1);
+            } else {
+                load_cols(b0, b1 < a0 ? b1 : a0);
+                load_cols(b0 > a1 ? b0 : a1, b1);
+            }
             __syncthreads();
+            const ChainWin N = P.wins[wi + 1];
             zero_pad(N.o, N.p);
         } else {
-            store_cols(a0, a1);
+            store_cols(a0 + direct, a1);
         }
+        CPROF_T(tt1);
+        CPROF_ADD(3, tt0, tt1);
     }
     }  // task loop
 }
@@ -238,11 +378,6 @@ struct BandDesc {
 };
 constexpr int BPW = 32;  // panel width of the factorization (ht_factor.cu PBW)
 
-__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool ok)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
-}
 
 // double-buffered V_b/T_b staging fits in shared memory for windows of up to 256 rows
 __host__ __device__ __forceinline__ bool band_double_buffer(int p8) { return p8 <= 256; }
@@ -522,3 +657,16 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
+
+#ifdef CHAIN_PROF
+extern "C" __attribute__((visibility("default"))) int ht_chain_prof_read(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_chain_prof, sizeof(g_chain_prof));
+    if (reset) {
+        static unsigned long long z[256][8];
+        cudaMemcpyToSymbol(g_chain_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
