@@ -345,6 +345,23 @@ def main():
                               "seconds": sec, "flops": fl}
     except Exception as exc:  # measurement hook only; never affects the timed result
         roof["standalone"] = {"error": str(exc)}
+    # DRAM traffic of one live launch of the same kernel at this config, from the committed
+    # `ncu --set full` capture (profiles/r02/ncu_chain.json, scripts/gpu_ncu_chain.sh)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_chain.json")) as f:
+            nj = json.load(f)
+        live = nj.get("chain_cfg3_live") if cfg == 3 else None
+        if live:
+            roof["traffic"] = live["dram_read_bytes"] + live["dram_write_bytes"]
+            roof["traffic_launch"] = {"flops": live["fp64_tensor_flops"], "duration_s_under_ncu": live["duration_s"],
+                                      "grid": live["grid"], "dmma_active_pct": live["dmma_active_pct"],
+                                      "source": "profiles/r02/ncu_chain.txt (launch 301 of the cfg3 reduction)"}
+        st = nj.get("chain_cfg3_standalone")
+        if st and "standalone" in roof and "error" not in roof["standalone"]:
+            roof["standalone"]["traffic"] = st["dram_read_bytes"] + st["dram_write_bytes"]
+            roof["standalone"]["algorithmic_bytes"] = 2.0 * n * ((nwin - 1) * nb + 2 * nb) * 8
+    except (OSError, ValueError, KeyError):
+        pass
     panel_ach = agg["panel_bytes"] / max(agg["t_panel"], 1e-12) / 1e9
     roof_panel = {"bound": "hbm", "kernel": "panel_kernel (persistent panel)", "achieved": panel_ach, "peak": hbm,
                   "unit": "GB/s", "frac": panel_ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}

@@ -464,7 +464,7 @@ struct Run {
         if (!ws.empty()) {
             const Win &b = ws.back();
             x.ov = b.ov + (size_t)b.p * b.q;
-            x.oq = b.oq + (size_t)b.p * b.p;
+            x.oq = b.oq + (((size_t)b.p * b.p + 1) & ~(size_t)1);  // 16-byte aligned Qhat (bulk-copy staging)
             x.og = b.og + (size_t)b.q * b.q;
             x.ot = b.ot + (size_t)b.q;
         }
