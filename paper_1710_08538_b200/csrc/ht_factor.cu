@@ -58,8 +58,8 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
 // Householder scalars of x = [alpha; tail], ||tail||^2 = ss > 0 (dlarfg convention, R-Z1):
 // beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta = 1 + |alpha| / ||x||,
 // scal = 1 / (alpha - beta) = sign(alpha) / (||x|| tau)  (so that v = [1; tail * scal]).
-// One rsqrt and one reciprocal of tau in [1, 2] (float seed + two Newton steps, no range
-// checks needed): a short dependency chain on the column step's critical path.
+// One rsqrt and one division by tau in [1, 2]: a short dependency chain on the column
+// step's critical path.
 __device__ __forceinline__ void house_scalars(double alpha, double ss, double &beta, double &tau, double &scal)
 {
     const double N = fma(alpha, alpha, ss);
@@ -67,10 +67,7 @@ __device__ __forceinline__ void house_scalars(double alpha, double ss, double &b
     const double nrm = N * r;
     beta = alpha >= 0.0 ? -nrm : nrm;
     tau = fma(fabs(alpha), r, 1.0);
-    double it = (double)(1.0f / (float)tau);  // tau in [1, 2]
-    it = it * fma(-tau, it, 2.0);
-    it = it * fma(-tau, it, 2.0);
-    const double sc = r * it;
+    const double sc = r / tau;  // (measured: one IEEE division is ~40 cycles shorter than a float seed + 2 Newton steps)
     scal = alpha >= 0.0 ? sc : -sc;
 }
 
@@ -522,22 +519,43 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
 #ifdef HT_FACTOR_STEP_PROF
                 FPROF(28);
 #endif
-                if (rs == 1 || rs == -1) {  // R: contiguous along rows: lanes over rows
-                    for (int j = warp; j < nc; j += FNW)
-                        for (int r = lane; r < p; r += 32)
-                            d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = (r <= c0 + j) ? Ps[j * L::LDP + r] : 0.0;
-                } else {                     // R: contiguous along columns: lanes over columns
-                    for (int r = warp; r < p; r += FNW)
-                        if (lane < nc) d.W[(int64_t)r * rs + (int64_t)(c0 + lane) * cs] = (r <= c0 + lane) ? Ps[lane * L::LDP + r] : 0.0;
+                // R and V leave through Ps; every thread reads all its elements before its first
+                // global store (the shared-memory latency is paid once per batch, not per element)
+                constexpr int SB = 16, NPASS = (PBW * L::MAXP / FNT + SB - 1) / SB;  // elements per thread and pass
+                const bool rowfast = rs == 1 || rs == -1;
+                // R: rowfast -> lanes over rows (contiguous), else lanes over columns
+#pragma unroll 1
+                for (int ps = 0; ps < NPASS; ++ps) {
+                    double t[SB];
+#pragma unroll
+                    for (int e = 0; e < SB; ++e) {
+                        const int idx = tid + (ps * SB + e) * FNT;
+                        const int j = rowfast ? idx / L::MAXP : idx % PBW, r = rowfast ? idx % L::MAXP : idx / PBW;
+                        t[e] = (r <= c0 + j && j < PBW && r < L::MAXP) ? Ps[j * L::LDP + r] : 0.0;
+                    }
+#pragma unroll
+                    for (int e = 0; e < SB; ++e) {
+                        const int idx = tid + (ps * SB + e) * FNT;
+                        const int j = rowfast ? idx / L::MAXP : idx % PBW, r = rowfast ? idx % L::MAXP : idx / PBW;
+                        if (j < nc && r < p) d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] = t[e];
+                    }
                 }
 #ifdef HT_FACTOR_STEP_PROF
                 FPROF(29);
 #endif
-                for (int j = warp; j < nc; j += FNW) {  // V: unit diagonal, zeros above (and for tau = 0)
-                    const int col = c0 + j;
-                    const bool t0 = taus[j] == 0.0;
-                    for (int r = lane; r < p; r += 32)
-                        d.V[(int64_t)col * d.ldv + nat(r)] = (r < col) ? 0.0 : (r == col ? 1.0 : (t0 ? 0.0 : Ps[j * L::LDP + r]));
+#pragma unroll 1
+                for (int ps = 0; ps < NPASS; ++ps) {  // V: unit diagonal, zeros above (and for tau = 0)
+                    double t[SB];
+#pragma unroll
+                    for (int e = 0; e < SB; ++e) {
+                        const int idx = tid + (ps * SB + e) * FNT, j = idx / L::MAXP, r = idx % L::MAXP, col = c0 + j;
+                        t[e] = (r < col || j >= PBW) ? 0.0 : (r == col ? 1.0 : (taus[j] == 0.0 ? 0.0 : Ps[j * L::LDP + r]));
+                    }
+#pragma unroll
+                    for (int e = 0; e < SB; ++e) {
+                        const int idx = tid + (ps * SB + e) * FNT, j = idx / L::MAXP, r = idx % L::MAXP;
+                        if (j < nc && r < p) d.V[(int64_t)(c0 + j) * d.ldv + nat(r)] = t[e];
+                    }
                 }
             } else {
             // ---- the panel in registers: val[l][e] = P(rw0 + e, 8l + c8) ----
@@ -820,7 +838,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
             __syncthreads();
             FPROF(5);
         }
-        __threadfence();
+        // the next window of this launch may read what this one wrote (its R): a block barrier
+        // orders global writes and reads inside the CTA; later kernels follow in stream order
         __syncthreads();
     }
 }

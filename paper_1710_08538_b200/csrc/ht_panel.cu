@@ -301,7 +301,7 @@ __device__ __forceinline__ double ll_get(const unsigned long long *w, unsigned e
         lo = ld_volatile64(w);
         hi = ld_volatile64(w + 1);
         if ((unsigned)(lo >> 32) == epoch && (unsigned)(hi >> 32) == epoch) break;
-        __nanosleep(64);  // back off: the pollers of all waiting CTAs share L2 with the chain
+        __nanosleep(64);  // back off: the pollers of all waiting CTAs share L2 with the chain (0/16/256 ns: same solve time)
     }
     return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
