@@ -236,14 +236,21 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
         elapsed = float(t.item())
     out = {"elapsed": elapsed, "t_step": elapsed / steps, "reps": reps, "f_single": f_single}
     if want_e2e:
-        # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host
+        # end to end through the public API: host pencil -> device -> reduction -> H, T, Q, Z on the host.
+        # The pencil and the result buffers live in pinned host memory (allocated once, outside
+        # the timed region); each timed call copies A, B in and H, T, Q, Z out (ht_reduce_host).
         ts = []
+        if world == 1:
+            Ap, Bp = ht.pinned_empty(n), ht.pinned_empty(n)
+            Ap[:], Bp[:] = A_h, B_h
+            outs = tuple(ht.pinned_empty(n) for _ in range(4))
+            ht.ht_reduce(Ap, Bp, nb=nb, out=outs)  # warm-up (device staging, pinned pages)
         for _ in range(max(1, min(steps, 2))):
             if dist:
                 dist.barrier()
             t0 = time.time()
             if world == 1:
-                ht.ht_reduce(A_h, B_h, nb=nb)
+                ht.ht_reduce(Ap, Bp, nb=nb, out=outs)
             else:
                 hA = torch.from_numpy(np.ascontiguousarray(A_h.T)).pin_memory()
                 hB = torch.from_numpy(np.ascontiguousarray(B_h.T)).pin_memory()
@@ -379,7 +386,9 @@ def main():
     if "e2e_s" in m:
         te = m["e2e_s"]
         e2e = {"value": Fx / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
-               "d2h_bytes_per_step": 4 * n * n * 8, "s_per_step": te}
+               "d2h_bytes_per_step": 4 * n * n * 8, "s_per_step": te,
+               "path": "ht_reduce_host (C-ABI) from pinned host buffers: H2D of A, B + reduction + D2H of H, T, Q, Z"
+               if world == 1 else "H2D from pinned host memory + ht_reduce_mg + D2H of A, B, Q, Z"}
 
     # the other BASELINE.json configs, same binary, fewer steps (parity-tested sizes)
     others = {}

@@ -163,9 +163,25 @@ typedef struct {
 /*
  * North-star entry point (host memory).  A, B, Q, Z are n x n, column-major
  * with leading dimension n.  Synchronous: copies to the device, reduces,
- * copies back.  Returns HT_OK or an error code above.
+ * copies back.  Returns HT_OK or an error code above.  Same as
+ * ht_reduce_host(n, A, B, A, B, Q, Z, wantq, wantz, nb).
  */
 HT_API int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb);
+
+/*
+ * Out-of-place host entry point (H = Q^T A Z, T = Q^T B Z).
+ *   A, B   (in)  n x n column-major pencil, ld n; read only (not modified unless aliased).
+ *   H, T   (out) n x n, ld n: the Hessenberg and triangular results; H may alias A and
+ *                T may alias B (that is ht_reduce).
+ *   Q, Z   (out) n x n, ld n, if wantq / wantz (else ignored, may be NULL).
+ * Device staging buffers are kept per device between calls (freed by
+ * ht_release_workspace).  Host buffers allocated as pinned memory (cudaHostAlloc /
+ * cudaHostRegister) are copied by DMA on the library's stream at full link rate; pageable
+ * buffers work too, at the driver's staged-copy rate.  Synchronous.  Errors as ht_reduce
+ * (HT_EARG_* for NULL pointers or n < 0; on error H, T, Q, Z are unspecified).
+ */
+HT_API int ht_reduce_host(int64_t n, const double *A, const double *B, double *H, double *T, double *Q, double *Z,
+                          int wantq, int wantz, int64_t nb);
 
 /*
  * Device-memory entry point.  dA, dB, dQ, dZ are device pointers with leading

@@ -28,7 +28,7 @@ HT_FLAG_DEFLATE_ZERO_COLUMNS = 2
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
           -6: "HT_EARG_WANTQ", -7: "HT_EARG_WANTZ", -8: "HT_EARG_NB", -9: "HT_EARG_OPT",
           1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC", 5: "HT_ENCCL"}
-EXPORTS = ("ht_reduce", "ht_reduce_ex", "ht_reduce_mg", "ht_nccl_unique_id", "ht_nccl_comm_init",
+EXPORTS = ("ht_reduce", "ht_reduce_host", "ht_reduce_ex", "ht_reduce_mg", "ht_nccl_unique_id", "ht_nccl_comm_init",
            "ht_nccl_comm_destroy", "ht_mg_slab", "ht_strerror", "ht_version", "ht_release_workspace",
            "ht_bench_chain_apply")
 
@@ -83,6 +83,8 @@ def load_library():
         i64, P = ctypes.c_int64, ctypes.c_void_p
         lib.ht_reduce.restype = ctypes.c_int
         lib.ht_reduce.argtypes = [i64, P, P, P, P, ctypes.c_int, ctypes.c_int, i64]
+        lib.ht_reduce_host.restype = ctypes.c_int
+        lib.ht_reduce_host.argtypes = [i64, P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, i64]
         lib.ht_reduce_ex.restype = ctypes.c_int
         lib.ht_reduce_ex.argtypes = [i64, P, i64, P, i64, P, i64, P, i64, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(HTOptions), ctypes.POINTER(HTReport)]
@@ -134,18 +136,36 @@ def _check(rc: int):
         raise HTError(rc, ht_strerror(rc))
 
 
-def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True):
-    """Host entry point: returns (H, T, Q, Z) as Fortran-ordered float64 arrays."""
+def pinned_empty(n: int):
+    """An n x n Fortran-ordered float64 host array in pinned (page-locked) memory, so that
+    ht_reduce_host moves it by DMA at full link rate (allocation through torch, the plumbing)."""
+    import torch
+    return torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy().T
+
+
+def ht_reduce(A, B, nb: int = 0, wantq: bool = True, wantz: bool = True, out=None):
+    """Host entry point (ht_reduce_host): returns (H, T, Q, Z) as Fortran-ordered float64
+    arrays.  A and B are not modified.  `out` = (H, T, Q, Z) preallocated n x n Fortran-ordered
+    float64 arrays (e.g. from pinned_empty) to write into; Q / Z may be None if not wanted."""
     lib = load_library()
-    H = np.array(A, dtype=np.float64, order="F", copy=True)
-    T = np.array(B, dtype=np.float64, order="F", copy=True)
-    n = H.shape[0]
-    if H.shape != (n, n) or T.shape != (n, n):
+    fort = lambda M: M if (isinstance(M, np.ndarray) and M.dtype == np.float64 and M.flags.f_contiguous) \
+        else np.asfortranarray(M, dtype=np.float64)
+    A, B = fort(A), fort(B)
+    n = A.shape[0]
+    if A.shape != (n, n) or B.shape != (n, n):
         raise ValueError("A and B must be square and of equal size")
-    Q = np.zeros((n, n), order="F") if wantq else None
-    Z = np.zeros((n, n), order="F") if wantz else None
+    if out is None:
+        H, T = np.empty((n, n), order="F"), np.empty((n, n), order="F")
+        Q = np.empty((n, n), order="F") if wantq else None
+        Z = np.empty((n, n), order="F") if wantz else None
+    else:
+        H, T, Q, Z = out
+        for M in (H, T) + ((Q,) if wantq else ()) + ((Z,) if wantz else ()):
+            if M is None or M.shape != (n, n) or M.dtype != np.float64 or not M.flags.f_contiguous:
+                raise ValueError("out arrays must be n x n Fortran-ordered float64")
     ptr = lambda a: a.ctypes.data if a is not None else None
-    _check(lib.ht_reduce(n, ptr(H), ptr(T), ptr(Q), ptr(Z), int(wantq), int(wantz), int(nb)))
+    _check(lib.ht_reduce_host(n, ptr(A), ptr(B), ptr(H), ptr(T), ptr(Q) if wantq else None,
+                              ptr(Z) if wantz else None, int(wantq), int(wantz), int(nb)))
     return H, T, Q, Z
 
 

@@ -83,6 +83,22 @@ struct Work {
 std::mutex g_mu[16];  // one per device: calls on different devices run concurrently
 Work g_work[16];
 
+// Device staging of the host entry points (ht_reduce / ht_reduce_host), kept per device
+// between calls; its own lock (the call takes g_mu inside ht_reduce_ex).
+struct HostStage {
+    double *d[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t bytes = 0;
+    cudaStream_t st = nullptr;
+};
+std::mutex g_hmu[16];
+HostStage g_hst[16];
+void host_stage_free(HostStage &hs)
+{
+    for (auto &p : hs.d)
+        if (p) { cudaFree(p); p = nullptr; }
+    hs.bytes = 0;
+}
+
 // Per-kernel-class device time from CUDA events recorded on the launch stream.
 // Classes: 0 panel, 1 DMMA GEMM, 2 factorizations (side streams), 3 other, 4 chained window
 // applies, 5 absorb-right span and 6 absorb-left span (critical stream), 7 factorizations on
@@ -1193,6 +1209,10 @@ int ht_release_workspace(void)
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HT_ECUDA;
     if (dev < 0 || dev >= 16) return HT_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_hmu[dev]);
+        host_stage_free(g_hst[dev]);
+    }
     std::lock_guard<std::mutex> lk(g_mu[dev]);
     work_free(g_work[dev]);
     return HT_OK;
@@ -1553,40 +1573,57 @@ int ht_reduce_mg(int64_t n, const ht_mg_layout *L, void *nccl_comm, int rank, in
                        nccl_comm ? rank : 0, nranks > 1 ? nccl_comm : nullptr, L->gather_qz);
 }
 
-int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb)
+int ht_reduce_host(int64_t n, const double *A, const double *B, double *H, double *T, double *Q, double *Z,
+                   int wantq, int wantz, int64_t nb)
 {
     int rc = validate(n, A, n, B, n, Q, n, Z, n, wantq, wantz, nullptr);
     if (rc) return rc;
+    if (n > 0 && !H) return HT_EARG_A;
+    if (n > 0 && !T) return HT_EARG_B;
     if (n == 0) return HT_OK;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HT_ECUDA;
+    int ndev = 0, dev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || cudaGetDevice(&dev) != cudaSuccess) return HT_ECUDA;
+    if (dev < 0 || dev >= 16) return HT_ECUDA;
     const size_t bytes = (size_t)n * n * sizeof(double);
-    double *d[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int i = 0; i < 4; ++i)
-        if (cudaMalloc((void **)&d[i], bytes) != cudaSuccess) {
-            for (int j = 0; j < i; ++j) cudaFree(d[j]);
-            return HT_ENOMEM;
-        }
-    auto cleanup = [&]() { for (int i = 0; i < 4; ++i) cudaFree(d[i]); };
-    if (cudaMemcpy(d[0], A, bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d[1], B, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
-        cleanup();
+    std::lock_guard<std::mutex> lk(g_hmu[dev]);
+    HostStage &hs = g_hst[dev];
+    if (hs.bytes < bytes) {
+        host_stage_free(hs);
+        for (int i = 0; i < 4; ++i)
+            if (cudaMalloc((void **)&hs.d[i], bytes) != cudaSuccess) {
+                cudaGetLastError();
+                host_stage_free(hs);
+                return HT_ENOMEM;
+            }
+        hs.bytes = bytes;
+    }
+    if (!hs.st && cudaStreamCreateWithFlags(&hs.st, cudaStreamNonBlocking) != cudaSuccess) return HT_ECUDA;
+    double **d = hs.d;
+    if (cudaMemcpyAsync(d[0], A, bytes, cudaMemcpyHostToDevice, hs.st) != cudaSuccess ||
+        cudaMemcpyAsync(d[1], B, bytes, cudaMemcpyHostToDevice, hs.st) != cudaSuccess) {
+        cudaStreamSynchronize(hs.st);
         return HT_ECUDA;
     }
     ht_options opt;
     memset(&opt, 0, sizeof(opt));
     opt.nb = nb;
+    opt.stream = hs.st;
     rc = ht_reduce_ex(n, d[0], n, d[1], n, wantq ? d[2] : nullptr, n, wantz ? d[3] : nullptr, n, wantq, wantz, &opt,
                       nullptr);
     if (rc == HT_OK) {
-        if (cudaMemcpy(A, d[0], bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(B, d[1], bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            (wantq && cudaMemcpy(Q, d[2], bytes, cudaMemcpyDeviceToHost) != cudaSuccess) ||
-            (wantz && cudaMemcpy(Z, d[3], bytes, cudaMemcpyDeviceToHost) != cudaSuccess))
+        if (cudaMemcpyAsync(H, d[0], bytes, cudaMemcpyDeviceToHost, hs.st) != cudaSuccess ||
+            cudaMemcpyAsync(T, d[1], bytes, cudaMemcpyDeviceToHost, hs.st) != cudaSuccess ||
+            (wantq && cudaMemcpyAsync(Q, d[2], bytes, cudaMemcpyDeviceToHost, hs.st) != cudaSuccess) ||
+            (wantz && cudaMemcpyAsync(Z, d[3], bytes, cudaMemcpyDeviceToHost, hs.st) != cudaSuccess))
             rc = HT_ECUDA;
     }
-    cleanup();
+    if (cudaStreamSynchronize(hs.st) != cudaSuccess && rc == HT_OK) rc = HT_ECUDA;
     return rc;
+}
+
+int ht_reduce(int64_t n, double *A, double *B, double *Q, double *Z, int wantq, int wantz, int64_t nb)
+{
+    return ht_reduce_host(n, A, B, A, B, Q, Z, wantq, wantz, nb);
 }
 
 }  // extern "C"

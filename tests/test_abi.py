@@ -46,6 +46,16 @@ def test_argument_errors_before_any_write():
     assert lib.ht_reduce(4, A.ctypes.data, A.ctypes.data, None, A.ctypes.data, 0, 3, 0) == -7
     assert np.array_equal(A, keep)
     assert lib.ht_reduce(0, None, None, None, None, 1, 1, 0) == 0
+    # out-of-place host entry point: inputs, then outputs
+    p = A.ctypes.data
+    assert lib.ht_reduce_host(-1, p, p, p, p, None, None, 0, 0, 0) == -1
+    assert lib.ht_reduce_host(4, None, p, p, p, None, None, 0, 0, 0) == -2
+    assert lib.ht_reduce_host(4, p, None, p, p, None, None, 0, 0, 0) == -3
+    assert lib.ht_reduce_host(4, p, p, None, p, None, None, 0, 0, 0) == -2
+    assert lib.ht_reduce_host(4, p, p, p, None, None, None, 0, 0, 0) == -3
+    assert lib.ht_reduce_host(4, p, p, p, p, None, None, 1, 0, 0) == -4
+    assert np.array_equal(A, keep)
+    assert lib.ht_reduce_host(0, None, None, None, None, None, None, 1, 1, 0) == 0
 
 
 def test_ex_option_errors_before_any_write():

@@ -304,6 +304,31 @@ def test_host_entry_point_matches_device():
     assert np.array_equal(Q, Q2) and np.array_equal(Z, Z2)
 
 
+def test_host_entry_point_out_of_place_pinned():
+    """ht_reduce_host: A, B untouched, outputs (pageable or pinned) bitwise equal to the
+    in-place ht_reduce; the device staging is reused across calls and sizes."""
+    A, B = ht_inputs.pencil("qruniform", 130, 5)
+    A0, B0 = A.copy(), B.copy()
+    ref = ht.ht_reduce(A, B, nb=16)
+    assert np.array_equal(A, A0) and np.array_equal(B, B0)
+    lib = ht.load_library()
+    Hi, Ti = np.asfortranarray(A.copy()), np.asfortranarray(B.copy())
+    Qi, Zi = np.empty((130, 130), order="F"), np.empty((130, 130), order="F")
+    assert lib.ht_reduce(130, Hi.ctypes.data, Ti.ctypes.data, Qi.ctypes.data, Zi.ctypes.data, 1, 1, 16) == 0
+    for x, y in zip(ref, (Hi, Ti, Qi, Zi)):
+        assert np.array_equal(x, y)
+    Ap, Bp = ht.pinned_empty(130), ht.pinned_empty(130)
+    Ap[:], Bp[:] = A, B
+    outs = tuple(ht.pinned_empty(130) for _ in range(4))
+    got = ht.ht_reduce(Ap, Bp, nb=16, out=outs)
+    assert all(g is o for g, o in zip(got, outs))
+    for x, y in zip(ref, got):
+        assert np.array_equal(x, y)
+    assert np.array_equal(Ap, A0) and np.array_equal(Bp, B0)
+    small = ht.ht_reduce(A[:40, :40], np.triu(B[:40, :40]), nb=8)  # smaller n after a larger one
+    assert small[0].shape == (40, 40)
+
+
 def test_deterministic():
     A, B = ht_inputs.pencil("qruniform", 300, 4)
     r1 = gpu_reduce(A, B, nb=32)
