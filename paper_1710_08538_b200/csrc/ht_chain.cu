@@ -75,11 +75,13 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
 
     // Qhat chunks arrive by bulk copy (cp.async.bulk, one per Qhat row, completion counted on
     // the buffer's mbarrier) when the window's rows are 16-byte aligned; else by 8-byte cp.async
-    __shared__ __align__(8) unsigned long long qbar[2];
+    __shared__ __align__(8) unsigned long long qbar[2], ebar;
     const unsigned qb0 = (unsigned)__cvta_generic_to_shared(&qbar[0]);
+    const unsigned eb = (unsigned)__cvta_generic_to_shared(&ebar);  // entering columns (bulk path)
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(qb0) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(qb0 + 8) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(eb) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     // rows k >= p of a ragged last chunk are not rewritten: they meet zero slab columns, so
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     unsigned qpar = 0;  // bit b: parity of the next wait on Qhat buffer b
+    unsigned epar = 0;  // parity of the next wait on ebar
 
     // slab tasks over all matrices; a capped grid loops over them (persistent style), so that
     // concurrent streams keep SMs free for the factorization chain
@@ -146,15 +149,32 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
     // a handful of columns per call, so plain warp/lane loops (no division by runtime sizes)
     auto load_cols_async = [&](int64_t c_lo, int64_t c_hi) {
         const int nc = (int)(c_hi - c_lo);
-        if (M.left) {
-            for (int s = warp; s < h; s += CNT / 32)
-                for (int c = lane; c < nc; c += 32)
-                    cp_async8(&Xs[slot(c_lo + c) * ldh + s], s < hs ? gaddr(s, c_lo + c) : M.X, s < hs);
+        if (M.left) {  // columns fastest (contiguous in X), every lane busy
+            const int total = nc * h;
+            for (int idx = tid; idx < total; idx += CNT) {
+                const int s = idx / nc, c = idx - s * nc;
+                cp_async8(&Xs[slot(c_lo + c) * ldh + s], s < hs ? gaddr(s, c_lo + c) : M.X, s < hs);
+            }
         } else {
             for (int c = warp; c < nc; c += CNT / 32)
                 for (int s = lane; s < h; s += 32)
                     cp_async8(&Xs[slot(c_lo + c) * ldh + s], s < hs ? gaddr(s, c_lo + c) : M.X, s < hs);
         }
+    };
+    // right applies with 16-byte aligned slab columns: one bulk copy per entering column
+    // (hs rows, contiguous in X), issued by warp 1's lanes, bytes counted on ebar
+    auto load_cols_bulk = [&](int64_t c_lo, int64_t c_hi) {
+        if (warp != 1) return;
+        const int nc = (int)(c_hi - c_lo);
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(eb), "r"((unsigned)(nc * hs * 8)) : "memory");
+        }
+        __syncwarp();
+        for (int c = lane; c < nc; c += 32)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                         ::"r"((unsigned)__cvta_generic_to_shared(&Xs[slot(c_lo + c) * ldh])), "l"(gaddr(0, c_lo + c)),
+                         "r"(hs * 8), "r"(eb) : "memory");
     };
     auto store_cols = [&](int64_t c_lo, int64_t c_hi) {
         const int nc = (int)(c_hi - c_lo);
@@ -205,9 +225,12 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
         const bool inside = active && s0 >= lo && s0 + hs <= hi;
         const bool early = inside && !last && b0 >= a0 && b1 >= a1 && b1 - b0 <= cap;
         const int direct = !inside ? 0 : last ? p : early ? (int)(b0 - a0 < p ? b0 - a0 : p) : 0;
+        const bool ebulk = early && !M.left && (hs % 2) == 0 && (M.ld % 2) == 0 && (((uintptr_t)(M.X + s0)) & 15) == 0;
         const int64_t e_beg = a0 + pp > a1 ? a0 + pp : a1;  // first early-prefetchable entering column
         int64_t e_cur = e_beg;
         CPROF_T(tw0);
+        // the ring's generic-proxy writes (epilogue, transition) before any bulk copy into it
+        if (ebulk) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
         if (active) {
             const int nwr = h / 32, nwc = pp / 32;
@@ -226,16 +249,20 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             auto fetch = [&](int k0, int buf) {
                 double *qd = Qs + (size_t)buf * kc * ldq;
                 if (qbulk) {
-                    if (tid == 0) {
+                    // warp 0: lane 0 posts the byte count, then lane r copies Qhat row k0 + r
+                    if (warp == 0) {
                         const int nr = p - k0 < kc ? p - k0 : kc;
                         const unsigned mb = qb0 + 8 * buf;
-                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                                     "r"((unsigned)(nr > 0 ? nr * p * 8 : 0)) : "memory");
-                        for (int r = 0; r < nr; ++r)
+                        if (lane == 0) {
+                            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                                         "r"((unsigned)(nr > 0 ? nr * p * 8 : 0)) : "memory");
+                        }
+                        __syncwarp();
+                        if (lane < nr)
                             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                                         ::"r"((unsigned)__cvta_generic_to_shared(qd + r * ldq)),
-                                         "l"(W.Qw + (size_t)(k0 + r) * p), "r"(p * 8), "r"(mb) : "memory");
+                                         ::"r"((unsigned)__cvta_generic_to_shared(qd + lane * ldq)),
+                                         "l"(W.Qw + (size_t)(k0 + lane) * p), "r"(p * 8), "r"(mb) : "memory");
                     }
                     return;
                 }
@@ -274,10 +301,11 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                     int64_t lim = a0 + (int64_t)kt * kc + cap;
                     if (lim > b1) lim = b1;
                     if (lim > e_cur) {
-                        load_cols_async(e_cur, lim);
+                        if (ebulk) load_cols_bulk(e_cur, lim);
+                        else load_cols_async(e_cur, lim);
                         e_cur = lim;
                     }
-                    cp_async_commit();
+                    if (!ebulk) cp_async_commit();
                 }
                 if (wact) {
                     const double *qb = Qs + (size_t)buf * kc * ldq;
@@ -297,8 +325,9 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                     }
                 }
                 // the next Qhat chunk has landed; this chunk's entering columns may still fly
-                if (kt + 1 < nk) qwait(buf ^ 1, early);
-                else if (early) cp_async_wait<1>();
+                const bool ecp = early && !ebulk;
+                if (kt + 1 < nk) qwait(buf ^ 1, ecp);
+                else if (ecp) cp_async_wait<1>();
                 CPROF_T(tb0);
                 __syncthreads();
                 CPROF_T(tb1);
@@ -306,6 +335,8 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             }
             CPROF_T(tl1);
             CPROF_ADD(1, tl0, tl1);
+            if (ebulk && tid == 32)  // all entering copies of this window are issued
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(eb) : "memory");
             // epilogue: slab(s, o + c) <- acc for s in [lo, hi), c < p; the first `direct`
             // columns leave the chain here and go straight to HBM
             if (wact) {
@@ -328,6 +359,13 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
             }
         }
         cp_async_wait<0>();
+        if (ebulk) {  // (ebulk implies active: the arrival above happened)
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+                             : "=r"(done) : "r"(eb), "r"(epar) : "memory");
+            epar ^= 1u;
+        }
         __syncthreads();
         CPROF_T(tt0);
         CPROF_ADD(2, tw0, tt0);
