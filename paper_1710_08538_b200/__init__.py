@@ -252,11 +252,12 @@ def reduce_device(A, B, Q=None, Z=None, nb=0, stream=None, **kw):
     (tensor t with t[j, i] = M[i, j], i.e. t = M^T row-major). Returns the report."""
     n = A.shape[0]
     for t in (A, B, Q, Z):
-        if t is not None:
-            assert t.is_cuda and t.is_contiguous() and t.shape == (n, n)
+        if t is not None:  # rows of t (= columns of M) may be padded: stride (ld, 1), ld >= n
+            assert t.is_cuda and t.shape == (n, n) and (n == 0 or t.stride(1) == 1) and t.stride(0) >= n
     if stream is None:
         import torch
         stream = torch.cuda.current_stream().cuda_stream
     opt = make_options(nb=nb, stream=stream, **kw)
     p = lambda t: t.data_ptr() if t is not None else None
-    return ht_reduce_ex(n, p(A), n, p(B), n, p(Q), n, p(Z), n, Q is not None, Z is not None, opt)
+    ld = lambda t: max(t.stride(0), 1) if t is not None else max(n, 1)
+    return ht_reduce_ex(n, p(A), ld(A), p(B), ld(B), p(Q), ld(Q), p(Z), ld(Z), Q is not None, Z is not None, opt)

@@ -329,6 +329,29 @@ def test_host_entry_point_out_of_place_pinned():
     assert small[0].shape == (40, 40)
 
 
+@pytest.mark.parametrize("pad", [1, 2, 3])
+def test_leading_dimensions(pad):
+    """ld = n + pad (odd pads take the 8-byte fallbacks of the bulk-copy and vector-load paths):
+    the same pencil gives the same H, T, Q, Z as ld = n, element by element."""
+    A, B = ht_inputs.pencil("qruniform", 600, 12)
+    ref = gpu_reduce(A, B, nb=128)
+    n = A.shape[0]
+    def padded(M):
+        buf = torch.full((n, n + pad), float("nan"), dtype=torch.float64, device="cuda")
+        t = buf[:, :n]
+        if M is not None:
+            t.copy_(torch.from_numpy(np.ascontiguousarray(M.T)))
+        return buf, t
+    (bA, tA), (bB, tB), (bQ, tQ), (bZ, tZ) = padded(A), padded(B), padded(None), padded(None)
+    ht.reduce_device(tA, tB, tQ, tZ, nb=128)
+    torch.cuda.synchronize()
+    for x, t in zip(ref[:4], (tA, tB, tQ, tZ)):
+        got = t.cpu().numpy().T
+        assert np.allclose(got, x, rtol=0, atol=1e-13 * max(1.0, np.abs(x).max())), np.abs(got - x).max()
+    for b in (bA, bB, bQ, bZ):  # the padding columns were never written
+        assert torch.isnan(b[:, n:]).all()
+
+
 def test_deterministic():
     A, B = ht_inputs.pencil("qruniform", 300, 4)
     r1 = gpu_reduce(A, B, nb=32)
