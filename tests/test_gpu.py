@@ -332,13 +332,16 @@ def test_host_entry_point_out_of_place_pinned():
 @pytest.mark.parametrize("pad", [1, 2, 3])
 def test_leading_dimensions(pad):
     """ld = n + pad (odd pads take the 8-byte fallbacks of the bulk-copy and vector-load paths):
-    the same pencil gives the same H, T, Q, Z as ld = n, element by element."""
+    the same pencil gives the same H, T, Q, Z as ld = n, element by element; NaN guard regions
+    around every matrix and in its padding stay untouched (a write-bounds check standing in for
+    compute-sanitizer memcheck, which this GPU pool does not run)."""
     A, B = ht_inputs.pencil("qruniform", 600, 12)
     ref = gpu_reduce(A, B, nb=128)
     n = A.shape[0]
+    G = 3  # guard columns of M (rows of the tensor) before and after the matrix
     def padded(M):
-        buf = torch.full((n, n + pad), float("nan"), dtype=torch.float64, device="cuda")
-        t = buf[:, :n]
+        buf = torch.full((n + 2 * G, n + pad), float("nan"), dtype=torch.float64, device="cuda")
+        t = buf[G:G + n, :n]
         if M is not None:
             t.copy_(torch.from_numpy(np.ascontiguousarray(M.T)))
         return buf, t
@@ -348,8 +351,9 @@ def test_leading_dimensions(pad):
     for x, t in zip(ref[:4], (tA, tB, tQ, tZ)):
         got = t.cpu().numpy().T
         assert np.allclose(got, x, rtol=0, atol=1e-13 * max(1.0, np.abs(x).max())), np.abs(got - x).max()
-    for b in (bA, bB, bQ, bZ):  # the padding columns were never written
-        assert torch.isnan(b[:, n:]).all()
+    for b in (bA, bB, bQ, bZ):  # padding and guard regions were never written (out-of-bounds check)
+        assert torch.isnan(b[G:G + n, n:]).all()
+        assert torch.isnan(b[:G]).all() and torch.isnan(b[G + n:]).all()
 
 
 def test_deterministic():
