@@ -458,8 +458,12 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
     const bool dbl = band_double_buffer(p8);  // windows of <= 256 rows: prefetch the next block
     // Bulk-copy path (copy engine, one cp.async.bulk per column, completion on an mbarrier):
     // needs 16-byte aligned columns of whole 8-row multiples; else 8-byte cp.async.
+#ifdef BAND_NOBULK
+    const bool bulk = false;
+#else
     const bool bulk = (p % 8) == 0 && (A.ldv % 2) == 0 && (A.ldt % 2) == 0 && ((uintptr_t)A.V & 15) == 0 &&
                       ((uintptr_t)A.T & 15) == 0;
+#endif
     __shared__ __align__(8) unsigned long long mbar[2];
     const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
     if (bulk && tid == 0) {
@@ -478,12 +482,15 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
                 for (int r = tid; r < p8; r += 256) vb[j * ldr + r] = 0.0;
                 if (tid < BPW) tb[j * LDY + tid] = 0.0;
             }
-            if (tid == 0) {
+            if (warp == 0) {  // lane 0 posts the byte count; lane j copies column j of V_b and T_b
                 const unsigned mb = mb0 + 8 * bf;
                 const unsigned bytes = (unsigned)(nc * (p + BPW) * 8);
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
-                for (int j = 0; j < nc; ++j) {
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+                }
+                __syncwarp();
+                for (int j = lane; j < nc; j += 32) {
                     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                                  ::"r"((unsigned)__cvta_generic_to_shared(vb + j * ldr)), "l"(A.V + (int64_t)(j0 + j) * A.ldv),
                                  "r"(p * 8), "r"(mb) : "memory");
@@ -517,19 +524,31 @@ __global__ void __launch_bounds__(256) band_wy_kernel(const BandDesc *descs, con
         ++uses[bf];
     };
     if (dbl) stage(0);
-    if (A.left) {  // contiguous along c
-        for (int s = 0; s < 8; ++s)
-            for (int c = tid; c < p8; c += 256) {
-                double v = 0.0;
-                if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
-                Ss[s * lds + c] = v;
+    // the slab (8 x p): every thread issues all its loads before its shared-memory stores
+    // (p8 <= 512: at most 16 elements per thread)
+    {
+        constexpr int ME = 16;
+        double t[ME];
+#pragma unroll
+        for (int e = 0; e < ME; ++e) {
+            const int i = tid + e * 256;
+            t[e] = 0.0;
+            if (i < 8 * p8) {
+                int ss, c;
+                if (A.left) { ss = i / p8; c = i - ss * p8; }  // contiguous along c
+                else { c = i >> 3; ss = i & 7; }                // contiguous along s
+                if (ss < ns && c < p) t[e] = A.ident ? ((sb + ss == A.o + c) ? 1.0 : 0.0) : *xp(ss, c);
             }
-    } else {       // contiguous along s
-        for (int i = tid; i < 8 * p8; i += 256) {
-            const int c = i >> 3, s = i & 7;
-            double v = 0.0;
-            if (s < ns && c < p) v = A.ident ? ((sb + s == A.o + c) ? 1.0 : 0.0) : *xp(s, c);
-            Ss[s * lds + c] = v;
+        }
+#pragma unroll
+        for (int e = 0; e < ME; ++e) {
+            const int i = tid + e * 256;
+            if (i < 8 * p8) {
+                int ss, c;
+                if (A.left) { ss = i / p8; c = i - ss * p8; }
+                else { c = i >> 3; ss = i & 7; }
+                Ss[ss * lds + c] = t[e];
+            }
         }
     }
     for (int b = 0; b < nblk; ++b) {
