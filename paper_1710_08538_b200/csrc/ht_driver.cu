@@ -70,6 +70,8 @@ struct Work {
     int *d_irtrace = nullptr;
     double *Dinv = nullptr, *Bt = nullptr, *ypart = nullptr, *ypartB = nullptr, *BV = nullptr;
     int *dsafe = nullptr;
+    double *Dinv4 = nullptr;                 // 256-row solve (trsv4): inverted 256 x 256 diagonal blocks
+    int *dsafe4 = nullptr, *h_dsafe4 = nullptr;
     double *fro_part = nullptr;  // fixed-order partial sums of ||B||_F^2
     double *mgbuf = nullptr;     // packed all-gather staging (ht_reduce_mg)
     size_t mgcap = 0;
@@ -210,6 +212,11 @@ void work_free(Work &w)
     if (w.dsafe) cudaFree(w.dsafe);
     w.Dinv = nullptr;
     w.dsafe = nullptr;
+    if (w.Dinv4) cudaFree(w.Dinv4);
+    if (w.dsafe4) cudaFree(w.dsafe4);
+    if (w.h_dsafe4) cudaFreeHost(w.h_dsafe4);
+    w.Dinv4 = nullptr;
+    w.dsafe4 = w.h_dsafe4 = nullptr;
     if (w.d_fd) cudaFree(w.d_fd);
     if (w.h_out) cudaFreeHost(w.h_out);
     if (w.h_scal) cudaFreeHost(w.h_scal);
@@ -313,6 +320,9 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.ypartB, (size_t)(N / 256 + 2) * (size_t)N));
     TRY(dalloc(&w.BV, nnb));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    TRY(dalloc(&w.Dinv4, (size_t)(N / 256 + 2) * 256 * 256));
+    if (cudaMalloc((void **)&w.dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMallocHost((void **)&w.h_dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -1338,6 +1348,7 @@ int reduce_body(Run &R, const ht_options *opt)
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.yll = w->yll; pa.yll_exp = w->yll_exp; pa.bexp = w->bexp; pa.epoch = w->epoch;
             pa.Dinv = w->Dinv; pa.Bt = w->Bt; pa.ldbt = n; pa.dsafe = w->dsafe; pa.ypart = w->ypart;
+            pa.Dinv4 = w->Dinv4; pa.dsafe4 = w->dsafe4; pa.h_dsafe4 = w->h_dsafe4;
             pa.ypartB = w->ypartB; pa.BV = w->BV; pa.vbx = vv + 7 * N;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;

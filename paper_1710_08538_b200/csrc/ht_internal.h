@@ -75,6 +75,12 @@ struct PanelArgs {
     double *Bt;         // Dinv_b * B(block b, blocks > b): pre-scaled block rows
     int64_t ldbt;
     int *dsafe;         // per block: 1 = use Dinv, 0 = sequential scaled substitution
+    // 256-row solve on 4-CTA clusters (ht_panel.cu trsv4), used for a panel when every 256-row
+    // diagonal block is safe: Dinv4 = inverses of the 256 x 256 diagonal blocks (ld 256),
+    // Bt = Dinv4_b B(block b, blocks > b) packed with ld 256; dsafe4 per 256-row block
+    double *Dinv4;
+    int *dsafe4, *h_dsafe4;  // device / pinned host
+    int solve4;
     int *bexp;          // trsv block exponents
     unsigned epoch;     // trsv flag epoch base
     double tol;         // 2 u ||B||_F

@@ -36,6 +36,8 @@ namespace {
 constexpr int PNT = 512;   // threads per CTA
 constexpr int NWP = PNT / 32;
 constexpr int TB = 128;    // triangular-solve block size
+constexpr int T4 = 256;    // trsv4: solve block rows (4-CTA clusters, 64-column slices)
+constexpr int C4 = 4;
 constexpr int NBMAX = 256; // max panel width supported
 constexpr int RBMAX = 256; // max own rows per CTA (uniform slabs)
 constexpr double BIG = 0x1p256;
@@ -53,6 +55,7 @@ struct __align__(16) PanelSmem {
     double cbv[TB];
     double yrecv[TB];  // y~_{b+1} handed over by the partner CTA of the cluster (DSMEM)
     unsigned long long mbar;  // completes when the partner has written yrecv/erecv (TB remote arrivals)
+    unsigned long long mbar4; // trsv4, cluster rank 0: the 3 partial-sum messages of a block have landed
     int ival[4];
     int erecv;
 };
@@ -71,6 +74,8 @@ __device__ __forceinline__ unsigned long long gtime()
 struct Ctx {
     const PanelArgs &a;
     unsigned mbpar = 0;  // parity of the next phase of g_sm.mbar (lo CTAs of the solve clusters)
+    unsigned mb4par = 0; // parity of the next phase of g_sm.mbar4 (trsv4, cluster rank 0)
+    int tbs;             // rows per solve block: 128 (trsv_blocked) or 256 (trsv4)
     int G, bid, tid, lane, warp;
     int64_t n, p0, M, rb0, rb1;
     int nr;
@@ -94,6 +99,7 @@ struct Ctx {
         part[0] = a.part;
         part[1] = a.part + (size_t)G * a.pw;
         ph = 0;
+        tbs = a.solve4 ? 256 : TB;
     }
     // partials are stored index-major: (CTA b, index c) at part[ph][c * G + b], so a gather
     // reads contiguous CTA runs
@@ -652,10 +658,218 @@ __device__ void trsv_blocked(Ctx &C, BaseF base, UnewF unew, int k, const double
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 256-row flag-chained solve on 4-CTA clusters (trsv4).  Same recurrence as trsv_blocked,
+//   y~_b = Dinv4_b rhs_b - sum_{c > b} Bt_bc y~_c,   Bt_bc = Dinv4_b B_bc   (packed, ld T4),
+// with blocks of T4 = 256 rows: half as many hops on the chain's critical path.  Cluster
+// rank q owns the 64-column slice q of every tile of its block row (T4 x 64 doubles in
+// registers, 32 per thread) and consumes only slice q of each y~_c; its 256-row partial sums
+// (and its slice of Dinv4_b rhs_b) reach rank 0 in one bulk copy over distributed shared
+// memory, and rank 0 forms and publishes y~_b (one exponent per block, as trsv_blocked).
+// Used for a panel only when every 256-row diagonal block is safe (ht_panel_run).
+__host__ __device__ __forceinline__ int64_t bt4_row_offset(int64_t M, int64_t b)
+{
+    return (int64_t)T4 * (b * M - (int64_t)T4 * b * (b + 1) / 2);
+}
+struct Tile4 {
+    double2 x[16];  // rows 2rp, 2rp+1 x columns 16 grp + u of the slice
+};
+__device__ __forceinline__ void tile4_load(Tile4 &t, const double *X, int w, int h, int tid)
+{
+    const int rp = tid & 127, grp = tid >> 7;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int c = 16 * grp + u;
+        if (c < w && 2 * rp + 1 < h) {
+            t.x[u] = *reinterpret_cast<const double2 *>(X + (size_t)c * T4 + 2 * rp);
+        } else {
+            t.x[u].x = (c < w && 2 * rp < h) ? X[(size_t)c * T4 + 2 * rp] : 0.0;
+            t.x[u].y = 0.0;
+        }
+    }
+}
+__device__ __forceinline__ void tile4_fma(const Tile4 &t, const double *ys, int tid, double &a0, double &a1)
+{
+    const int grp = tid >> 7;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const double yv = ys[16 * grp + u];
+        a0 = fma(t.x[u].x, yv, a0);
+        a1 = fma(t.x[u].y, yv, a1);
+    }
+}
+// slice q (w values) of the published solution block cb (256-row blocks) and its exponent
+__device__ __forceinline__ int fetch4(Ctx &C, int cb, int q, int w, unsigned epoch, double *ys)
+{
+    const int64_t c0 = C.p0 + (int64_t)cb * T4 + 64 * q;
+    if (C.tid < 64) ys[C.tid] = (C.tid < w) ? ll_get(C.a.yll + 2 * (c0 + C.tid), epoch) : 0.0;
+    if (C.tid == 64) g_sm.ival[cb & 1] = ll_get_exp(C.a.yll_exp + cb, epoch);
+    __syncthreads();
+    return g_sm.ival[cb & 1];
+}
+template <class BaseF, class UnewF>
+__device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, unsigned epoch)
+{
+    const PanelArgs &a = C.a;
+    const int64_t n = C.n, p0 = C.p0, M = C.M;
+    const int Nb = (int)((M + T4 - 1) / T4);
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank(), ncl = C.G / C4, cid = C.bid / C4;
+    const int rp = C.tid & 127, grp = C.tid >> 7;
+    constexpr int SZ = 2 * T4 + 8;  // message: 256 partial sums, 256 slice sums of Dinv4 rhs, exponent
+    double *ys = g_dyn;             // [64]
+    double *rs = ys + 64;           // [64] rhs slice
+    double *pa = rs + 64;           // [4][T4] partial sums of the column groups
+    double *pc = pa + 4 * T4;       // [4][T4]
+    double *snd = pc + 4 * T4;      // [SZ] message to rank 0
+    double *rcv = snd + SZ;         // [3][SZ] messages at rank 0
+    for (int sb = cid; sb < Nb; sb += ncl) {
+        const int b = Nb - 1 - sb;
+        const int64_t r0 = p0 + (int64_t)b * T4;
+        const int h = (int)(n - r0 < T4 ? n - r0 : T4);
+        const bool last = (b == Nb - 1);
+        const int hq = h - 64 * q < 0 ? 0 : (h - 64 * q > 64 ? 64 : h - 64 * q);  // rows of slice q
+        // (1) slice q of rhs_b, then its share of Dinv4_b rhs_b (independent of the chain)
+        {
+            const int row = C.tid >> 3, part = C.tid & 7;
+            const int64_t r = r0 + 64 * q + row;
+            double u = 0.0;
+            if (row < hq)
+                for (int c = part; c < k; c += 8) u = fma(a.U[(size_t)c * n + r], z2[c], u);
+            u += __shfl_xor_sync(0xffffffffu, u, 1);
+            u += __shfl_xor_sync(0xffffffffu, u, 2);
+            u += __shfl_xor_sync(0xffffffffu, u, 4);
+            if (part == 0) rs[row] = (row < hq) ? base(r) - u - unew(r) * z2[k] : 0.0;
+            __syncthreads();
+        }
+        double c0 = 0.0, c1 = 0.0;
+        {
+            Tile4 dt;
+            tile4_load(dt, a.Dinv4 + (size_t)b * T4 * T4 + (size_t)(64 * q) * T4, hq, h, C.tid);
+            tile4_fma(dt, rs, C.tid, c0, c1);
+        }
+        // (2) off-diagonal tiles c > b+1, as their solution slices arrive
+        double acc0 = 0.0, acc1 = 0.0;
+        int Eacc = 0;
+        const double *rowp = a.Bt + bt4_row_offset(M, b);  // columns from p0 + T4 (b+1), ld T4
+        for (int cb = Nb - 1; cb > b + 1; --cb) {
+            const int64_t cw0 = (int64_t)T4 * cb + 64 * q;  // first column of the slice (relative to p0)
+            const int w = (int)(M - cw0 < 0 ? 0 : (M - cw0 > 64 ? 64 : M - cw0));
+            Tile4 tr;
+            tile4_load(tr, rowp + (size_t)(cw0 - (int64_t)T4 * (b + 1)) * T4, w, h, C.tid);
+            const int ecb = fetch4(C, cb, q, w, epoch, ys);
+            if (ecb > Eacc) {
+                acc0 *= pow2i(Eacc - ecb);
+                acc1 *= pow2i(Eacc - ecb);
+                Eacc = ecb;
+            }
+            double t0 = 0.0, t1 = 0.0;
+            tile4_fma(tr, ys, C.tid, t0, t1);
+            const double sc = pow2i(ecb - Eacc);
+            acc0 = fma(t0, sc, acc0);
+            acc1 = fma(t1, sc, acc1);
+            __syncthreads();  // ys is reused
+        }
+        int E = Eacc;
+        if (!last) {  // (3) the critical tile (b, b+1): loaded before the wait for y~_{b+1}
+            const int64_t cw0 = (int64_t)T4 * (b + 1) + 64 * q;
+            const int w = (int)(M - cw0 < 0 ? 0 : (M - cw0 > 64 ? 64 : M - cw0));
+            Tile4 ct;
+            tile4_load(ct, rowp + (size_t)(64 * q) * T4, w, h, C.tid);
+            const int e1 = fetch4(C, b + 1, q, w, epoch, ys);
+            double t0 = 0.0, t1 = 0.0;
+            tile4_fma(ct, ys, C.tid, t0, t1);
+            E = max(e1, Eacc);
+            const double sa_ = pow2i(Eacc - E), sb_ = pow2i(e1 - E);
+            acc0 = fma(t0, sb_, acc0 * sa_);
+            acc1 = fma(t1, sb_, acc1 * sa_);
+        }
+        // (4) fold the 4 column groups; ranks 1-3 send their 256-row sums to rank 0
+        pa[grp * T4 + 2 * rp] = acc0;
+        pa[grp * T4 + 2 * rp + 1] = acc1;
+        pc[grp * T4 + 2 * rp] = c0;
+        pc[grp * T4 + 2 * rp + 1] = c1;
+        __syncthreads();
+        double sa = 0.0, sc = 0.0;
+        if (C.tid < T4) {
+            sa = (pa[C.tid] + pa[T4 + C.tid]) + (pa[2 * T4 + C.tid] + pa[3 * T4 + C.tid]);
+            sc = (pc[C.tid] + pc[T4 + C.tid]) + (pc[2 * T4 + C.tid] + pc[3 * T4 + C.tid]);
+            if (q != 0) {
+                snd[C.tid] = sa;
+                snd[T4 + C.tid] = sc;
+            }
+        }
+        if (q != 0) {
+            if (C.tid == 0) snd[2 * T4] = (double)E;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy
+            __syncthreads();
+            if (C.tid == 0) {
+                unsigned dst, mbr;
+                const unsigned src = (unsigned)__cvta_generic_to_shared(snd);
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst)
+                             : "r"((unsigned)__cvta_generic_to_shared(rcv + (q - 1) * SZ)), "r"(0));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(mbr)
+                             : "r"((unsigned)__cvta_generic_to_shared(&g_sm.mbar4)), "r"(0));
+                asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(mbr),
+                             "r"(SZ * 8) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(dst), "r"(src), "r"(SZ * 8), "r"(mbr) : "memory");
+            }
+        } else {
+            // (5) rank 0: combine, rescale if needed, publish y~_b
+            mbar_wait_parity(&g_sm.mbar4, C.mb4par);
+            C.mb4par ^= 1u;
+            int ei[3];
+            int Eall = E;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                ei[i] = (int)rcv[i * SZ + 2 * T4];
+                Eall = max(Eall, ei[i]);
+            }
+            double xv = 0.0;
+            if (C.tid < T4) {
+                double s = sa * pow2i(E - Eall), c = sc;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    s = fma(rcv[i * SZ + C.tid], pow2i(ei[i] - Eall), s);
+                    c += rcv[i * SZ + T4 + C.tid];
+                }
+                xv = c * pow2i(-Eall) - s;
+            }
+            int e = Eall;
+            const bool big = (C.tid < h) && !(fabs(xv) <= BIG);
+            int ex = 0;
+            if (__syncthreads_or(big)) {
+                double mx = (C.tid < h) ? fabs(xv) : 0.0;
+                mx = warp_max(mx);
+                if (C.lane == 0) g_sm.red[C.warp] = mx;
+                __syncthreads();
+                mx = 0.0;
+                for (int w = 0; w < NWP; ++w) mx = fmax(mx, g_sm.red[w]);
+                if (!(mx <= BIG)) frexp(mx, &ex);
+                if (!isfinite(mx)) ex = 0;
+            }
+            if (ex) xv = ldexp(xv, -ex);
+            e += ex;
+            if (C.tid < h) {
+                a.vy[r0 + C.tid] = xv;
+                ll_put(a.yll + 2 * (r0 + C.tid), xv, epoch);
+            }
+            if (C.tid == 0) {
+                a.bexp[b] = e;
+                st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
+            }
+        }
+        // the messages' buffers are reused by the next block of this cluster
+        cl.sync();
+    }
+    __syncthreads();
+}
+
 // After a completed solve (grid synced): Emax over all blocks.
 __device__ int trsv_emax(Ctx &C)
 {
-    const int Nb = (int)((C.M + TB - 1) / TB);
+    const int Nb = (int)((C.M + C.tbs - 1) / C.tbs);
     int e = INT_MIN;
     for (int b = C.tid; b < Nb; b += PNT) e = max(e, __ldcg(&C.a.bexp[b]));  // all loads in parallel
 #pragma unroll
@@ -902,6 +1116,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
     if (threadIdx.x == 0) {  // the solve's hand-over barrier: TB remote arrivals per phase
         const unsigned mb = (unsigned)__cvta_generic_to_shared(&g_sm.mbar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(TB) : "memory");
+        const unsigned mb4 = (unsigned)__cvta_generic_to_shared(&g_sm.mbar4);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb4), "r"(C4 - 1) : "memory");  // trsv4 senders
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cg::this_cluster().sync();  // the partner's barrier is initialised before any remote arrive
@@ -1001,7 +1217,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         __syncthreads();
         C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
-        trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch, j0);
+        if (a.solve4) trsv4(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch);
+        else trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch, j0);
         grid.sync();
         mark(1);
         int emax = trsv_emax(C);
@@ -1009,7 +1226,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         C.ph++;
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
-            int eb = __ldcg(&a.bexp[(r - p0) / TB]);
+            int eb = __ldcg(&a.bexp[(r - p0) / C.tbs]);
             g_sm.vloc[rl] = ldexp(__ldcg(&a.vy[r]), eb - emax);
         }
         __syncthreads();
@@ -1142,8 +1359,12 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // S_{k+1} (U^T r)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
-            trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
-                         [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, g_sm.sv3, epoch, -1);
+            if (a.solve4)
+                trsv4(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
+                      [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, g_sm.sv3, epoch);
+            else
+                trsv_blocked(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
+                             [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, g_sm.sv3, epoch, -1);
             grid.sync();
             const int ec = trsv_emax(C);
             if (ec > 0) { ++rescales; break; }  // a rescaled correction counts as IR failure
@@ -1293,6 +1514,63 @@ __global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t l
     }
 }
 
+// trsv4 set-up: Dinv4_b = [[Dinv_2b, X], [0, Dinv_2b+1]] (ld T4) with X = -Dinv_2b B_{2b,2b+1}
+// Dinv_2b+1 formed by two GEMMs afterwards; this kernel writes the diagonal quadrants and zeros
+// the rest (the lower-left quadrant doubles as the GEMMs' scratch and is zeroed again by
+// inv4_safety_kernel).
+__global__ void __launch_bounds__(256) inv4_assemble_kernel(const double *Dinv, int Nb, double *Dinv4)
+{
+    const int b4 = blockIdx.x, i0 = 2 * b4;
+    double *D = Dinv4 + (size_t)b4 * T4 * T4;
+    for (int idx = threadIdx.x; idx < T4 * T4; idx += 256) {
+        const int r = idx % T4, c = idx / T4;
+        double v = 0.0;
+        if (r < TB && c < TB) v = Dinv[(size_t)i0 * TB * TB + (size_t)c * TB + r];
+        else if (r >= TB && c >= TB && i0 + 1 < Nb) v = Dinv[(size_t)(i0 + 1) * TB * TB + (size_t)(c - TB) * TB + (r - TB)];
+        D[idx] = v;
+    }
+}
+// Safety of each 256-row block (the criterion of inv_diag_kernel on the whole block) and the
+// final zeroing of the scratch quadrant.
+__global__ void __launch_bounds__(256) inv4_safety_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
+                                                          double *Dinv4, const int *dsafe, int Nb, int *dsafe4)
+{
+    __shared__ double sm[2][8];
+    const int b4 = blockIdx.x, i0 = 2 * b4, tid = threadIdx.x;
+    const int64_t r0 = p0 + (int64_t)b4 * T4;
+    const int h = (int)(n - r0 < T4 ? n - r0 : T4);
+    double *D = Dinv4 + (size_t)b4 * T4 * T4;
+    double im = 0.0, dm = 0.0;
+    bool fin = true;
+    for (int idx = tid; idx < T4 * T4; idx += 256) {
+        const int r = idx % T4, c = idx / T4;
+        if (r >= TB && c < TB) D[idx] = 0.0;  // scratch quadrant
+        else {
+            const double v = D[idx];
+            if (!isfinite(v)) fin = false;
+            im = fmax(im, fabs(v));
+        }
+        if (r < h && c < h && r <= c) dm = fmax(dm, fabs(B[(size_t)(r0 + c) * ldb + r0 + r]));
+    }
+    if (!fin) im = INFINITY;
+    im = warp_max(im);
+    dm = warp_max(dm);
+    if ((tid & 31) == 0) {
+        sm[0][tid >> 5] = im;
+        sm[1][tid >> 5] = dm;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, d = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a = fmax(a, sm[0][w]);
+            d = fmax(d, sm[1][w]);
+        }
+        const bool ok = dsafe[i0] && (i0 + 1 >= Nb || dsafe[i0 + 1]);
+        dsafe4[b4] = (ok && isfinite(a) && a <= 0x1p200 && a * d <= 4e3) ? 1 : 0;
+    }
+}
+
 }  // namespace
 
 int ht_panel_max_blocks(int *nblocks_out)
@@ -1317,10 +1595,76 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb = (int)((M + TB - 1) / TB);
     inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
     HT_CUDA_TRY(cudaGetLastError());
-    // Bt(block b, blocks > b) = Dinv_b * B(block b, blocks > b): pre-scaled block rows, packed
-    // (bt_row_offset, ld TB: every TB x TB tile contiguous)
-    a->ldbt = TB;
-    if (Nb > 1) {
+    // The 256-row solve on 4-CTA clusters (trsv4) when every 256-row diagonal block is safe
+    // (decided on the host: one small copy per panel), else the 128-row paired solve.
+    static const bool no4 = getenv("HT_NO_TRSV4") != nullptr;  // development: force the 128-row solve
+    static const bool nocl = getenv("HT_PANEL_NOCLUSTER") != nullptr;
+    const int Nb4 = (int)((M + T4 - 1) / T4);
+    a->solve4 = 0;
+    int ncl4 = 0;
+    if (!no4 && !nocl && Nb4 >= 2 && a->Dinv4) {
+        cudaLaunchConfig_t oc = {};
+        oc.gridDim = dim3((unsigned)(nblocks & ~(C4 - 1)));
+        oc.blockDim = dim3(PNT);
+        oc.dynamicSmemBytes = DYN_DOUBLES * sizeof(double);
+        cudaLaunchAttribute oat[1];
+        oat[0].id = cudaLaunchAttributeClusterDimension;
+        oat[0].val.clusterDim.x = C4;
+        oat[0].val.clusterDim.y = 1;
+        oat[0].val.clusterDim.z = 1;
+        oc.attrs = oat;
+        oc.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&ncl4, panel_kernel, &oc) != cudaSuccess) {
+            cudaGetLastError();
+            ncl4 = 0;
+        }
+    }
+    if (ncl4 >= 2) {
+        inv4_assemble_kernel<<<Nb4, 256, 0, st>>>(a->Dinv, Nb, a->Dinv4);
+        HT_CUDA_TRY(cudaGetLastError());
+        std::vector<GemmBatchItem> g1, g2;
+        for (int b4 = 0; b4 < Nb4; ++b4) {
+            const int i0 = 2 * b4;
+            if (i0 + 1 >= Nb) continue;
+            const int64_t r0 = a->s0 + 1 + (int64_t)i0 * TB, c0 = r0 + TB;
+            const int w1 = (int)std::min<int64_t>(TB, a->n - c0);
+            double *D = a->Dinv4 + (size_t)b4 * T4 * T4;
+            // W = B_{i0,i0+1} Dinv_{i0+1} into the lower-left quadrant; X = -Dinv_{i0} W (upper right)
+            g1.push_back(GemmBatchItem{a->B + r0 + c0 * a->ldb, a->Dinv + (size_t)(i0 + 1) * TB * TB, D + TB, a->ldb, TB, T4,
+                                       TB, w1, w1, 1.0, 0.0, 0.0});
+            g2.push_back(GemmBatchItem{a->Dinv + (size_t)i0 * TB * TB, D + TB, D + (size_t)TB * T4, TB, T4, T4, TB, w1, TB,
+                                       -1.0, 0.0, 0.0});
+        }
+        if (!g1.empty()) {
+            int rc = ht_gemm_multi(st, 'N', 'N', g1.data(), (int)g1.size());
+            if (rc) return rc;
+            rc = ht_gemm_multi(st, 'N', 'N', g2.data(), (int)g2.size());
+            if (rc) return rc;
+        }
+        inv4_safety_kernel<<<Nb4, 256, 0, st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv4, a->dsafe, Nb, a->dsafe4);
+        HT_CUDA_TRY(cudaGetLastError());
+        HT_CUDA_TRY(cudaMemcpyAsync(a->h_dsafe4, a->dsafe4, Nb4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        HT_CUDA_TRY(cudaStreamSynchronize(st));
+        bool all = true;
+        for (int b4 = 0; b4 < Nb4; ++b4) all = all && a->h_dsafe4[b4] != 0;
+        a->solve4 = all ? 1 : 0;
+    }
+    if (a->solve4) {
+        // Bt = Dinv4_b B(block b, blocks > b), block rows of T4 rows packed with ld T4
+        std::vector<GemmBatchItem> it;
+        for (int b4 = 0; b4 + 1 < Nb4; ++b4) {
+            const int64_t r0 = a->s0 + 1 + (int64_t)b4 * T4, c0 = r0 + T4;
+            const int w = (int)(a->n - c0);
+            it.push_back(GemmBatchItem{a->Dinv4 + (size_t)b4 * T4 * T4, a->B + r0 + c0 * a->ldb, a->Bt + bt4_row_offset(M, b4),
+                                       T4, a->ldb, T4, T4, w, T4, 1.0, 0.0, 0.0});
+        }
+        int rc = ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size());
+        if (rc) return rc;
+        for (const auto &x : it) g_ht_flops -= 2.0 * TB * (double)TB * x.N;  // the zero lower-left quadrant of Dinv4
+    } else if (Nb > 1) {
+        // Bt(block b, blocks > b) = Dinv_b * B(block b, blocks > b): pre-scaled block rows, packed
+        // (bt_row_offset, ld TB: every TB x TB tile contiguous)
+        a->ldbt = TB;
         std::vector<GemmBatchItem> it;
         for (int b = 0; b + 1 < Nb; ++b) {
             const int64_t r0 = a->s0 + 1 + (int64_t)b * TB, c0 = r0 + TB;
@@ -1331,13 +1675,15 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         int rc = ht_gemm_multi(st, 'N', 'N', it.data(), (int)it.size());
         if (rc) return rc;
     }
+    a->ldbt = TB;
     // cooperative launch (grid barriers) in clusters of 2 CTAs (the solve hands blocks over
     // through distributed shared memory); the grid is even.  HT_PANEL_NOCLUSTER=1 (profiling
     // only: ncu cannot replay cooperative cluster launches) runs unpaired single CTAs.
-    static const bool nocl = getenv("HT_PANEL_NOCLUSTER") != nullptr;
+    const int csz = a->solve4 ? C4 : 2;
     if (!nocl) {
-        nblocks &= ~1;
-        if (nblocks < 2) nblocks = 2;
+        nblocks &= ~(csz - 1);
+        if (a->solve4 && nblocks > C4 * ncl4) nblocks = C4 * ncl4;
+        if (nblocks < csz) nblocks = csz;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)nblocks);
@@ -1348,7 +1694,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.x = (unsigned)csz;
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;

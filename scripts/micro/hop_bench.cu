@@ -124,13 +124,76 @@ __global__ void pingpong_l2(int iters, long long *cyc, unsigned long long *words
     sink[blockIdx.x * NT + tid] = v;
 }
 
+// V4: one 256-row hop of a 4-CTA cluster: register mat-vec (32 FMA per thread), fold of the 4
+// column groups through shared memory, reduce-scatter of the 256-row partials over DSMEM
+// (each CTA receives 3 x 64 partials, 192 remote arrivals per phase), sum, next hop
+struct Sm4 {
+    double part[4][256];
+    double recv[3][64];
+    double yslice[64];
+    unsigned long long mbar;
+};
+__global__ void __cluster_dims__(4, 1, 1) hop4(int iters, long long *cyc, double *sink)
+{
+    __shared__ Sm4 sm;
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank(), tid = threadIdx.x;
+    if (tid == 0) {
+        const unsigned mb = (unsigned)__cvta_generic_to_shared(&sm.mbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(192) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 64) sm.yslice[tid] = 1.0 + tid * 1e-3;
+    double tile[32];
+    for (int i = 0; i < 32; ++i) tile[i] = 1e-3 * (tid + i);
+    cl.sync();
+    unsigned par = 0;
+    const int rp = tid & 127, grp = tid >> 7;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        // (1) mat-vec: rows 2rp, 2rp+1 x 16 columns of this thread's group
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const double y = sm.yslice[grp * 16 + u];
+            a0 = fma(tile[2 * u], y, a0);
+            a1 = fma(tile[2 * u + 1], y, a1);
+        }
+        sm.part[grp][2 * rp] = a0;
+        sm.part[grp][2 * rp + 1] = a1;
+        __syncthreads();
+        // (2) fold + (3) send the 3 foreign 64-row slices (threads 0..255: row r of 256)
+        if (tid < 256) {
+            const double v = (sm.part[0][tid] + sm.part[1][tid]) + (sm.part[2][tid] + sm.part[3][tid]);
+            const int dst = tid >> 6;
+            if (dst != q) {
+                Sm4 *peer = cl.map_shared_rank(&sm, dst);
+                const int slot = q < dst ? q : q - 1;
+                peer->recv[slot][tid & 63] = v;
+                remote_arrive(&sm.mbar, dst);
+            } else {
+                sm.part[0][tid] = v;  // own slice
+            }
+        }
+        // (4) wait for the 3 peers, sum the own slice -> next hop's y slice
+        wait_parity(&sm.mbar, par);
+        par ^= 1u;
+        if (tid < 64) sm.yslice[tid] = sm.part[0][64 * q + tid] + (sm.recv[0][tid] + sm.recv[1][tid] + sm.recv[2][tid]) * 1e-30;
+        __syncthreads();
+    }
+    const long long t1 = clock64();
+    if (tid == 0 && q == 0) cyc[0] = (t1 - t0) / iters;
+    sink[blockIdx.x * 512 + tid] = sm.yslice[tid & 63];
+    cl.sync();
+}
+
 int main()
 {
     long long *cyc, h[4] = {0, 0, 0, 0};
     double *sink;
     unsigned long long *words;
     cudaMalloc(&cyc, 4 * 8);
-    cudaMalloc(&sink, 4 * NT * 8);
+    cudaMalloc(&sink, 8 * NT * 8);
     cudaMalloc(&words, TB * 8);
     cudaMemset(words, 0, TB * 8);
     const int iters = 20000;
@@ -138,7 +201,13 @@ int main()
     pingpong<1><<<2, NT>>>(iters, cyc, sink);
     pingpong<2><<<2, NT>>>(iters, cyc, sink);
     pingpong_l2<<<2, NT>>>(iters, cyc, words, sink);
+    long long *c4;
+    cudaMalloc(&c4, 8);
+    hop4<<<4, NT>>>(iters, c4, sink);
     cudaError_t e = cudaDeviceSynchronize();
+    long long h4 = 0;
+    cudaMemcpy(&h4, c4, 8, cudaMemcpyDeviceToHost);
+    printf("4-CTA 256-row hop (mat-vec + fold + DSMEM reduce-scatter + sum): %lld cycles\n", h4);
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
     printf("status %s\n", cudaGetErrorString(e));
     const char *nm[4] = {"DSMEM, 128 remote arrivals", "DSMEM, 4 warp arrivals + fence", "DSMEM bulk copy (1 KB)", "L2 flag-in-data words"};
