@@ -120,6 +120,12 @@ typedef struct {
    re-triangularised (QR), and only the trailing (n-l) x (n-l) pencil is reduced to HT form.
    The leading l x l part is already in generalised Schur form (T's first l columns are 0). */
 #define HT_FLAG_DEFLATE_ZERO_COLUMNS 2u
+/* Solve-path selection (verification): the panel's triangular solves (P3, IR corrections) run
+   on 256-row blocks with 4-CTA clusters whenever every 256-row diagonal block of the panel's B
+   is well conditioned, else on 128-row blocks with 2-CTA clusters.  This flag forces the
+   128-row path for every panel; the result agrees to rounding (the same recurrence, blocked
+   differently). */
+#define HT_FLAG_SOLVE128 4u
 
 /* Statistics of one reduction (the paper's Table 3/4 columns). */
 typedef struct {

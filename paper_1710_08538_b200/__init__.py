@@ -25,6 +25,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
 HT_OK = 0
 HT_FLAG_GENERAL_B = 1
 HT_FLAG_DEFLATE_ZERO_COLUMNS = 2
+HT_FLAG_SOLVE128 = 4
 ERRORS = {-1: "HT_EARG_N", -2: "HT_EARG_A", -3: "HT_EARG_B", -4: "HT_EARG_Q", -5: "HT_EARG_Z",
           -6: "HT_EARG_WANTQ", -7: "HT_EARG_WANTZ", -8: "HT_EARG_NB", -9: "HT_EARG_OPT",
           1: "HT_ENONFINITE", 2: "HT_ECUDA", 3: "HT_ENOMEM", 4: "HT_ENUMERIC", 5: "HT_ENCCL"}

@@ -1106,7 +1106,7 @@ int validate(int64_t n, const double *A, int64_t lda, const double *B, int64_t l
     if (wantz != 0 && wantz != 1) return HT_EARG_WANTZ;
     if (opt && opt->nb > ((int64_t)1 << 20)) return HT_EARG_NB;
     if (opt && (opt->n_force_ir_fail < 0 || (opt->n_force_ir_fail > 0 && !opt->force_ir_fail))) return HT_EARG_OPT;
-    if (opt && (opt->flags & ~(HT_FLAG_GENERAL_B | HT_FLAG_DEFLATE_ZERO_COLUMNS))) return HT_EARG_OPT;
+    if (opt && (opt->flags & ~(HT_FLAG_GENERAL_B | HT_FLAG_DEFLATE_ZERO_COLUMNS | HT_FLAG_SOLVE128))) return HT_EARG_OPT;
     if (opt && (opt->row_begin != 0 || opt->row_end != 0) &&
         (opt->row_begin < 0 || opt->row_end > n || opt->row_begin > opt->row_end))
         return HT_EARG_OPT;
@@ -1348,7 +1348,8 @@ int reduce_body(Run &R, const ht_options *opt)
             pa.part = w->part; pa.pw = (int)nb + 8;
             pa.yll = w->yll; pa.yll_exp = w->yll_exp; pa.bexp = w->bexp; pa.epoch = w->epoch;
             pa.Dinv = w->Dinv; pa.Bt = w->Bt; pa.ldbt = n; pa.dsafe = w->dsafe; pa.ypart = w->ypart;
-            pa.Dinv4 = w->Dinv4; pa.dsafe4 = w->dsafe4; pa.h_dsafe4 = w->h_dsafe4;
+            pa.Dinv4 = (flags & HT_FLAG_SOLVE128) ? nullptr : w->Dinv4;  // null: 128-row solve only
+            pa.dsafe4 = w->dsafe4; pa.h_dsafe4 = w->h_dsafe4;
             pa.ypartB = w->ypartB; pa.BV = w->BV; pa.vbx = vv + 7 * N;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;

@@ -152,6 +152,23 @@ def test_headline_nb128_vs_oracle_T(cfg, n, fails):
                                                   "absH_vs_oracleT": dh, "absT_vs_oracleT": dt})
 
 
+@pytest.mark.parametrize("cfg,n,fails", [(3, 1300, ()), (3, 1300, (500, 901)), (5, 900, ())])
+def test_solve_paths_agree(cfg, n, fails):
+    """The panel's solves on 256-row blocks / 4-CTA clusters (default when the diagonal blocks
+    are safe) and on 128-row blocks / 2-CTA clusters (HT_FLAG_SOLVE128) are the same recurrence
+    blocked differently: both match Oracle-T, and each other to rounding."""
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    nb = ht_inputs.CONFIGS[cfg]["nb"] if n > 1000 else 128
+    r4 = gpu_reduce(A, B, nb=nb, force_ir_fail=fails)
+    r2 = gpu_reduce(A, B, nb=nb, force_ir_fail=fails, flags=ht.HT_FLAG_SOLVE128)
+    Hr, Tr = oracle_T_cached(cfg, n)
+    for H, T, Q, Z, _ in (r4, r2):
+        check_props(A, B, H, T, Q, Z)
+        check_parity(A, B, H, T, Hr, Tr)
+    for x, y, nrm in zip(r4[:4], r2[:4], (C.fro(A), C.fro(B), 1.0, 1.0)):
+        assert np.max(np.abs(np.abs(x) - np.abs(y))) <= 1e-11 * nrm
+
+
 def test_flop_accounting_within_15pct_of_model():
     """SURVEY §8(c) pin: instrumented executed flops (per-launch formulas, the paper's
     interposition convention P:2161-2162) within +-15% of the App. A model -- catches
