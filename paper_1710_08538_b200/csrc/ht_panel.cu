@@ -295,17 +295,17 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned long long *bar, unsign
 }
 __device__ __forceinline__ void ll_put(unsigned long long *w, double x, unsigned epoch)
 {
+    // one 16-byte store; each 8-byte word is single-copy atomic and carries the epoch itself
     const unsigned long long b = (unsigned long long)__double_as_longlong(x);
     const unsigned long long e = (unsigned long long)epoch << 32;
-    st_volatile64(w, e | (b & 0xffffffffull));
-    st_volatile64(w + 1, e | (b >> 32));
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(e | (b & 0xffffffffull)), "l"(e | (b >> 32))
+                 : "memory");
 }
 __device__ __forceinline__ double ll_get(const unsigned long long *w, unsigned epoch)
 {
     unsigned long long lo, hi;
     while (true) {
-        lo = ld_volatile64(w);
-        hi = ld_volatile64(w + 1);
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
         if ((unsigned)(lo >> 32) == epoch && (unsigned)(hi >> 32) == epoch) break;
         __nanosleep(64);  // back off: the pollers of all waiting CTAs share L2 with the chain (0/16/256 ns: same solve time)
     }
@@ -801,7 +801,7 @@ __device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, u
         }
         if (q != 0) {
             if (C.tid == 0) snd[2 * T4] = (double)E;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy
+            if (C.tid < T4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // writers: generic -> bulk copy
             __syncthreads();
             if (C.tid == 0) {
                 unsigned dst, mbr;
@@ -810,7 +810,8 @@ __device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, u
                              : "r"((unsigned)__cvta_generic_to_shared(rcv + (q - 1) * SZ)), "r"(0));
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(mbr)
                              : "r"((unsigned)__cvta_generic_to_shared(&g_sm.mbar4)), "r"(0));
-                asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(mbr),
+                // relaxed: rank 0 needs only the copied bytes (complete_tx), not this thread's other writes
+                asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(mbr),
                              "r"(SZ * 8) : "memory");
                 asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                              ::"r"(dst), "r"(src), "r"(SZ * 8), "r"(mbr) : "memory");
@@ -851,14 +852,10 @@ __device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, u
             }
             if (ex) xv = ldexp(xv, -ex);
             e += ex;
-            if (C.tid < h) {
-                a.vy[r0 + C.tid] = xv;
-                ll_put(a.yll + 2 * (r0 + C.tid), xv, epoch);
-            }
-            if (C.tid == 0) {
-                a.bexp[b] = e;
-                st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
-            }
+            if (C.tid == 0) st_volatile64(a.yll_exp + b, ((unsigned long long)epoch << 32) | (unsigned)e);
+            if (C.tid < h) ll_put(a.yll + 2 * (r0 + C.tid), xv, epoch);  // the chain's hand-over first
+            if (C.tid < h) a.vy[r0 + C.tid] = xv;
+            if (C.tid == 0) a.bexp[b] = e;
         }
         // the messages' buffers are reused by the next block of this cluster
         cl.sync();
