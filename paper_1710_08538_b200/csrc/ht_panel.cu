@@ -817,8 +817,15 @@ __device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, u
                              ::"r"(dst), "r"(src), "r"(SZ * 8), "r"(mbr) : "memory");
             }
         } else {
-            // (5) rank 0: combine, rescale if needed, publish y~_b
-            mbar_wait_parity(&g_sm.mbar4, C.mb4par);
+            // (5) rank 0: combine, rescale if needed, publish y~_b.  The messages are bulk copies into
+            // this CTA's shared memory counted on its own mbarrier: a CTA-scope wait suffices
+            {
+                const unsigned ma = (unsigned)__cvta_generic_to_shared(&g_sm.mbar4);
+                unsigned done = 0;
+                while (!done)
+                    asm volatile("{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+                                 : "=r"(done) : "r"(ma), "r"(C.mb4par) : "memory");
+            }
             C.mb4par ^= 1u;
             int ei[3];
             int Eall = E;
