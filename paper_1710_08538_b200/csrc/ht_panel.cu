@@ -307,7 +307,10 @@ __device__ __forceinline__ double ll_get(const unsigned long long *w, unsigned e
     while (true) {
         asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
         if ((unsigned)(lo >> 32) == epoch && (unsigned)(hi >> 32) == epoch) break;
-        __nanosleep(64);  // back off: the pollers of all waiting CTAs share L2 with the chain (0/16/256 ns: same solve time)
+#ifndef HT_POLL_NS
+#define HT_POLL_NS 64
+#endif
+        if (HT_POLL_NS > 0) __nanosleep(HT_POLL_NS);  // back off: the pollers of all waiting CTAs share L2 with the chain
     }
     return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
@@ -317,7 +320,7 @@ __device__ __forceinline__ int ll_get_exp(const unsigned long long *w, unsigned 
     while (true) {
         v = ld_volatile64(w);
         if ((unsigned)(v >> 32) == epoch) break;
-        __nanosleep(64);
+        if (HT_POLL_NS > 0) __nanosleep(HT_POLL_NS);
     }
     return (int)(unsigned)(v & 0xffffffffull);
 }
