@@ -41,6 +41,13 @@ struct Work {
     cudaStream_t own_stream = nullptr;
     double *U = nullptr, *V = nullptr, *Y = nullptr, *S = nullptr, *T = nullptr;
     double *vec = nullptr, *part = nullptr;
+    // U, V, Y, BV, S, T and the panel's n-vectors live in ONE allocation (`hot`, hot_bytes) so
+    // that the panel launch can mark it L2-persisting (ht_panel_run): the fused sweep streams
+    // the trailing A and B (~0.5 GB per column) and the side streams stream A, Q, Z, which
+    // otherwise evict these small, reused arrays between columns (every access then pays HBM
+    // latency on the panel's latency-bound phases).
+    double *hot = nullptr;
+    size_t hot_bytes = 0;
     unsigned long long *yll = nullptr, *yll_exp = nullptr;
     int *bexp = nullptr;
     unsigned epoch = 0;
@@ -180,7 +187,9 @@ struct Timer {
 
 void work_free(Work &w)
 {
-    double **dp[] = {&w.U, &w.V, &w.Y, &w.S, &w.T, &w.vec, &w.part, &w.VW, &w.UW, &w.Vhat, &w.tau,
+    w.U = w.V = w.Y = w.S = w.T = w.vec = w.BV = nullptr;  // carved out of w.hot
+    w.hot_bytes = 0;
+    double **dp[] = {&w.hot, &w.part, &w.VW, &w.UW, &w.Vhat, &w.tau,
                      &w.Gm, &w.Tm, &w.Wt, &w.Qw, &w.tmp, &w.W1, &w.W2, &w.UR, &w.fscr, &w.d_scal,
                      &w.VhatL, &w.QwL, &w.TmL, &w.tauL, &w.WtL, &w.fscrL, &w.W1A, &w.W2A, &w.W1Q, &w.W2Q,
                      &w.VhatR, &w.QwR, &w.TmR, &w.tauR, &w.WtR, &w.VhatB, &w.QwB, &w.TmB, &w.tauB, &w.WtB};
@@ -207,8 +216,6 @@ void work_free(Work &w)
     w.ypart = nullptr;
     if (w.ypartB) cudaFree(w.ypartB);
     w.ypartB = nullptr;
-    if (w.BV) cudaFree(w.BV);
-    w.BV = nullptr;
     if (w.dsafe) cudaFree(w.dsafe);
     w.Dinv = nullptr;
     w.dsafe = nullptr;
@@ -255,9 +262,14 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     const int64_t N = std::max<int64_t>(n, 8), NB = std::max<int64_t>(nb, 1);
     TRY(ht_panel_max_blocks(&w.gmax));
     const size_t nnb = (size_t)N * NB, nb2 = (size_t)NB * NB;
-    TRY(dalloc(&w.U, nnb)); TRY(dalloc(&w.V, nnb)); TRY(dalloc(&w.Y, nnb));
-    TRY(dalloc(&w.S, nb2)); TRY(dalloc(&w.T, nb2));
-    TRY(dalloc(&w.vec, 8 * (size_t)N));
+    {
+        auto r32 = [](size_t c) { return (c + 31) & ~(size_t)31; };  // 256-byte aligned pieces
+        const size_t a = r32(nnb), b = r32(nb2), cnt = 4 * a + 2 * b + r32(8 * (size_t)N);
+        TRY(dalloc(&w.hot, cnt));
+        w.hot_bytes = cnt * sizeof(double);
+        w.U = w.hot; w.V = w.U + a; w.Y = w.V + a; w.BV = w.Y + a;
+        w.S = w.BV + a; w.T = w.S + b; w.vec = w.T + b;
+    }
     TRY(dalloc(&w.part, 2 * (size_t)w.gmax * (NB + 8)));
     const size_t nblk = (size_t)(N / 64 + 4);
     if (cudaMalloc((void **)&w.yll, 2 * (size_t)N * sizeof(unsigned long long)) != cudaSuccess) return HT_ENOMEM;
@@ -318,7 +330,6 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     TRY(dalloc(&w.Bt, (size_t)N * (size_t)N));
     TRY(dalloc(&w.ypart, (size_t)(N / 256 + 2) * (size_t)N));
     TRY(dalloc(&w.ypartB, (size_t)(N / 256 + 2) * (size_t)N));
-    TRY(dalloc(&w.BV, nnb));
     if (cudaMalloc((void **)&w.dsafe, (size_t)(N / 128 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     TRY(dalloc(&w.Dinv4, (size_t)(N / 256 + 2) * 256 * 256));
     if (cudaMalloc((void **)&w.dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
@@ -1351,6 +1362,7 @@ int reduce_body(Run &R, const ht_options *opt)
             pa.Dinv4 = (flags & HT_FLAG_SOLVE128) ? nullptr : w->Dinv4;  // null: 128-row solve only
             pa.dsafe4 = w->dsafe4; pa.h_dsafe4 = w->h_dsafe4;
             pa.ypartB = w->ypartB; pa.BV = w->BV; pa.vbx = vv + 7 * N;
+            pa.hot = w->hot; pa.hot_bytes = w->hot_bytes;
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;

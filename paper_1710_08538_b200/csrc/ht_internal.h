@@ -96,6 +96,8 @@ struct PanelArgs {
     double *ypartB;     // the same for B x
     double *BV;         // n x nb: B v_i of the panel's right reflectors (absolute row index)
     double *vbx;        // n-vector: B x of the current solve
+    void *hot;          // U, V, Y, BV, S, T, n-vectors: one allocation, L2-persisting for the panel
+    size_t hot_bytes;
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used
 };
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks);

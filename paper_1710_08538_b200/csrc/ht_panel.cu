@@ -26,6 +26,9 @@
 // off-diagonal solve tiles) are issued with many independent loads per thread.
 #include <cooperative_groups.h>
 #include <vector>
+#include <algorithm>
+#include <mutex>
+#include <cstdlib>
 #include "ht_common.cuh"
 #include "ht_internal.h"
 
@@ -106,27 +109,39 @@ struct Ctx {
     __device__ void putpart(int c, double v) { part[ph & 1][(size_t)c * G + bid] = v; }
     __device__ double *curpart() { return part[ph & 1]; }
 
+    // The helpers below are latency-bound (a CTA owns ~n/148 rows, k <= nb columns): each
+    // one issues ALL loads of a batch before the first use (one memory round trip per
+    // batch instead of one per loop iteration), with fixed summation orders (deterministic).
+    //
     // out[c] = sum over own rows of X(r,c) * vloc[r - rb0], c < ncols -> partial (off + c).
-    // Warps take 4 columns at a time and issue all their loads before summing
-    // (memory-level parallelism); lane partials go through shared staging.
+    // Warps take 8 columns, lanes 2 x 32 rows per batch; lane partials through shared staging.
     __device__ void coltdot(const double *X, int64_t ldx, int ncols, int off)
     {
         double *stg = g_dyn;  // ncols x 33
-        for (int c0 = warp * 4; c0 < ncols; c0 += NWP * 4) {
-            double acc[4];
+        constexpr int CU = 8;
+        for (int cb = warp * CU; cb < ncols; cb += NWP * CU) {
+            double acc[CU];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = 0.0;
-            for (int rl = lane; rl < nr; rl += 32) {
-                double xv[4];
+            for (int u = 0; u < CU; ++u) acc[u] = 0.0;
+            for (int r0 = 0; r0 < nr; r0 += 64) {
+                double xv[2][CU], vv[2];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) xv[u] = (c0 + u < ncols) ? X[(size_t)(c0 + u) * ldx + rb0 + rl] : 0.0;
-                const double vv = g_sm.vloc[rl];
+                for (int h = 0; h < 2; ++h) {
+                    const int rl = r0 + 32 * h + lane;
+                    const bool ok = rl < nr;
+                    vv[h] = ok ? g_sm.vloc[rl] : 0.0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc[u] = fma(xv[u], vv, acc[u]);
+                    for (int u = 0; u < CU; ++u)
+                        xv[h][u] = (ok && cb + u < ncols) ? X[(size_t)(cb + u) * ldx + rb0 + rl] : 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < CU; ++u) acc[u] = fma(xv[h][u], vv[h], acc[u]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (c0 + u < ncols) stg[(c0 + u) * 33 + lane] = acc[u];
+            for (int u = 0; u < CU; ++u)
+                if (cb + u < ncols) stg[(cb + u) * 33 + lane] = acc[u];
         }
         __syncthreads();
         for (int c = tid; c < ncols; c += PNT) {
@@ -137,19 +152,38 @@ struct Ctx {
         }
         __syncthreads();
     }
-    // returns (in g_dyn[rl]) sum_c X(rb0+rl, c) * coef[c] for own rows; all warps split the columns.
+    // returns (in g_dyn[rl]) sum_c X(rb0+rl, c) * coef[c] for own rows; warps split the
+    // columns (c = warp + NWP t), lanes take 2 x 32 rows; 8 columns x 2 rows of loads in flight.
     __device__ void rowgemv(const double *X, int64_t ldx, int ncols, const double *coef)
     {
         double *stg = g_dyn + TB * 4;  // NWP x RBMAX
-        for (int rc = 0; rc < nr; rc += 32) {
-            const int rl = rc + lane;
-            double s = 0.0;
-            if (rl < nr) {
-                const double *xp = X + rb0 + rl;
-#pragma unroll 4
-                for (int c = warp; c < ncols; c += NWP) s += xp[(size_t)c * ldx] * coef[c];
+        constexpr int CU = 8;
+        for (int rc = 0; rc < nr; rc += 64) {
+            double s[2] = {0.0, 0.0};
+            for (int c0 = warp; c0 < ncols; c0 += NWP * CU) {
+                double xs[2][CU];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rl = rc + 32 * h + lane;
+#pragma unroll
+                    for (int t = 0; t < CU; ++t) {
+                        const int c = c0 + NWP * t;
+                        xs[h][t] = (rl < nr && c < ncols) ? X[(size_t)c * ldx + rb0 + rl] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < CU; ++t) {
+                    const int c = c0 + NWP * t;
+                    const double cf = c < ncols ? coef[c] : 0.0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) s[h] = fma(xs[h][t], cf, s[h]);
+                }
             }
-            stg[warp * RBMAX + rl] = s;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rl = rc + 32 * h + lane;
+                if (rl < RBMAX) stg[warp * RBMAX + rl] = s[h];
+            }
         }
         __syncthreads();
         for (int rl = tid; rl < nr; rl += PNT) {
@@ -161,23 +195,24 @@ struct Ctx {
         __syncthreads();
     }
     // after a grid sync: dst[c] = sum_b part[b][off + c]  (fixed order: deterministic).
-    // Warps take 2 columns at a time, lanes split the CTA partials; all loads of a lane
+    // Warps take 4 columns at a time, lanes split the CTA partials; all loads of a lane
     // are issued before the sums (the partials live in L2: latency, not bandwidth, bound).
     __device__ void gather(double *dst, int ncols, int off)
     {
         const double *pp = curpart() + (size_t)off * G;
         constexpr int MAXB = 8;  // G <= 256 CTAs
-        for (int c0 = warp * 2; c0 < ncols; c0 += NWP * 2) {
-            double v[2][MAXB];
+        constexpr int CU = 4;
+        for (int c0 = warp * CU; c0 < ncols; c0 += NWP * CU) {
+            double v[CU][MAXB];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < CU; ++u)
 #pragma unroll
                 for (int q = 0; q < MAXB; ++q) {
                     const int b = lane + 32 * q;
                     v[u][q] = (b < G && c0 + u < ncols) ? __ldcg(pp + (size_t)(c0 + u) * G + b) : 0.0;
                 }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < CU; ++u) {
                 double t = 0.0;
 #pragma unroll
                 for (int q = 0; q < MAXB; ++q) t += v[u][q];
@@ -961,7 +996,7 @@ __device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int
 // are dealt round-robin to the CTAs; inside an item every warp streams 16 columns with
 // 16-byte loads over all 256 rows (16 independent loads in flight per lane), so each
 // SM keeps ~128 KB of loads outstanding.  Item partial sums go to ypart[cc][r]
-// (cc = column chunk) and are added in a fixed order by tiled_sum() after a grid sync
+// (cc = column chunk) and are added in a fixed order by tiled_sum2() after a grid sync
 // (deterministic).
 constexpr int TRT = 256, TCW = 256;
 struct TileGeom {
@@ -1107,13 +1142,44 @@ __device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_
     __syncthreads();
 }
 
-// y(r) = sum of the item partials of row r (after a grid sync), fixed order.
-__device__ __forceinline__ double tiled_sum(const Ctx &C, const TileGeom &tg, int64_t r, const double *yp)
+// Both fused-sweep row sums of the own rows: f(rl, sum of A's item partials, sum of B's).
+// Eight threads per row split the column chunks (all their loads issued at once) and combine
+// by a fixed xor-shuffle tree (deterministic); 64 rows per pass.
+template <class F>
+__device__ __forceinline__ void tiled_sum2(const Ctx &C, const TileGeom &ta, const TileGeom &tb, const double *ya,
+                                           const double *yb, F f)
 {
-    const int rb = (int)((r - tg.r_al) / TRT);
-    double t = 0.0;
-    for (int cc = tg.cc_min(rb); cc < tg.ncc; ++cc) t += __ldcg(yp + (size_t)cc * C.n + r);
-    return t;
+    constexpr int SUB = 8, PER = 8;
+    const int sub = C.tid & (SUB - 1);
+    for (int rl0 = 0; rl0 < C.nr; rl0 += PNT / SUB) {
+        const int rl = rl0 + C.tid / SUB;
+        const bool ok = rl < C.nr;
+        const int64_t r = C.rb0 + rl;
+        const int ca = ok ? ta.cc_min((int)((r - ta.r_al) / TRT)) : 0;
+        const int cb = ok ? tb.cc_min((int)((r - tb.r_al) / TRT)) : 0;
+        double sa = 0.0, sb = 0.0;
+        const int nccm = ta.ncc > tb.ncc ? ta.ncc : tb.ncc;
+        for (int c0 = 0; c0 < nccm; c0 += SUB * PER) {  // one pass for n <= 16384
+            double va[PER], vb[PER];
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int cc = c0 + sub + SUB * e;
+                va[e] = (ok && cc >= ca && cc < ta.ncc) ? __ldcg(ya + (size_t)cc * C.n + r) : 0.0;
+                vb[e] = (ok && cc >= cb && cc < tb.ncc) ? __ldcg(yb + (size_t)cc * C.n + r) : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                sa += va[e];
+                sb += vb[e];
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < SUB; o <<= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+        if (ok && sub == 0) f(rl, sa, sb);
+    }
 }
 
 __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ PanelArgs a)
@@ -1296,31 +1362,20 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             grid.sync();
             mark(4);
             if (k > 0) C.rowgemv(a.BV, n, k, g_sm.sv2);  // (B V) z for own rows
-            for (int rl = C.tid; rl < C.nr; rl += PNT) {
+            tiled_sum2(C, tga, tgb, a.ypart, a.ypartB, [&](int rl, double ax, double bx) {
                 const int64_t r = C.rb0 + rl;
-                const double bx = tiled_sum(C, tgb, r, a.ypartB);
-                a.vw[r] = tiled_sum(C, tga, r, a.ypart);
+                a.vw[r] = ax;
                 a.vbx[r] = bx;
-                if (k > 0) a.vw2[r] = bx - g_dyn[rl];  // w2 = B w
-            }
+                if (k > 0) {
+                    const double w2 = bx - g_dyn[rl];  // w2 = B w
+                    a.vw2[r] = w2;
+                    g_sm.vloc[rl] = w2;
+                }
+            });
             if (accepted) break;  // k = 0
             __syncthreads();
             C.ph++;
-            {   // partial U^T w2
-                double *stg = g_dyn;
-                for (int c = C.warp; c < ku; c += NWP) {
-                    double s = 0.0;
-#pragma unroll 4
-                    for (int64_t r = C.rb0 + C.lane; r < C.rb1; r += 32) s += U[(size_t)c * n + r] * a.vw2[r];
-                    stg[c * 33 + C.lane] = s;
-                }
-                __syncthreads();
-                for (int c = C.tid; c < ku; c += PNT) {
-                    double t = 0.0;
-                    for (int l = 0; l < 32; ++l) t += stg[c * 33 + l];
-                    C.putpart(c, t);
-                }
-            }
+            C.coltdot(U, n, ku, 0);  // partial U^T w2
             grid.sync();
             mark(7);
             // r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:)
@@ -1596,6 +1651,36 @@ int ht_panel_max_blocks(int *nblocks_out)
     return 0;
 }
 
+// L2 persisting window for `bytes` of panel workspace: sets the device's persisting carve-out
+// once (min(bytes, 3/8 of L2, the device maximum)) and returns the window size and hit ratio.
+// HT_NO_L2PERSIST=1 (development) disables it.
+int ht_l2_persist_window(size_t bytes, size_t *win, float *hit)
+{
+    static const bool off = getenv("HT_NO_L2PERSIST") != nullptr;
+    *win = 0;
+    *hit = 0.f;
+    if (off) return 0;
+    int dev = 0, l2 = 0, maxp = 0, maxw = 0;
+    HT_CUDA_TRY(cudaGetDevice(&dev));
+    HT_CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    HT_CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    HT_CUDA_TRY(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    if (maxp <= 0 || maxw <= 0) return 0;
+    const size_t carve = std::min<size_t>({(size_t)l2 / 8 * 3, (size_t)maxp, bytes});
+    static std::mutex mu;
+    static size_t have[64] = {0};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (have[dev & 63] < carve) {
+            HT_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+            have[dev & 63] = carve;
+        }
+    }
+    *win = std::min<size_t>(bytes, (size_t)maxw);
+    *hit = (float)std::min(1.0, (double)carve / (double)*win);
+    return 0;
+}
+
 int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
 {
     const int64_t M = a->n - a->s0 - 1;
@@ -1697,7 +1782,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     cfg.blockDim = dim3(PNT);
     cfg.dynamicSmemBytes = DYN_DOUBLES * sizeof(double);
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;
@@ -1706,6 +1791,21 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = nocl ? 1 : 2;
+    // The panel's small arrays (U, V, Y, B V, S, T, n-vectors; one allocation) are re-read by
+    // every column's latency-bound phases while the fused sweep streams ~0.5 GB of A and B per
+    // column (and the side streams stream A, Q, Z): an L2-persisting access-policy window keeps
+    // them on chip.  The persisting carve-out is sized once per device (at most 3/8 of L2).
+    size_t win = 0;
+    float hit = 0.f;
+    if (a->hot && a->hot_bytes && ht_l2_persist_window(a->hot_bytes, &win, &hit) == 0 && win > 0) {
+        at[cfg.numAttrs].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[cfg.numAttrs].val.accessPolicyWindow.base_ptr = a->hot;
+        at[cfg.numAttrs].val.accessPolicyWindow.num_bytes = win;
+        at[cfg.numAttrs].val.accessPolicyWindow.hitRatio = hit;
+        at[cfg.numAttrs].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[cfg.numAttrs].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs++;
+    }
     HT_CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_kernel, *a));
     return 0;
 }
