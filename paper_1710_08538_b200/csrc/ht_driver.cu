@@ -1412,9 +1412,10 @@ int reduce_body(Run &R, const ht_options *opt)
         if (prof_on) {
             double hp[16];
             HT_CUDA_TRY(cudaMemcpy(hp, ptime, sizeof(hp), cudaMemcpyDeviceToHost));
-            const char *names[8] = {"P1", "P2+trsv", "P3 rest", "P4 r+IR", "P5 A*v", "P5 Y", "P4 w", "P4 B*w"};
+            const char *names[16] = {"P1.sync2", "P2+trsv", "P3 rest", "P4 r+IR", "P4 sweep", "P5", "P4 VTx,TVTx", "P4 sums+UTw2",
+                                     "P1.Yv", "P1.UTa", "P1.sync1", "P1.gather", "P1.S^T", "P1.U(S^T)", "P1.tail", ""};
             fprintf(stderr, "[ht profile] panel phases (s):");
-            for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.3f", names[i], hp[i]);
+            for (int i = 0; i < 15; ++i) fprintf(stderr, " %s=%.4f", names[i], hp[i]);
             fprintf(stderr, "\n");
         }
         if (fprof) {

@@ -44,7 +44,13 @@ constexpr int C4 = 4;
 constexpr int NBMAX = 256; // max panel width supported
 constexpr int RBMAX = 256; // max own rows per CTA (uniform slabs)
 constexpr double BIG = 0x1p256;
-constexpr int DYN_DOUBLES = TB * TB + 8 * TB;  // M tile / staging + trsv group partials (8 x TB)
+// Per-CTA shared-memory copies of S and T (packed upper triangles, column c at c(c+1)/2) for
+// panels of width <= STC_NB solved by trsv4: every column's small mat-vecs with S and T then
+// read shared memory instead of L2 (each was a few dependent L2 round trips per column).  They
+// sit above the staging areas of the phases (<= OFF_ST doubles); trsv_blocked's 128 x 128 tile
+// overlaps them, so the 128-row solve keeps S and T in global memory.
+constexpr int STC_NB = 128, STC_SZ = STC_NB * (STC_NB + 1) / 2, OFF_ST = 4608;
+constexpr int DYN_DOUBLES = (TB * TB + 8 * TB) > (OFF_ST + 2 * STC_SZ) ? (TB * TB + 8 * TB) : (OFF_ST + 2 * STC_SZ);
 
 struct __align__(16) PanelSmem {
     double sv1[NBMAX + 2];
@@ -54,6 +60,7 @@ struct __align__(16) PanelSmem {
     double svx[NBMAX + 2];   // V^T x of the current solve (kept for P5's V^T v)
     double vloc[RBMAX];      // own-row vector cache
     double red[32];
+    double pt[16];     // HT_PROFILE: per-phase seconds of CTA 0 (flushed to a.ptime at the end)
     double rhs[TB];
     double cbv[TB];
     double yrecv[TB];  // y~_{b+1} handed over by the partner CTA of the cluster (DSMEM)
@@ -276,6 +283,41 @@ struct Ctx {
 #pragma unroll 8
             for (int l = 0; l < 32; ++l) t += stg[o * 33 + l];
             out[o] = scale * t;
+        }
+        __syncthreads();
+    }
+    // trimv with M in shared memory, packed upper triangle (column c at c(c+1)/2): four threads
+    // per output (m <= 128 outputs per pass) each sum a strided quarter, combined by a fixed
+    // xor-shuffle tree (deterministic).  ~300 cycles instead of several L2 round trips.
+    template <bool TR>
+    __device__ void trimv_sm(const double *Mp, int m, const double *v, double *out, double scale = 1.0)
+    {
+        constexpr int TPO = 4;
+        for (int o0 = 0; o0 < m; o0 += PNT / TPO) {
+            const int o = o0 + tid / TPO, part = tid % TPO;
+            double s0 = 0.0, s1 = 0.0;
+            if (o < m) {
+                if (TR) {  // out[o] = sum_{i <= o} M(i, o) v[i]
+                    const double *col = Mp + o * (o + 1) / 2;
+                    int i = part;
+                    for (; i + TPO <= o; i += 2 * TPO) {
+                        s0 = fma(col[i], v[i], s0);
+                        s1 = fma(col[i + TPO], v[i + TPO], s1);
+                    }
+                    if (i <= o) s0 = fma(col[i], v[i], s0);
+                } else {   // out[o] = sum_{o <= c < m} M(o, c) v[c]
+                    int c = o + part;
+                    for (; c + TPO < m; c += 2 * TPO) {
+                        s0 = fma(Mp[c * (c + 1) / 2 + o], v[c], s0);
+                        s1 = fma(Mp[(c + TPO) * (c + TPO + 1) / 2 + o], v[c + TPO], s1);
+                    }
+                    if (c < m) s0 = fma(Mp[c * (c + 1) / 2 + o], v[c], s0);
+                }
+            }
+            double sum = s0 + s1;
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            if (part == 0 && o < m) out[o] = scale * sum;
         }
         __syncthreads();
     }
@@ -1198,16 +1240,27 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
     double *A = a.A;
     double *U = a.U, *V = a.V, *Y = a.Y, *S = a.S, *T = a.T;
     const int nb = a.nb;
+    // S, T cached in shared memory; re-derived from the launch parameters at every use (kept
+    // out of registers: the solve's tile loop runs at the 128-register limit)
+#define stc (a.solve4 && a.nb <= STC_NB)
+#define Ssm (g_dyn + OFF_ST)
+#define Tsm (g_dyn + OFF_ST + STC_SZ)
+    auto Sg = [&](int i, int c) -> double { return stc ? Ssm[c * (c + 1) / 2 + i] : S[(size_t)c * nb + i]; };
+    auto Tget = [&](int i, int c) -> double { return stc ? Tsm[c * (c + 1) / 2 + i] : T[(size_t)c * nb + i]; };
     unsigned epoch = a.epoch;
     int k = 0, failed = 0;
     long long ir_steps = 0, ir_cols = 0, rescales = 0;
     int ffi = 0;  // cursor into the forced-failure list
     const bool prof = a.ptime && C.bid == 0 && C.tid == 0;
-    unsigned long long tp = prof ? gtime() : 0ull;
-    auto mark = [&](int bin) {
+    unsigned long long tp = 0ull;
+    if (prof) {
+        for (int i = 0; i < 16; ++i) g_sm.pt[i] = 0.0;
+        tp = gtime();
+    }
+    auto mark = [&](int bin) {  // shared-memory accumulation: no global round trip per mark
         if (prof) {
             unsigned long long t = gtime();
-            a.ptime[bin] += (double)(t - tp) * 1e-9;
+            g_sm.pt[bin] += (double)(t - tp) * 1e-9;
             tp = t;
         }
     };
@@ -1219,6 +1272,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         for (int c = C.tid; c < k; c += PNT) g_sm.sv1[c] = (c == k - 1) ? 1.0 : V[(size_t)c * n + j0];
         __syncthreads();
         C.rowgemv(Y, n, k, g_sm.sv1);
+        mark(8);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
             const int64_t r = C.rb0 + rl;
             double a0 = A[(size_t)j0 * lda + r];
@@ -1227,11 +1281,16 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         }
         __syncthreads();
         C.coltdot(U, n, k, 0);
+        mark(9);
         grid.sync();
+        mark(10);
         C.gather(g_sm.sv2, k, 0);
         __syncthreads();
-        C.trimv<true>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, g_sm.sv2, g_sm.sv3);  // sv3 = S^T t
+        mark(11);
+        if (stc) C.trimv_sm<true>(Ssm, k, g_sm.sv2, g_sm.sv3); else C.trimv<true>(Sg, k, g_sm.sv2, g_sm.sv3);  // sv3 = S^T t
+        mark(12);
         C.rowgemv(U, n, k, g_sm.sv3);
+        mark(13);
         C.ph++;
         {
             double ss = 0.0;
@@ -1247,6 +1306,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             C.coltdot(U, n, k, 1);
             C.block_reduce_to_part(ss, 0);
         }
+        mark(14);
         grid.sync();
         mark(0);
         // ================= P2: left reflector (no barrier needed) ============
@@ -1269,7 +1329,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         // U^T u = scal * U^T a_tail + U(j0+1, :)^T   (u(j0+1) = 1)
         for (int c = C.tid; c < k; c += PNT) g_sm.sv2[c] = scal_u * g_sm.sv1[1 + c] + U[(size_t)c * n + j0 + 1];
         __syncthreads();
-        C.trimv<false>([&](int i, int c) { return S[(size_t)c * nb + i]; }, k, g_sm.sv2, g_sm.snew, -tau_u);
+        if (stc) C.trimv_sm<false>(Ssm, k, g_sm.sv2, g_sm.snew, -tau_u); else C.trimv<false>(Sg, k, g_sm.sv2, g_sm.snew, -tau_u);
         if (C.tid == 0) g_sm.snew[k] = tau_u;
         auto unew = [&](int64_t r) -> double {
             return (r < j0 + 1) ? 0.0 : (r == j0 + 1 ? 1.0 : __ldcg(&a.vx[r]) * scal_u);
@@ -1283,12 +1343,14 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         __syncthreads();
         if (C.bid == 0)
             for (int i = C.tid; i <= k; i += PNT) S[(size_t)k * nb + i] = g_sm.snew[i];
-        auto Sget = [&](int i, int c) -> double { return c == k ? g_sm.snew[i] : S[(size_t)c * nb + i]; };
+        if (stc)
+            for (int i = C.tid; i <= k; i += PNT) Ssm[k * (k + 1) / 2 + i] = g_sm.snew[i];
+        auto Sget = [&](int i, int c) -> double { return c == k ? g_sm.snew[i] : Sg(i, c); };
 
         // ================= P3: factored solve ==================================
         for (int c = C.tid; c < ku; c += PNT) g_sm.sv1[c] = (c == k) ? 1.0 : U[(size_t)c * n + j0 + 1];
         __syncthreads();
-        C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
+        if (stc) C.trimv_sm<false>(Ssm, ku, g_sm.sv1, g_sm.sv3); else C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
         if (a.solve4) trsv4(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch);
         else trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch, j0);
@@ -1307,7 +1369,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         grid.sync();
         C.gather(g_sm.sv1, k, 0);
         __syncthreads();
-        C.trimv<true>([&](int i, int c) { return T[(size_t)c * nb + i]; }, k, g_sm.sv1, g_sm.sv2);  // T^T (V^T y~)
+        if (stc) C.trimv_sm<true>(Tsm, k, g_sm.sv1, g_sm.sv2); else C.trimv<true>(Tget, k, g_sm.sv1, g_sm.sv2);  // T^T (V^T y~)
         C.rowgemv(V, n, k, g_sm.sv2);
         C.ph++;
         {
@@ -1351,11 +1413,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         bool this_col_ir = false;
         const TileGeom tga(p0, n, j0 + 1, n, false);  // A(s+1:n, j+1:n)
         const TileGeom tgb(p0, n, j0 + 1, n, true);   // B(s+1:n, j+1:n), upper part
-        auto Tget = [&](int i, int c) { return T[(size_t)c * nb + i]; };
         while (true) {
             C.gather(g_sm.svx, k, 2);  // V^T x
             __syncthreads();
-            if (k > 0) C.trimv<false>(Tget, k, g_sm.svx, g_sm.sv2);  // z = T V^T x
+            if (k > 0) { if (stc) C.trimv_sm<false>(Tsm, k, g_sm.svx, g_sm.sv2); else C.trimv<false>(Tget, k, g_sm.svx, g_sm.sv2); }  // z = T V^T x
             mark(6);
             tiled_matvec(C, tga, A, lda, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypart);
             tiled_matvec(C, tgb, a.B, a.ldb, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypartB);
@@ -1381,7 +1442,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             // r = sigma e1 - ((I - U S^T U^T) w2)(j0+1:)
             C.gather(g_sm.sv1, ku, 0);
             __syncthreads();
-            C.trimv<true>(Sget, ku, g_sm.sv1, g_sm.sv2);  // S_{k+1}^T t
+            if (stc) C.trimv_sm<true>(Ssm, ku, g_sm.sv1, g_sm.sv2); else C.trimv<true>(Sget, ku, g_sm.sv1, g_sm.sv2);  // S_{k+1}^T t
             C.rowgemv(U, n, ku, g_sm.sv2);
             C.ph++;
             const double sigma = ldexp(1.0, -emax);
@@ -1418,7 +1479,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             this_col_ir = true;
             C.gather(g_sm.sv1, ku, 1);  // U^T r_ext
             __syncthreads();
-            C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // S_{k+1} (U^T r)
+            if (stc) C.trimv_sm<false>(Ssm, ku, g_sm.sv1, g_sm.sv3); else C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // S_{k+1} (U^T r)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
             if (a.solve4)
@@ -1437,7 +1498,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             grid.sync();
             C.gather(g_sm.sv1, k, 0);
             __syncthreads();
-            C.trimv<true>(Tget, k, g_sm.sv1, g_sm.sv2);
+            if (stc) C.trimv_sm<true>(Tsm, k, g_sm.sv1, g_sm.sv2); else C.trimv<true>(Tget, k, g_sm.sv1, g_sm.sv2);
             C.rowgemv(V, n, k, g_sm.sv2);
             C.ph++;
             {
@@ -1494,10 +1555,16 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             g_sm.sv1[c] = vj + scal_v * (g_sm.svx[c] - vj * x1);
         }
         __syncthreads();
-        if (C.bid == 0) {
-            C.trimv<false>(Tget, k, g_sm.sv1, g_sm.sv2, -gam);
-            for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = g_sm.sv2[i];
-            if (C.tid == 0) T[(size_t)k * nb + k] = gam;
+        if (C.bid == 0 || stc) {  // every CTA keeps its copy of T (all compute the new column)
+            if (stc) C.trimv_sm<false>(Tsm, k, g_sm.sv1, g_sm.sv2, -gam); else C.trimv<false>(Tget, k, g_sm.sv1, g_sm.sv2, -gam);
+            if (C.bid == 0) {
+                for (int i = C.tid; i < k; i += PNT) T[(size_t)k * nb + i] = g_sm.sv2[i];
+                if (C.tid == 0) T[(size_t)k * nb + k] = gam;
+            }
+            if (stc) {
+                for (int i = C.tid; i < k; i += PNT) Tsm[k * (k + 1) / 2 + i] = g_sm.sv2[i];
+                if (C.tid == 0) Tsm[k * (k + 1) / 2 + k] = gam;
+            }
         }
         C.rowgemv(Y, n, k, g_sm.sv1);
         for (int rl = C.tid; rl < C.nr; rl += PNT) {
@@ -1513,7 +1580,12 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         __syncthreads();
         mark(5);
     }
+#undef stc
+#undef Ssm
+#undef Tsm
     grid.sync();
+    if (prof)
+        for (int i = 0; i < 16; ++i) a.ptime[i] += g_sm.pt[i];
     if (C.bid == 0 && C.tid == 0) {
         a.out[0] = k;
         a.out[1] = failed;
