@@ -48,6 +48,9 @@ struct Work {
     // latency on the panel's latency-bound phases).
     double *hot = nullptr;
     size_t hot_bytes = 0;
+    // wavefront factorization of staircase chains (ht_factor_run): epoch flags + ticket
+    int *wave_flags = nullptr, *wave_ticket = nullptr;
+    int wave_epoch = 0;
     unsigned long long *yll = nullptr, *yll_exp = nullptr;
     int *bexp = nullptr;
     unsigned epoch = 0;
@@ -195,6 +198,9 @@ void work_free(Work &w)
                      &w.VhatR, &w.QwR, &w.TmR, &w.tauR, &w.WtR, &w.VhatB, &w.QwB, &w.TmB, &w.tauB, &w.WtB};
     for (auto p : dp)
         if (*p) { cudaFree(*p); *p = nullptr; }
+    if (w.wave_flags) cudaFree(w.wave_flags);
+    if (w.wave_ticket) cudaFree(w.wave_ticket);
+    w.wave_flags = w.wave_ticket = nullptr;
     if (w.yll) cudaFree(w.yll);
     if (w.yll_exp) cudaFree(w.yll_exp);
     w.yll = nullptr; w.yll_exp = nullptr;
@@ -335,6 +341,10 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (cudaMalloc((void **)&w.dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
+    if (cudaMalloc((void **)&w.wave_flags, (size_t)w.ndesc * 8 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.wave_ticket, 2 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    cudaMemset(w.wave_flags, 0, (size_t)w.ndesc * 8 * sizeof(int));
+    w.wave_epoch = 0;
     w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
     if (cudaMalloc((void **)&w.d_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
     if (cudaMallocHost((void **)&w.h_fd, w.ndesc * sizeof(FactorDesc)) != cudaSuccess) return HT_ENOMEM;
@@ -346,6 +356,14 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     w.nbcap = NB;
     *out = &w;
     return 0;
+}
+
+// HT_NO_WAVE=1 (development): factor the R1/L1 staircase chains window by window (one CTA)
+// instead of as a wavefront (ht_factor_run).
+static bool no_wave()
+{
+    static const bool v = getenv("HT_NO_WAVE") != nullptr;
+    return v;
 }
 
 // Critical-stream phase profile (HT_PHASES=1, development only): the time between two
@@ -513,8 +531,11 @@ struct Run {
     // Factor the windows `ws` (descriptors `fds`, one per window) on stream `s` with the
     // window store `sto`, then form Qw = I - V T V^T for each (on `sf` if given: it waits
     // for the factorization through evF).
+    // wave: the descriptors are one staircase chain ([new rows; R of the previous window]),
+    // factored as a wavefront (ht_factor_run); the ticket is per store (main / side) so that
+    // chains on different streams may run concurrently.
     int factor_and_form(const std::vector<FactorDesc> &fds, const std::vector<Win> &ws, const Store &sto,
-                        cudaStream_t s, cudaStream_t sf = nullptr)
+                        cudaStream_t s, cudaStream_t sf = nullptr, bool wave = false)
     {
         const int nd = (int)fds.size();
         if (nd == 0) return 0;
@@ -531,7 +552,14 @@ struct Run {
         }
         HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
         tm.begin(s, s == st ? 7 : 2);
-        TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
+        if (wave && nd > 1 && !no_wave()) {
+            // flags are indexed by descriptor slot (fd_cur + i): distinct for concurrent chains
+            const int ep = ++w->wave_epoch;
+            TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp, w->wave_flags + (size_t)w->fd_cur * 8,
+                              w->wave_ticket + (sto.Vhat == w->Vhat ? 0 : 1), ep));
+        } else {
+            TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
+        }
         tm.end(s);
         if (s == st) ph.mark(st, 8);
         if (sf) {
@@ -783,7 +811,7 @@ struct Run {
             }
             HT_CUDA_TRY(cudaEventRecord(w->ev_fork, st));
             HT_CUDA_TRY(cudaStreamWaitEvent(w->side_stream, w->ev_fork, 0));
-            TRY(factor_and_form(fl, winsL, sl, w->side_stream));
+            TRY(factor_and_form(fl, winsL, sl, w->side_stream, nullptr, true));
             HT_CUDA_TRY(cudaEventRecord(w->ev_join, w->side_stream));
         }
 
@@ -808,14 +836,32 @@ struct Run {
                           w->tau + x.ot};
             if (i > 0) fd.dense = p - (int)ks;  // view: [ks new rows; L of the window above, reversed; 0]
             wl.push_back(ChainWin{w->Qw + x.oq, J + 1 + rb[i], x.p, {0, 0, 0}, {J + 1 + rb[i + 2], n, n}});
-            if (pipelined) {
+            if (pipelined && no_wave()) {
                 TRY(factor_and_form(std::vector<FactorDesc>{fd}, std::vector<Win>{x}, main_store(), st, sBq));
                 TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, n}}, {wl.back()}, 0));
             } else {
                 fds.push_back(fd);
             }
         }
-        if (pipelined) {
+        if (pipelined && !no_wave()) {
+            // The R1 chain as wavefront launches on st in groups of windows; sB forms each
+            // group's Qhat and applies the group to B (R2, chain order) while st factors the
+            // next group.  (One launch for the whole chain would leave B's R2 chain -- whose
+            // top slab passes every window -- exposed after it.)
+            static const int grp_env = getenv("HT_WAVE_GROUP") ? atoi(getenv("HT_WAVE_GROUP")) : 0;
+            const int grp = grp_env > 0 ? grp_env : 16;
+            for (int g0 = 0; g0 < r; g0 += grp) {
+                const int g1 = std::min(r, g0 + grp);
+                // a group's first window continues the chain: its input (the previous group's
+                // last R) is complete in stream order, so it needs no flag
+                std::vector<FactorDesc> fg(fds.begin() + g0, fds.begin() + g1);
+                std::vector<Win> wg(wins.begin() + g0, wins.begin() + g1);
+                std::vector<ChainWin> cg(wl.begin() + g0, wl.begin() + g1);
+                TRY(factor_and_form(fg, wg, main_store(), st, sBq, true));
+                TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, n}}, cg, 0));
+            }
+            TRY(dep(st, sBq, 11));
+        } else if (pipelined) {
             TRY(dep(st, sBq, 11));  // B's R2 chain done, all R1 windows formed
         } else {
             TRY(factor_and_form(fds, 0));

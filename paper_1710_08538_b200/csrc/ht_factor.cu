@@ -213,8 +213,36 @@ __device__ __forceinline__ void vt_times_panel(const FactorDesc &d, int i, int r
 // Q_0 Q_1 ...,  Q_b = I - V_b T_b V_b^T  (V_b = columns 32b..32b+31).  The off-diagonal
 // blocks of T are never formed: every consumer applies Q panel block by panel block
 // (ht_band_wy / ht_form_qhat, ht_chain.cu).  (The 512-thread leaf layout shares this code.)
+// Wavefront mode for staircase chains whose windows are [new rows; R of the previous window]
+// (R1: V2 top -> bottom, L1: U2 bottom -> top; sec. 3.3.1b, 3.3.2b).  Window i's column c
+// holds R_{i-1}(0..c, c) in its bottom rows, and left-looking panel b of window i reads only
+// R_{i-1}'s columns of panel b -- which window i-1 stores at the end of ITS panel b (later
+// reflectors of window i-1 never touch them).  So panel b of window i may start as soon as
+// (i-1, b) and (i, b-1) are done: a (windows + panels) wavefront instead of windows x panels.
+// Persistent CTAs take windows in order from an atomic ticket (a CTA only ever waits on a
+// lower ticket, which is already running: no deadlock) and publish "(i, b) stored" as an
+// epoch-valued flag (release after a fence; the waiter acquires, then a block barrier).
+struct WaveArgs {
+    int *flags;      // [nd][WF_NB] epoch flags, null = sequential mode (one CTA, windows in order)
+    int *ticket;     // zeroed before the launch
+    int epoch;
+};
+constexpr int WF_NB = 8;  // panels per window (q <= 256)
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <class L>
-__global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch)
+__global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch,
+                                                             const WaveArgs wa)
 {
     constexpr int FNT = L::NT, FNW = L::NW, RPT = L::RPT, TPW = L::TPW;
     constexpr bool WIDE = L::WIDE;
@@ -237,7 +265,15 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
     unsigned long long *fprof = g_fprof;
     unsigned long long fprof_t = fprof ? fclock() : 0ull;
 
-    for (int di = 0; di < nd; ++di) {
+    __shared__ int s_ticket;
+    auto next_window = [&](int cur) -> int {
+        if (!wa.flags) return cur + 1;
+        __syncthreads();
+        if (tid == 0) s_ticket = atomicAdd(wa.ticket, 1);
+        __syncthreads();
+        return s_ticket;
+    };
+    for (int di = next_window(-1); di < nd; di = next_window(di)) {
         const FactorDesc d = descs[di];
         const int p = d.p, q = d.q;
         // rows >= dense + c + 1 of view column c are exactly zero (staircase windows)
@@ -248,6 +284,11 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
         const int nblk = (q + PBW - 1) / PBW;
         for (int b = 0; b < nblk; ++b) {
             const int c0 = b * PBW, nc = min(PBW, q - c0);
+            if (wa.flags && di > 0) {  // wavefront: R_{i-1}'s columns of panel b are stored
+                if (tid == 0)
+                    while (ld_acquire_gpu(wa.flags + (size_t)(di - 1) * WF_NB + b) != wa.epoch) __nanosleep(64);
+                __syncthreads();
+            }
             // ---- load panel columns c0 .. c0+nc of the view (zero padding) ----
             {
                 constexpr int PER = (PBW * L::LDP + FNT - 1) / FNT;
@@ -257,7 +298,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
                 for (int e = 0; e < PER; ++e) {
                     const int idx = tid + e * FNT;
                     const int j = rowfast ? idx / L::LDP : idx % PBW, r = rowfast ? idx % L::LDP : idx / PBW;
-                    t[e] = (j < nc && r < p) ? d.W[(int64_t)r * rs + (int64_t)(c0 + j) * cs] : 0.0;
+                    t[e] = (j < nc && r < p) ? __ldcg(d.W + ((int64_t)r * rs + (int64_t)(c0 + j) * cs)) : 0.0;
                 }
 #pragma unroll
                 for (int e = 0; e < PER; ++e) {
@@ -836,6 +877,10 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
             }
             __threadfence_block();
             __syncthreads();
+            if (wa.flags && tid == 0) {  // publish: panel b's R columns (and V, T_b) are stored
+                __threadfence();
+                st_release_gpu(wa.flags + (size_t)di * WF_NB + b, wa.epoch);
+            }
             FPROF(5);
         }
         // the next window of this launch may read what this one wrote (its R): a block barrier
@@ -845,7 +890,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
 }
 
 template <class L>
-int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch)
+int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, const WaveArgs &wa, int grid)
 {
     const int smem = L::DOUBLES * (int)sizeof(double);
     static std::mutex mu;
@@ -855,7 +900,7 @@ int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gs
         return 0;
     });
     if (rc) return rc;
-    factor_qr_kernel<L><<<1, L::NT, smem, st>>>(d_descs, nd, gscratch);
+    factor_qr_kernel<L><<<grid, L::NT, smem, st>>>(d_descs, nd, gscratch, wa);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -873,11 +918,19 @@ int ht_factor_set_prof(unsigned long long *dev)
     return 0;
 }
 
-int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp)
+int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp, int *wave_flags,
+                  int *wave_ticket, int wave_epoch)
 {
     if (nd <= 0) return 0;
-    if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch);
-    if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch);
-    if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch);
+    WaveArgs wa{nullptr, nullptr, 0};
+    int grid = 1;
+    if (wave_flags && nd > 1) {
+        wa = WaveArgs{wave_flags, wave_ticket, wave_epoch};
+        HT_CUDA_TRY(cudaMemsetAsync(wave_ticket, 0, sizeof(int), st));
+        grid = nd < HT_WAVE_CTAS ? nd : HT_WAVE_CTAS;
+    }
+    if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch, wa, grid);
+    if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch, wa, grid);
+    if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch, wa, grid);
     return 4;  // HT_ENUMERIC: window taller than 512 rows (nb <= 256 guarantees p <= 512)
 }

@@ -53,7 +53,13 @@ int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const
                  const double *const *T, void *d_descs, void *h_descs);
 size_t ht_band_desc_size();
 
-int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp);
+// Window factorizations of `nd` descriptors.  wave_flags == null: one CTA, windows in order.
+// Otherwise the descriptors form a staircase chain ([new rows; R of the previous window]) and
+// are factored as a wavefront by HT_WAVE_CTAS persistent CTAs (ht_factor.cu): wave_flags holds
+// nd x 8 ints (epoch-valued, never reset), wave_ticket one int (zeroed on `st` here).
+constexpr int HT_WAVE_CTAS = 6;
+int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp,
+                  int *wave_flags = nullptr, int *wave_ticket = nullptr, int wave_epoch = 0);
 int ht_factor_set_prof(unsigned long long *dev);
 
 // panel kernel (ht_panel.cu)
