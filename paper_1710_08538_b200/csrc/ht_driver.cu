@@ -741,10 +741,15 @@ struct Run {
         static const int env = getenv("HT_SB_GRID") ? atoi(getenv("HT_SB_GRID")) : 0;
         return env;
     }
-    int side_grid() const
+    int side_grid() const  // CTAs of A's window applies while the critical chains run
     {
         static const int env = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 0;
-        return env > 0 ? env : (n >= 12288 ? 96 : 64);
+        return env > 0 ? env : (n >= 12288 ? 96 : 56);
+    }
+    int side_grid_qz() const  // the same for Q and Z
+    {
+        static const int env = getenv("HT_SIDE_GRID_QZ") ? atoi(getenv("HT_SIDE_GRID_QZ")) : 0;
+        return env > 0 ? env : side_grid();
     }
     int absorb(int64_t s0, int64_t k)
     {
@@ -893,7 +898,7 @@ struct Run {
                 ht_slab(0, n, P, q, &a0, &a1);
                 TRY(chain_on(sA, {ChainMat{A, lda, 0, a0, a1}}, wa, side_grid()));
             }
-            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, side_grid()));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, wa, side_grid_qz()));
         }
         TRY(wupdate(wx[1]));
         for (int q = part_begin(); q < part_end(); ++q) {
@@ -921,7 +926,7 @@ struct Run {
                 ht_slab(0, n, P, q, &a0, &a1);
                 TRY(chain_on(sA, {ChainMat{A, lda, 0, a0, a1}}, ws, side_grid()));
             }
-            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, side_grid()));
+            if (wz) TRY(chain_on(sQ, {ChainMat{Z, ldz, 0, qz0, qz1}}, ws, side_grid_qz()));
             ws.clear();
             return 0;
         };
@@ -1027,7 +1032,7 @@ struct Run {
             }
             std::vector<ChainWin> wlq = wlu;
             for (auto &x : wlq) x.lo[0] = 0;
-            if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, side_grid()));
+            if (wq) TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wlq, side_grid_qz()));
         }
         {
             // B(p0:p0+2k, J+1:n) (st) and A(p0:p0+2k, J:n) (sA):  X <- X - UR S^T (X^T UR)^T
@@ -1072,7 +1077,7 @@ struct Run {
             if (wq) {
                 std::vector<ChainWin> wq_ = ws;
                 for (auto &x : wq_) x.lo[0] = 0;
-                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, grid));
+                TRY(chain_on(sQ, {ChainMat{Q, ldq, 0, qz0, qz1}}, wq_, grid ? side_grid_qz() : 0));
             }
             ws.clear();
             return 0;
