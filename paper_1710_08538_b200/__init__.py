@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libht_b200.so")
+LIB_PATH = os.path.join(_HERE, "lib", os.environ.get("HT_DEV_LIBNAME", "libht_b200.so"))  # HT_DEV_LIBNAME: development variants only
 
 HT_OK = 0
 HT_FLAG_GENERAL_B = 1

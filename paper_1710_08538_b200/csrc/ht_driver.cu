@@ -1380,7 +1380,7 @@ int reduce_body(Run &R, const ht_options *opt)
         unsigned long long *ttr = nullptr;
         const int64_t tcol = getenv("HT_TRACE_COL") ? atoll(getenv("HT_TRACE_COL")) : -1;
         if (tcol >= 0) {
-            const size_t nt = (size_t)((n - 1 + 127) / 128 + 2) * 8;
+            const size_t nt = (size_t)((n - 1 + 63) / 64 + 4) * 8;  // 64-row units (trsv4r) or 128-row blocks
             HT_CUDA_TRY(cudaMalloc(&ttr_buf.p, nt * sizeof(unsigned long long)));
             ttr = (unsigned long long *)ttr_buf.p;
             HT_CUDA_TRY(cudaMemset(ttr, 0, nt * sizeof(unsigned long long)));
@@ -1481,7 +1481,7 @@ int reduce_body(Run &R, const ht_options *opt)
             TRY(ht_factor_set_prof(nullptr));
         }
         if (ttr) {
-            const int nbk = (int)((n - 1 + 127) / 128) + 2;
+            const int nbk = (int)((n - 1 + 63) / 64) + 4;
             std::vector<unsigned long long> h((size_t)nbk * 8);
             HT_CUDA_TRY(cudaMemcpy(h.data(), ttr, h.size() * 8, cudaMemcpyDeviceToHost));
             unsigned long long t0 = ~0ull;

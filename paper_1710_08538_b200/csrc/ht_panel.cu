@@ -67,6 +67,7 @@ struct __align__(16) PanelSmem {
     unsigned long long mbar;  // completes when the partner has written yrecv/erecv (TB remote arrivals)
     unsigned long long mbar4; // trsv4, cluster rank 0: the 3 partial-sum messages of a block have landed
     int ival[4];
+    int es4[4];        // trsv4r: exponents of the four 64-row slices of a fetched block
     int erecv;
 };
 
@@ -109,7 +110,7 @@ struct Ctx {
         part[0] = a.part;
         part[1] = a.part + (size_t)G * a.pw;
         ph = 0;
-        tbs = a.solve4 ? 256 : TB;
+        tbs = a.solve4 == 2 ? 64 : (a.solve4 ? 256 : TB);
     }
     // partials are stored index-major: (CTA b, index c) at part[ph][c * G + b], so a gather
     // reads contiguous CTA runs
@@ -950,6 +951,250 @@ __device__ void trsv4(Ctx &C, BaseF base, UnewF unew, int k, const double *z2, u
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 256-row flag-chained solve with the rows of a block split over four CTAs (trsv4r).
+// Same recurrence as trsv4,  y~_b = Dinv4_b rhs_b - sum_{c > b} Bt_bc y~_c  (Bt_bc = Dinv4_b B_bc),
+// but because Dinv4_b is the inverse of the whole 256 x 256 diagonal block, every ROW of y~_b
+// depends only on the blocks below it: the four 64-row slices (b, q) of a block are independent
+// work units.  Unit (b, q) holds rows 64q.. of the critical tile Bt_{b,b+1} in registers (64 x 256,
+// 32 doubles per thread), waits for all of y~_{b+1} (four published slices), folds its eight
+// column groups in shared memory and publishes its 64 rows with their own exponent -- no
+// cluster, no distributed-shared-memory combine step on the chain (a hop is one L2 hand-over
+// plus one register mat-vec).  Units u = 4 (Nb-1-b) + q go to CTA u mod G in increasing u; a
+// unit only waits on lower units, so the chain cannot deadlock.  Exponent words and bexp are
+// per 64-row slice (C.tbs = 64).
+__device__ __forceinline__ void tile64_load(double (&t)[32], const double *X, int w, int h, int tid)
+{
+    const int rr = 32 * ((tid >> 5) & 1) + (tid & 31), grp = tid >> 6;  // row of the slice, 8 column groups
+    const double *x = X + (size_t)(32 * grp) * T4 + rr;
+    if (rr < h && 32 * grp + 32 <= w) {  // full: unpredicated loads at immediate offsets (few registers)
+#pragma unroll
+        for (int u = 0; u < 32; ++u) t[u] = __ldcs(x + (size_t)u * T4);  // streamed once
+    } else {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) t[u] = (32 * grp + u < w && rr < h) ? __ldcs(x + (size_t)u * T4) : 0.0;
+    }
+}
+__device__ __forceinline__ double tile64_dot(const double (&t)[32], const double *ys, int tid)
+{
+    const double *y = ys + 32 * (tid >> 6);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int u = 0; u < 32; u += 4) {
+        s0 = fma(t[u], y[u], s0);
+        s1 = fma(t[u + 1], y[u + 1], s1);
+        s2 = fma(t[u + 2], y[u + 2], s2);
+        s3 = fma(t[u + 3], y[u + 3], s3);
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+// part pf (columns 8 pf .. 8 pf + 7 of the thread's 32) of a 64 x 256 slice tile: the streamed
+// tiles go through 8 registers at a time (the critical tile holds 32)
+constexpr int TPART = 8;
+__device__ __forceinline__ void tile64_load_part(double (&t)[TPART], const double *X, int w, int h, int tid, int pf)
+{
+    const int rr = 32 * ((tid >> 5) & 1) + (tid & 31), grp = tid >> 6, c0 = 32 * grp + TPART * pf;
+    const double *x = X + (size_t)c0 * T4 + rr;
+    if (rr < h && c0 + TPART <= w) {
+#pragma unroll
+        for (int u = 0; u < TPART; ++u) t[u] = __ldcs(x + (size_t)u * T4);
+    } else {
+#pragma unroll
+        for (int u = 0; u < TPART; ++u) t[u] = (c0 + u < w && rr < h) ? __ldcs(x + (size_t)u * T4) : 0.0;
+    }
+}
+__device__ __forceinline__ double tile64_dot_part(const double (&t)[TPART], const double *ys, int tid, int pf)
+{
+    const double *y = ys + 32 * (tid >> 6) + TPART * pf;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < TPART; u += 2) {
+        s0 = fma(t[u], y[u], s0);
+        s1 = fma(t[u + 1], y[u + 1], s1);
+    }
+    return s0 + s1;
+}
+// all hc rows of the published block cb into ys[], the four slice exponents into g_sm.es4
+__device__ __forceinline__ void fetch4r(const PanelArgs &a, int64_t p0, int cb, int hc, unsigned epoch, double *ys)
+{
+    const int64_t c0 = p0 + (int64_t)cb * T4;
+    const int tid = threadIdx.x;
+    if (tid < T4) ys[tid] = (tid < hc) ? ll_get(a.yll + 2 * (c0 + tid), epoch) : 0.0;
+    else if (tid < T4 + 4) {
+        const int q = tid - T4;
+        g_sm.es4[q] = (64 * q < hc) ? ll_get_exp(a.yll_exp + 4 * cb + q, epoch) : 0;
+    }
+    __syncthreads();
+}
+// The right-hand side of a solve, rhs(r) = base(r) - U(r, 0:k) z2(0:k) - unew(r) z2(k), in scalar
+// form (the solve is a separate, non-inlined function so that its critical tile owns the
+// registers):  base(r) = bvec ? bvec[r] : (r == jb ? 1 : 0);
+//              unew(r) = ucol ? ucol[r] : (r < j1 ? 0 : (r == j1 ? 1 : ux[r] * uscal)).
+struct RhsSpec {
+    const double *bvec, *ucol, *ux;
+    int64_t jb, j1;
+    double uscal;
+    __device__ __forceinline__ double base(int64_t r) const { return bvec ? __ldcg(bvec + r) : (r == jb ? 1.0 : 0.0); }
+    __device__ __forceinline__ double unew(int64_t r) const
+    {
+        return ucol ? __ldcg(ucol + r) : (r < j1 ? 0.0 : (r == j1 ? 1.0 : __ldcg(ux + r) * uscal));
+    }
+};
+__device__ __noinline__ void trsv4r(const PanelArgs &a, const RhsSpec rs, int k, const double *z2, unsigned epoch,
+                                    int64_t jcol)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, G = gridDim.x, bid = blockIdx.x;
+    unsigned long long *tt = (a.ttrace && jcol == a.tcol && tid == 0) ? a.ttrace : nullptr;  // HT_TRACE_COL
+    const int64_t n = a.n, p0 = a.s0 + 1, M = n - p0;
+    const int Nb = (int)((M + T4 - 1) / T4);
+    const int grp = tid >> 6, rr = 32 * ((tid >> 5) & 1) + lane;
+    double *ys = g_dyn;           // [T4] fetched y~_c
+    double *rhs = ys + T4;        // [T4] rhs_b
+    double *pw = rhs + T4;        // [NWP][T4] rhs partials / [3][8][64] fold
+    for (int u = bid; u < 4 * Nb; u += G) {
+        const int sb = u >> 2, q = u & 3, b = Nb - 1 - sb;
+        const int64_t rb0 = p0 + (int64_t)b * T4;
+        const int hb = (int)(n - rb0 < T4 ? n - rb0 : T4);
+        const int h = hb - 64 * q < 0 ? 0 : (hb - 64 * q > 64 ? 64 : hb - 64 * q);
+        if (h <= 0) continue;  // no rows: nothing to publish, consumers skip the slice
+        const int64_t r0 = rb0 + 64 * q;
+        unsigned long long *tu = tt ? tt + 8 * (size_t)(4 * b + q) : nullptr;
+        if (tu) tu[4] = gtime();
+        const double *rowp = a.Bt + bt4_row_offset(M, b) + 64 * q;  // columns from p0 + T4 (b+1), ld T4
+        const int wcrit = (b + 1 < Nb) ? (int)(M - (int64_t)T4 * (b + 1) < T4 ? M - (int64_t)T4 * (b + 1) : T4) : 0;
+        // (1) rhs_b = base - U z2 - unew z2(k) over the hb rows of block b: warps over columns,
+        //     lanes over rows, 4 columns x 8 row chunks of loads per batch
+        {
+            double acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+            for (int c0 = warp; c0 < k; c0 += NWP * 2) {
+                double uv[2][8];
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int c = c0 + NWP * t;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int r = 32 * j + lane;
+                        uv[t][j] = (c < k && r < hb) ? a.U[(size_t)c * n + rb0 + r] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int c = c0 + NWP * t;
+                    const double zc = c < k ? z2[c] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = fma(uv[t][j], zc, acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pw[warp * T4 + 32 * j + lane] = acc[j];
+            __syncthreads();
+            if (tid < T4) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < NWP; ++w) s += pw[w * T4 + tid];
+                const int64_t r = rb0 + tid;
+                rhs[tid] = (tid < hb) ? rs.base(r) - s - rs.unew(r) * z2[k] : 0.0;
+            }
+            __syncthreads();
+        }
+        // (2) this slice's rows of Dinv4_b rhs_b (half tiles: the critical tile holds 32 registers)
+        double cd = 0.0;
+#pragma unroll 1
+        for (int pf = 0; pf < 32 / TPART; ++pf) {
+            double t[TPART];
+            tile64_load_part(t, a.Dinv4 + (size_t)b * T4 * T4 + 64 * q, hb, h, tid, pf);
+            cd += tile64_dot_part(t, rhs, tid, pf);
+            asm volatile("" ::: "memory");
+        }
+        // (3) off-diagonal tiles c > b+1 as their solutions arrive (exponent per column group)
+        double acc = 0.0;
+        int E = 0;
+        for (int cb = Nb - 1; cb > b + 1; --cb) {
+            const int wc = (int)(M - (int64_t)T4 * cb < T4 ? M - (int64_t)T4 * cb : T4);
+            double t[32];  // the whole slice tile in flight (per-SM streaming bandwidth)
+            tile64_load(t, rowp + (size_t)T4 * (cb - b - 1) * T4, wc, h, tid);
+            fetch4r(a, p0, cb, wc, epoch, ys);
+            const int ec = g_sm.es4[grp >> 1];
+            const double tc = tile64_dot(t, ys, tid);
+            if (ec > E) {
+                acc *= pow2i(E - ec);
+                E = ec;
+            }
+            acc = fma(tc, pow2i(ec - E), acc);
+            __syncthreads();  // ys is reused
+        }
+        if (tu) tu[0] = gtime();
+        // (4) the critical tile (b, b+1): loaded after the streamed tiles (registers), before the
+        // wait for y~_{b+1}
+        if (b + 1 < Nb) {
+            double tcrit[32];
+            tile64_load(tcrit, rowp, wcrit, h, tid);
+            fetch4r(a, p0, b + 1, wcrit, epoch, ys);
+            if (tu) tu[1] = gtime();
+            const int ec = g_sm.es4[grp >> 1];
+            const double tc = tile64_dot(tcrit, ys, tid);
+            if (ec > E) {
+                acc *= pow2i(E - ec);
+                E = ec;
+            }
+            acc = fma(tc, pow2i(ec - E), acc);
+            if (tu) tu[5] = gtime() + (acc != acc);
+        }
+        // (5) fold the eight column groups: y~ = 2^Eall (cd 2^-Eall - sum acc 2^(E - Eall))
+        double *fa = pw, *fc = pw + 8 * 64;
+        int *fe = reinterpret_cast<int *>(pw + 16 * 64);
+        fa[grp * 64 + rr] = acc;
+        fc[grp * 64 + rr] = cd;
+        fe[grp * 64 + rr] = E;
+        __syncthreads();
+        if (tu) tu[6] = gtime();
+        double xv = 0.0;
+        int e = 0;
+        if (tid < 64) {
+            int Eall = 0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) Eall = max(Eall, fe[g * 64 + tid]);
+            double sa = 0.0, sc = 0.0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                sa = fma(fa[g * 64 + tid], pow2i(fe[g * 64 + tid] - Eall), sa);
+                sc += fc[g * 64 + tid];
+            }
+            xv = sc * pow2i(-Eall) - sa;
+            e = Eall;
+        }
+        if (tu) tu[3] = gtime();
+        // (6) overflow guard (reading R-Z8): a power-of-two rescale of the slice
+        const bool big = (tid < h) && !(fabs(xv) <= BIG);
+        int ex = 0;
+        if (__syncthreads_or(big)) {
+            double mx = (tid < h) ? fabs(xv) : 0.0;
+            mx = warp_max(mx);
+            if (lane == 0) g_sm.red[warp] = mx;
+            __syncthreads();
+            mx = fmax(g_sm.red[0], g_sm.red[1]);
+            if (!(mx <= BIG)) frexp(mx, &ex);
+            if (!isfinite(mx)) ex = 0;
+        }
+        if (tu) tu[7] = gtime();
+        // (7) publish: the rows (the chain's hand-over) first, then the slice exponent
+        if (tid < h) {
+            if (ex) xv = ldexp(xv, -ex);
+            ll_put(a.yll + 2 * (r0 + tid), xv, epoch);
+            a.vy[r0 + tid] = xv;
+        }
+        if (tid == 0) {
+            st_volatile64(a.yll_exp + 4 * b + q, ((unsigned long long)epoch << 32) | (unsigned)(e + ex));
+            a.bexp[4 * b + q] = e + ex;
+            if (tu) tu[2] = gtime();
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+}
+
 // After a completed solve (grid synced): Emax over all blocks.
 __device__ int trsv_emax(Ctx &C)
 {
@@ -1352,7 +1597,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
         __syncthreads();
         if (stc) C.trimv_sm<false>(Ssm, ku, g_sm.sv1, g_sm.sv3); else C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // z2 = S_{k+1} w, w(c) = U(j0+1, c)
         ++epoch;
-        if (a.solve4) trsv4(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch);
+        if (a.solve4 == 2) trsv4r(a, RhsSpec{nullptr, nullptr, a.vx, j0 + 1, j0 + 1, scal_u}, k, g_sm.sv3, epoch, j0);
+        else if (a.solve4) trsv4(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch);
         else trsv_blocked(C, [&](int64_t r) { return r == j0 + 1 ? 1.0 : 0.0; }, unew, k, g_sm.sv3, epoch, j0);
         grid.sync();
         mark(1);
@@ -1482,7 +1728,9 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             if (stc) C.trimv_sm<false>(Ssm, ku, g_sm.sv1, g_sm.sv3); else C.trimv<false>(Sget, ku, g_sm.sv1, g_sm.sv3);  // S_{k+1} (U^T r)
             ++epoch;
             // (vx now holds x, so the new column of U is read back from U(:, k), written in P2)
-            if (a.solve4)
+            if (a.solve4 == 2)
+                trsv4r(a, RhsSpec{a.vr, U + (size_t)k * n, nullptr, 0, 0, 0.0}, k, g_sm.sv3, epoch, -1);
+            else if (a.solve4)
                 trsv4(C, [&](int64_t r) { return __ldcg(&a.vr[r]); },
                       [&](int64_t r) { return __ldcg(&U[(size_t)k * n + r]); }, k, g_sm.sv3, epoch);
             else
@@ -1811,7 +2059,10 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         HT_CUDA_TRY(cudaStreamSynchronize(st));
         bool all = true;
         for (int b4 = 0; b4 < Nb4; ++b4) all = all && a->h_dsafe4[b4] != 0;
-        a->solve4 = all ? 1 : 0;
+        // the row-split solve (trsv4r, default) needs no clusters; HT_TRSV4_CLUSTER=1 (development)
+        // selects the 4-CTA cluster variant (trsv4)
+        static const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;
+        a->solve4 = all ? (cl4 ? 1 : 2) : 0;
     }
     if (a->solve4) {
         // Bt = Dinv4_b B(block b, blocks > b), block rows of T4 rows packed with ld T4
@@ -1843,10 +2094,10 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     // cooperative launch (grid barriers) in clusters of 2 CTAs (the solve hands blocks over
     // through distributed shared memory); the grid is even.  HT_PANEL_NOCLUSTER=1 (profiling
     // only: ncu cannot replay cooperative cluster launches) runs unpaired single CTAs.
-    const int csz = a->solve4 ? C4 : 2;
+    const int csz = a->solve4 == 1 ? C4 : 2;
     if (!nocl) {
         nblocks &= ~(csz - 1);
-        if (a->solve4 && nblocks > C4 * ncl4) nblocks = C4 * ncl4;
+        if (a->solve4 == 1 && nblocks > C4 * ncl4) nblocks = C4 * ncl4;
         if (nblocks < csz) nblocks = csz;
     }
     cudaLaunchConfig_t cfg = {};
