@@ -2014,7 +2014,10 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb4 = (int)((M + T4 - 1) / T4);
     a->solve4 = 0;
     int ncl4 = 0;
-    if (!no4 && !nocl && Nb4 >= 2 && a->Dinv4) {
+    static const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;
+    bool use4 = false;  // the 256-row solve is possible (trsv4r needs no clusters; trsv4 needs 4-CTA ones)
+    if (!no4 && Nb4 >= 2 && a->Dinv4 && !(cl4 && nocl)) use4 = true;
+    if (use4 && cl4) {
         cudaLaunchConfig_t oc = {};
         oc.gridDim = dim3((unsigned)(nblocks & ~(C4 - 1)));
         oc.blockDim = dim3(PNT);
@@ -2030,8 +2033,9 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
             cudaGetLastError();
             ncl4 = 0;
         }
+        use4 = ncl4 >= 2;
     }
-    if (ncl4 >= 2) {
+    if (use4) {
         inv4_assemble_kernel<<<Nb4, 256, 0, st>>>(a->Dinv, Nb, a->Dinv4);
         HT_CUDA_TRY(cudaGetLastError());
         std::vector<GemmBatchItem> g1, g2;
@@ -2061,7 +2065,6 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         for (int b4 = 0; b4 < Nb4; ++b4) all = all && a->h_dsafe4[b4] != 0;
         // the row-split solve (trsv4r, default) needs no clusters; HT_TRSV4_CLUSTER=1 (development)
         // selects the 4-CTA cluster variant (trsv4)
-        static const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;
         a->solve4 = all ? (cl4 ? 1 : 2) : 0;
     }
     if (a->solve4) {
