@@ -360,11 +360,7 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
 
 // HT_NO_WAVE=1 (development): factor the R1/L1 staircase chains window by window (one CTA)
 // instead of as a wavefront (ht_factor_run).
-static bool no_wave()
-{
-    static const bool v = getenv("HT_NO_WAVE") != nullptr;
-    return v;
-}
+static bool no_wave() { return getenv("HT_NO_WAVE") != nullptr; }  // read per call (tests toggle it)
 
 // Critical-stream phase profile (HT_PHASES=1, development only): the time between two
 // consecutive marks on the high-priority stream is charged to the later mark's phase.
@@ -853,7 +849,7 @@ struct Run {
             // group's Qhat and applies the group to B (R2, chain order) while st factors the
             // next group.  (One launch for the whole chain would leave B's R2 chain -- whose
             // top slab passes every window -- exposed after it.)
-            static const int grp_env = getenv("HT_WAVE_GROUP") ? atoi(getenv("HT_WAVE_GROUP")) : 0;
+            const int grp_env = getenv("HT_WAVE_GROUP") ? atoi(getenv("HT_WAVE_GROUP")) : 0;
             const int grp = grp_env > 0 ? grp_env : 16;
             for (int g0 = 0; g0 < r; g0 += grp) {
                 const int g1 = std::min(r, g0 + grp);

@@ -1976,7 +1976,7 @@ int ht_panel_max_blocks(int *nblocks_out)
 // HT_NO_L2PERSIST=1 (development) disables it.
 int ht_l2_persist_window(size_t bytes, size_t *win, float *hit)
 {
-    static const bool off = getenv("HT_NO_L2PERSIST") != nullptr;
+    const bool off = getenv("HT_NO_L2PERSIST") != nullptr;  // read per call (tests toggle it)
     *win = 0;
     *hit = 0.f;
     if (off) return 0;
@@ -2014,7 +2014,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     const int Nb4 = (int)((M + T4 - 1) / T4);
     a->solve4 = 0;
     int ncl4 = 0;
-    static const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;
+    const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;  // read per panel (tests toggle it)
     bool use4 = false;  // the 256-row solve is possible (trsv4r needs no clusters; trsv4 needs 4-CTA ones)
     if (!no4 && Nb4 >= 2 && a->Dinv4 && !(cl4 && nocl)) use4 = true;
     if (use4 && cl4) {

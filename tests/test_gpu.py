@@ -259,6 +259,39 @@ def test_streams_and_pipelining_match_one_stream_bitwise(monkeypatch):
         assert np.array_equal(M1, M2)
 
 
+@pytest.mark.parametrize("knob", ["HT_NO_WAVE", "HT_NO_L2PERSIST"])
+def test_scheduling_switches_are_bitwise_neutral(monkeypatch, knob):
+    """The wavefront factorization of the R1/L1 staircase chains (window i's panel b starts once
+    (i-1, b) and (i, b-1) are stored) and the L2-persisting panel workspace change only WHEN and
+    WHERE work runs, not its arithmetic: the outputs equal the window-by-window / plain-cache run
+    bit for bit (premature absorptions included)."""
+    A, B, _ = ht_inputs.config_pencil(3, n=1100)
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv(knob, "1")
+        out.append(gpu_reduce(A, B, nb=128, force_ir_fail=(300, 301))[:4])
+    for M1, M2 in zip(*out):
+        assert np.array_equal(M1, M2)
+
+
+def test_row_split_and_cluster_solves_agree(monkeypatch):
+    """trsv4r (the four 64-row slices of a 256-row block on four independent CTAs, default) and
+    trsv4 (column slices on a 4-CTA cluster combined by DSMEM, HT_TRSV4_CLUSTER=1) solve the same
+    recurrence with different summation orders: both match Oracle-T and each other to rounding."""
+    cfg, n = 3, 1300
+    A, B, _ = ht_inputs.config_pencil(cfg, n=n)
+    r1 = gpu_reduce(A, B, nb=128, force_ir_fail=(500,))
+    monkeypatch.setenv("HT_TRSV4_CLUSTER", "1")
+    r2 = gpu_reduce(A, B, nb=128, force_ir_fail=(500,))
+    Hr, Tr = oracle_T_cached(cfg, n)
+    for H, T, Q, Z, _ in (r1, r2):
+        check_props(A, B, H, T, Q, Z)
+        check_parity(A, B, H, T, Hr, Tr)
+    for x, y, nrm in zip(r1[:4], r2[:4], (C.fro(A), C.fro(B), 1.0, 1.0)):
+        assert np.max(np.abs(np.abs(x) - np.abs(y))) <= 1e-11 * nrm
+
+
 def test_chain_apply_measurement_hook():
     """ht_bench_chain_apply (bench.py's standalone roofline) runs the product kernel."""
     sec, fl = ht.ht_bench_chain_apply(1024, 128, 6, False, 2)
