@@ -46,8 +46,10 @@ struct ChainParams {
     ChainMat m[3];
     int nm;
     int h, cap;          // slab height, ring capacity (columns); both powers of two
-    const ChainWin *wins;
+    const ChainWin *wins;  // null: the windows are inl[0 .. nw) (launch parameters, nw <= 4)
     int nw;
+    ChainWin inl[4];
+    __device__ __forceinline__ ChainWin win(int i) const { return wins ? wins[i] : inl[i]; }
 };
 
 #ifdef CHAIN_PROF
@@ -196,14 +198,14 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
 
     {
         CPROF_T(t0);
-        const ChainWin w0 = P.wins[0];
+        const ChainWin w0 = P.win(0);
         load_cols(w0.o, (int64_t)w0.o + w0.p);
         zero_pad(w0.o, w0.p);
         CPROF_T(t1);
         CPROF_ADD(0, t0, t1);
     }
     for (int wi = 0; wi < P.nw; ++wi) {
-        const ChainWin W = P.wins[wi];
+        const ChainWin W = P.win(wi);
         const int p = W.p, pp = (p + 31) & ~31;
         const int64_t lo = W.lo[mi], hi = W.hi[mi];
         const bool active = (s0 < hi) && (s0 + hs > lo) && p > 0;
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
         const int64_t a0 = W.o, a1 = (int64_t)W.o + W.p;
         int64_t b0 = a1, b1 = a1;
         if (!last) {
-            const ChainWin N = P.wins[wi + 1];
+            const ChainWin N = P.win(wi + 1);
             b0 = N.o;
             b1 = (int64_t)N.o + N.p;
         }
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(CNT, 1) chain_apply_kernel(const __grid_consta
                 load_cols(b0 > a1 ? b0 : a1, b1);
             }
             __syncthreads();
-            const ChainWin N = P.wins[wi + 1];
+            const ChainWin N = P.win(wi + 1);
             zero_pad(N.o, N.p);
         } else {
             store_cols(a0 + direct, a1);
@@ -671,9 +673,13 @@ int ht_form_qhat(cudaStream_t st, int nw, double *const *Qw, const int *p, const
         hd[i] = BandDesc{Qw[i], p[i], 1, 1, 0, p[i], 0, p[i], q[i], V[i], p[i], T[i], q[i]};  // row-major Qhat
         pmax = std::max(pmax, p[i]);
     }
-    HT_CUDA_TRY(cudaMemcpyAsync(d_descs, hd, nw * sizeof(BandDesc), cudaMemcpyHostToDevice, st));
     const dim3 grid((unsigned)((pmax + 7) / 8), (unsigned)nw);
-    band_wy_kernel<<<grid, 256, band_smem(pmax), st>>>(reinterpret_cast<const BandDesc *>(d_descs), BandDesc{});
+    if (nw == 1) {  // by value: no host-to-device copy ahead of the kernel
+        band_wy_kernel<<<grid, 256, band_smem(pmax), st>>>(nullptr, hd[0]);
+    } else {
+        HT_CUDA_TRY(cudaMemcpyAsync(d_descs, hd, nw * sizeof(BandDesc), cudaMemcpyHostToDevice, st));
+        band_wy_kernel<<<grid, 256, band_smem(pmax), st>>>(reinterpret_cast<const BandDesc *>(d_descs), BandDesc{});
+    }
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -681,7 +687,8 @@ size_t ht_band_desc_size() { return sizeof(BandDesc); }
 
 // Apply a chain of explicit window transforms to up to 3 matrices (one launch).
 // d_wins: device array of nw windows (application order, monotone offsets).
-int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax, int maxgrid)
+int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax, int maxgrid,
+                   const ChainWin *h_wins)
 {
     if (nm <= 0 || nw <= 0) return 0;
     ChainParams P;
@@ -693,6 +700,10 @@ int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin
     if (pp <= 128) { P.cap = 128; P.h = 128; }
     P.wins = d_wins;
     P.nw = nw;
+    if (h_wins && nw <= 4) {  // by value: d_wins is not read
+        for (int i = 0; i < nw; ++i) P.inl[i] = h_wins[i];
+        P.wins = nullptr;
+    }
     int64_t nblk = 0;
     for (int i = 0; i < nm; ++i)
         if (mats[i].s_end > mats[i].s_begin) nblk += (mats[i].s_end - mats[i].s_begin + P.h - 1) / P.h;

@@ -13,6 +13,7 @@
 //         WY + one dense QR of the trailing m x m block of B).
 //   Remark 4: first right window has kt rows, k < kt <= 2k, k | (m-kt);
 //         restore chunks are aligned to the window boundaries.
+#include <cuda.h>  // green-context types only (the entry points are fetched at run time)
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -50,6 +51,10 @@ struct Work {
     size_t hot_bytes = 0;
     // wavefront factorization of staircase chains (ht_factor_run): epoch flags + ticket
     int *wave_flags = nullptr, *wave_ticket = nullptr;
+    bool green = false;  // sA, sQZ (and sA2, sQZ2: larger n) live in SM partitions (green contexts)
+    cudaStream_t sA2 = nullptr, sQZ2 = nullptr;
+    cudaStream_t side_a(int64_t n) const { return green && n >= 12288 ? sA2 : sA; }
+    cudaStream_t side_qz(int64_t n) const { return green && n >= 12288 ? sQZ2 : sQZ; }
     int wave_epoch = 0;
     unsigned long long *yll = nullptr, *yll_exp = nullptr;
     int *bexp = nullptr;
@@ -188,6 +193,48 @@ struct Timer {
 };
 
 
+// Side streams in an SM partition (green context, CUDA driver >= 12.4): the A/Q/Z window
+// applies run only on `nsm` SMs, so the critical stream's single-CTA factorizations, band
+// updates and sB's work always find free SMs (a factorization CTA needs a whole SM, and the
+// side kernels' CTAs run for milliseconds).  Entry points come from cudaGetDriverEntryPoint, so
+// the library has no link-time dependency on libcuda.  Returns false (caller keeps ordinary
+// streams) if green contexts are unavailable.
+static bool make_green_streams(int dev, int nsm, int priority, cudaStream_t *s1, cudaStream_t *s2)
+{
+    using GetRes = CUresult (*)(CUdevice, CUdevResource *, CUdevResourceType);
+    using Split = CUresult (*)(CUdevResource *, unsigned *, const CUdevResource *, CUdevResource *, unsigned, unsigned);
+    using GenDesc = CUresult (*)(CUdevResourceDesc *, CUdevResource *, unsigned);
+    using Create = CUresult (*)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned);
+    using SCreate = CUresult (*)(CUstream *, CUgreenCtx, unsigned, int);
+    void *f[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    const char *names[5] = {"cuDeviceGetDevResource", "cuDevSmResourceSplitByCount", "cuDevResourceGenerateDesc",
+                            "cuGreenCtxCreate", "cuGreenCtxStreamCreate"};
+    for (int i = 0; i < 5; ++i) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(names[i], &f[i], cudaEnableDefault, &q) != cudaSuccess || !f[i] ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    CUdevResource all, part, rem;
+    unsigned ng = 1;
+    CUdevResourceDesc desc;
+    CUgreenCtx g;
+    CUstream a, b;
+    if (((GetRes)f[0])((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+    if (nsm <= 0 || (unsigned)nsm >= all.sm.smCount) return false;
+    if (((Split)f[1])(&part, &ng, &all, &rem, 0, (unsigned)nsm) != CUDA_SUCCESS || ng < 1) return false;
+    if (((GenDesc)f[2])(&desc, &part, 1) != CUDA_SUCCESS) return false;
+    if (((Create)f[3])(&g, desc, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return false;
+    if (((SCreate)f[4])(&a, g, CU_STREAM_NON_BLOCKING, priority) != CUDA_SUCCESS ||
+        ((SCreate)f[4])(&b, g, CU_STREAM_NON_BLOCKING, priority) != CUDA_SUCCESS)
+        return false;
+    *s1 = (cudaStream_t)a;
+    *s2 = (cudaStream_t)b;
+    return true;
+}
+
 void work_free(Work &w)
 {
     w.U = w.V = w.Y = w.S = w.T = w.vec = w.BV = nullptr;  // carved out of w.hot
@@ -316,9 +363,16 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (!w.hp_stream) {
         int lo = 0, hi = 0;
         if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return HT_ECUDA;
+        // side streams (A; Q and Z) on an SM partition (green context; HT_NO_GREEN=1 or no
+        // green-context support: ordinary streams with capped grids).  Two partitions: 100 of
+        // 148 SMs below n = 12288, 120 above (the side work grows as n^3, the critical chains as
+        // n^2); HT_GREEN_SMS overrides both.
+        const int gsm = getenv("HT_GREEN_SMS") ? atoi(getenv("HT_GREEN_SMS")) : 0;
+        w.green = getenv("HT_NO_GREEN") == nullptr && make_green_streams(dev, gsm ? gsm : 100, lo, &w.sA, &w.sQZ) &&
+                  make_green_streams(dev, gsm ? gsm : 120, lo, &w.sA2, &w.sQZ2);
         if (cudaStreamCreateWithPriority(&w.hp_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
-            cudaStreamCreateWithPriority(&w.sA, cudaStreamNonBlocking, lo) != cudaSuccess ||
-            cudaStreamCreateWithPriority(&w.sQZ, cudaStreamNonBlocking, lo) != cudaSuccess ||
+            (!w.green && cudaStreamCreateWithPriority(&w.sA, cudaStreamNonBlocking, lo) != cudaSuccess) ||
+            (!w.green && cudaStreamCreateWithPriority(&w.sQZ, cudaStreamNonBlocking, lo) != cudaSuccess) ||
             cudaStreamCreateWithPriority(&w.sB, cudaStreamNonBlocking, hi) != cudaSuccess)
             return HT_ECUDA;
         if (cudaEventCreateWithFlags(&w.evF, cudaEventDisableTiming) != cudaSuccess ||
@@ -546,15 +600,17 @@ struct Run {
             maxp = std::max(maxp, fds[i].p);
             extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
         }
-        HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
+        // more than four descriptors go through device memory (<= 4 travel in the launch parameters)
+        const bool fbyval = nd <= 4 && getenv("HT_FACTOR_BYREF") == nullptr;
+        if (!fbyval) HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
         tm.begin(s, s == st ? 7 : 2);
         if (wave && nd > 1 && !no_wave()) {
             // flags are indexed by descriptor slot (fd_cur + i): distinct for concurrent chains
             const int ep = ++w->wave_epoch;
             TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp, w->wave_flags + (size_t)w->fd_cur * 8,
-                              w->wave_ticket + (sto.Vhat == w->Vhat ? 0 : 1), ep));
+                              w->wave_ticket + (sto.Vhat == w->Vhat ? 0 : 1), ep, fbyval ? hf : nullptr));
         } else {
-            TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp));
+            TRY(ht_factor_run(s, w->d_fd + w->fd_cur, nd, sto.fscr, maxp, nullptr, nullptr, 0, fbyval ? hf : nullptr));
         }
         tm.end(s);
         if (s == st) ph.mark(st, 8);
@@ -611,10 +667,11 @@ struct Run {
                 }
             }
         }
-        HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
+        const bool byval = nw <= 4 && getenv("HT_CHAIN_BYVAL") != nullptr;
+        if (!byval) HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
         tm.begin(s, 4);
         ++chain_launches;
-        int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid);
+        int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid, byval ? hc : nullptr);
         tm.end(s);
         w->cw_cur += nw;
         return rc;
@@ -740,7 +797,9 @@ struct Run {
     int side_grid() const  // CTAs of A's window applies while the critical chains run
     {
         static const int env = getenv("HT_SIDE_GRID") ? atoi(getenv("HT_SIDE_GRID")) : 0;
-        return env > 0 ? env : (n >= 12288 ? 96 : 56);
+        if (env > 0) return env;
+        if (w->green) return 0;  // the SM partition bounds them: full grids
+        return n >= 12288 ? 96 : 56;
     }
     int side_grid_qz() const  // the same for Q and Z
     {
@@ -753,7 +812,7 @@ struct Run {
         double *U = w->U, *V = w->V, *Y = w->Y, *S = w->S, *T = w->T;
         const bool serial = getenv("HT_SERIAL") != nullptr;  // debug: everything on st
         const int BATCH = getenv("HT_BATCH") ? atoi(getenv("HT_BATCH")) : 4;  // windows per side-stream apply
-        cudaStream_t sA = serial ? st : w->sA, sQ = serial ? st : w->sQZ;
+        cudaStream_t sA = serial ? st : w->side_a(n), sQ = serial ? st : w->side_qz(n);
         w->fd_cur = w->ld_cur = w->cw_cur = 0;
         TRY(dep(sA, st, 0));
         TRY(dep(sQ, st, 0));
@@ -1546,7 +1605,7 @@ int reduce_body(Run &R, const ht_options *opt)
 // makes every call fail).
 void drain(Work *w)
 {
-    cudaStream_t ss[] = {w->hp_stream, w->sA, w->sQZ, w->sB, w->side_stream};
+    cudaStream_t ss[] = {w->hp_stream, w->sA, w->sQZ, w->sB, w->side_stream, w->sA2, w->sQZ2};
     for (cudaStream_t s : ss)
         if (s) cudaStreamSynchronize(s);
 }

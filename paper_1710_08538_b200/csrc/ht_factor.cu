@@ -240,9 +240,14 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Up to four descriptors travel in the launch parameters (no host-to-device copy in the stream
+// ahead of the kernel: one fewer operation per window on the critical stream).
+struct FactorDescs4 {
+    FactorDesc d[4];
+};
 template <class L>
 __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *descs, int nd, double *gscratch,
-                                                             const WaveArgs wa)
+                                                             const WaveArgs wa, const __grid_constant__ FactorDescs4 inl)
 {
     constexpr int FNT = L::NT, FNW = L::NW, RPT = L::RPT, TPW = L::TPW;
     constexpr bool WIDE = L::WIDE;
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
         return s_ticket;
     };
     for (int di = next_window(-1); di < nd; di = next_window(di)) {
-        const FactorDesc d = descs[di];
+        const FactorDesc d = descs ? descs[di] : inl.d[di];
         const int p = d.p, q = d.q;
         // rows >= dense + c + 1 of view column c are exactly zero (staircase windows)
         const int dense = (d.dense > 0 && d.dense < p) ? d.dense : p;
@@ -890,7 +895,8 @@ __global__ void __launch_bounds__(L::NT, 1) factor_qr_kernel(const FactorDesc *d
 }
 
 template <class L>
-int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, const WaveArgs &wa, int grid)
+int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, const WaveArgs &wa, int grid,
+                  const FactorDescs4 &inl)
 {
     const int smem = L::DOUBLES * (int)sizeof(double);
     static std::mutex mu;
@@ -900,7 +906,7 @@ int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gs
         return 0;
     });
     if (rc) return rc;
-    factor_qr_kernel<L><<<grid, L::NT, smem, st>>>(d_descs, nd, gscratch, wa);
+    factor_qr_kernel<L><<<grid, L::NT, smem, st>>>(d_descs, nd, gscratch, wa, inl);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -919,9 +925,14 @@ int ht_factor_set_prof(unsigned long long *dev)
 }
 
 int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp, int *wave_flags,
-                  int *wave_ticket, int wave_epoch)
+                  int *wave_ticket, int wave_epoch, const FactorDesc *h_descs)
 {
     if (nd <= 0) return 0;
+    FactorDescs4 inl{};
+    if (h_descs && nd <= 4) {  // by value: d_descs is not read
+        for (int i = 0; i < nd; ++i) inl.d[i] = h_descs[i];
+        d_descs = nullptr;
+    }
     WaveArgs wa{nullptr, nullptr, 0};
     int grid = 1;
     if (wave_flags && nd > 1) {
@@ -929,8 +940,8 @@ int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gs
         HT_CUDA_TRY(cudaMemsetAsync(wave_ticket, 0, sizeof(int), st));
         grid = nd < HT_WAVE_CTAS ? nd : HT_WAVE_CTAS;
     }
-    if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch, wa, grid);
-    if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch, wa, grid);
-    if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch, wa, grid);
+    if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch, wa, grid, inl);
+    if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch, wa, grid, inl);
+    if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch, wa, grid, inl);
     return 4;  // HT_ENUMERIC: window taller than 512 rows (nb <= 256 guarantees p <= 512)
 }

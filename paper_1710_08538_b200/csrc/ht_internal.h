@@ -38,8 +38,10 @@ struct ChainWin {
     int p;
     int64_t lo[3], hi[3];
 };
+// maxgrid > 0: at most that many CTAs (they loop over the slabs).  h_wins (optional): the same
+// windows in host memory; with nw <= 4 they travel in the launch parameters (d_wins unread).
 int ht_chain_apply(cudaStream_t st, const ChainMat *mats, int nm, const ChainWin *d_wins, int nw, int pmax,
-                   int maxgrid = 0);  // maxgrid > 0: at most that many CTAs (they loop over the slabs)
+                   int maxgrid = 0, const ChainWin *h_wins = nullptr);
 // One window transform applied to a narrow band of slabs straight from its factors (no
 // explicit Qhat): on the slab view S(s, c) (element X[s + c*ld] for a right apply,
 // X[c + s*ld] for a left apply; s in [s0, s0+cnt), c in [0, p) offset by o)
@@ -58,8 +60,11 @@ size_t ht_band_desc_size();
 // are factored as a wavefront by HT_WAVE_CTAS persistent CTAs (ht_factor.cu): wave_flags holds
 // nd x 8 ints (epoch-valued, never reset), wave_ticket one int (zeroed on `st` here).
 constexpr int HT_WAVE_CTAS = 6;
+// h_descs (optional): the same descriptors in host memory; with nd <= 4 they are passed in the
+// launch parameters and d_descs is not read (no copy needed).
 int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gscratch, int maxp,
-                  int *wave_flags = nullptr, int *wave_ticket = nullptr, int wave_epoch = 0);
+                  int *wave_flags = nullptr, int *wave_ticket = nullptr, int wave_epoch = 0,
+                  const FactorDesc *h_descs = nullptr);
 int ht_factor_set_prof(unsigned long long *dev);
 
 // panel kernel (ht_panel.cu)
