@@ -909,9 +909,11 @@ struct Run {
             // next group.  (One launch for the whole chain would leave B's R2 chain -- whose
             // top slab passes every window -- exposed after it.)
             const int grp_env = getenv("HT_WAVE_GROUP") ? atoi(getenv("HT_WAVE_GROUP")) : 0;
+            // groups of 16; the last group is kept short (its B chain is exposed after it)
             const int grp = grp_env > 0 ? grp_env : 16;
-            for (int g0 = 0; g0 < r; g0 += grp) {
-                const int g1 = std::min(r, g0 + grp);
+            const int tail = grp_env > 0 ? 0 : std::min(r, 6);
+            for (int g0 = 0; g0 < r;) {
+                const int g1 = (g0 < r - tail) ? std::min(r - tail, g0 + grp) : r;
                 // a group's first window continues the chain: its input (the previous group's
                 // last R) is complete in stream order, so it needs no flag
                 std::vector<FactorDesc> fg(fds.begin() + g0, fds.begin() + g1);
@@ -919,6 +921,7 @@ struct Run {
                 std::vector<ChainWin> cg(wl.begin() + g0, wl.begin() + g1);
                 TRY(factor_and_form(fg, wg, main_store(), st, sBq, true));
                 TRY(chain_on(sBq, {ChainMat{B, ldb, 0, 0, n}}, cg, 0));
+                g0 = g1;
             }
             TRY(dep(st, sBq, 11));
         } else if (pipelined) {
