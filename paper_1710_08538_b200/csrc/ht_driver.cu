@@ -396,7 +396,7 @@ int work_get(int dev, int64_t n, int64_t nb, Work **out)
     if (cudaMallocHost((void **)&w.h_dsafe4, (size_t)(N / 256 + 2) * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
     w.ndesc = 4 * (N + 16);
     if (cudaMalloc((void **)&w.wave_flags, (size_t)w.ndesc * 8 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
-    if (cudaMalloc((void **)&w.wave_ticket, 2 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;
+    if (cudaMalloc((void **)&w.wave_ticket, 8 * sizeof(int)) != cudaSuccess) return HT_ENOMEM;  // [0,1] wave tickets, [2,3] sweep counters
     cudaMemset(w.wave_flags, 0, (size_t)w.ndesc * 8 * sizeof(int));
     w.wave_epoch = 0;
     w.ncw = 16 * (N + 16);  // chain windows: each window list is issued per stream (B; A; Q/Z)
@@ -1472,6 +1472,7 @@ int reduce_body(Run &R, const ht_options *opt)
             pa.dsafe4 = w->dsafe4; pa.h_dsafe4 = w->h_dsafe4;
             pa.ypartB = w->ypartB; pa.BV = w->BV; pa.vbx = vv + 7 * N;
             pa.hot = w->hot; pa.hot_bytes = w->hot_bytes;
+            pa.sweep_ctr = reinterpret_cast<unsigned *>(w->wave_ticket + 2);
             pa.tol = tolf * HT_U * nB; pa.max_ir = max_ir;
             pa.force_fail = w->d_force; pa.n_force_fail = nforce;
             pa.out = w->d_out;

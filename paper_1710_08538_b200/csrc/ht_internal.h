@@ -107,6 +107,7 @@ struct PanelArgs {
     double *ypartB;     // the same for B x
     double *BV;         // n x nb: B v_i of the panel's right reflectors (absolute row index)
     double *vbx;        // n-vector: B x of the current solve
+    unsigned *sweep_ctr;  // [2] fused-sweep item counters (alternating sweeps)
     void *hot;          // U, V, Y, BV, S, T, n-vectors: one allocation, L2-persisting for the panel
     size_t hot_bytes;
     int64_t *out;       // [0]=k done, [1]=failed, [2]=ir steps, [3]=ir extra columns, [4]=rescales, [5]=epoch used

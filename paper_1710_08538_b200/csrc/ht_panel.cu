@@ -1283,7 +1283,8 @@ __device__ void slab_sweep(Ctx &C, const double *X, int64_t ldx, int64_t r0, int
 // are dealt round-robin to the CTAs; inside an item every warp streams 16 columns with
 // 16-byte loads over all 256 rows (16 independent loads in flight per lane), so each
 // SM keeps ~128 KB of loads outstanding.  Item partial sums go to ypart[cc][r]
-// (cc = column chunk) and are added in a fixed order by tiled_sum2() after a grid sync
+// (cc = column chunk) and are added in a fixed order by tiled_sum2() after a grid sync;
+// the items of both mat-vecs are handed out dynamically (tiled_matvec2)
 // (deterministic).
 constexpr int TRT = 256, TCW = 256;
 struct TileGeom {
@@ -1321,14 +1322,14 @@ struct TileGeom {
     }
 };
 
+// One 256 x 256 item of a fused-sweep mat-vec (see tiled_matvec2).
 template <class VF>
-__device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf, double *yp)
+__device__ __forceinline__ void sweep_item(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf, double *yp,
+                                           int it)
 {
     double *red = g_dyn;               // [NWP][TRT]
     double *vs = g_dyn + NWP * TRT;    // [TCW]
     const bool vec = (ldx % 2) == 0;
-    const int nit = tg.items();
-    for (int it = C.bid; it < nit; it += C.G) {
         int rb, cc;
         tg.item(it, rb, cc);
         const int64_t r0 = tg.r_al + (int64_t)TRT * rb, c0 = tg.c_beg + (int64_t)TCW * cc;
@@ -1425,6 +1426,31 @@ __device__ void tiled_matvec(Ctx &C, const TileGeom &tg, const double *X, int64_
             for (int w = 0; w < NWP; ++w) t += red[w * TRT + C.tid];
             if (r < tg.r_end) yp[(size_t)cc * C.n + r] = t;
         }
+}
+
+// The fused sweep's two mat-vecs (A over A(s+1:n, j+1:n), B over the upper part of B) as one
+// pool of 256 x 256 items handed out by an atomic counter: a CTA takes its next item as it
+// finishes one (the next index is fetched while the current item streams), so the A/B split
+// and the last round no longer leave SMs idle (static round-robin did).  Partial sums go to
+// yp[cc][r] exactly as before: the result does not depend on which CTA took which item.
+// ctr: this sweep's counter (zeroed before the sweep, see the panel loop).
+template <class VF>
+__device__ void tiled_matvec2(Ctx &C, const TileGeom &ta, const double *XA, int64_t lda_, double *ypA, const TileGeom &tb,
+                              const double *XB, int64_t ldb_, double *ypB, VF vf, unsigned *ctr)
+{
+    const int na = ta.items(), nt = na + tb.items();
+    if (C.tid == 0) g_sm.ival[2] = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    int it = g_sm.ival[2];
+    while (it < nt) {
+        unsigned nxt = 0;
+        if (C.tid == 0) nxt = atomicAdd(ctr, 1u);  // in flight while this item streams
+        if (it < na) sweep_item(C, ta, XA, lda_, vf, ypA, it);
+        else sweep_item(C, tb, XB, ldb_, vf, ypB, it - na);
+        __syncthreads();  // every thread has read g_sm.ival[2]
+        if (C.tid == 0) g_sm.ival[2] = (int)nxt;
+        __syncthreads();
+        it = g_sm.ival[2];
     }
     __syncthreads();
 }
@@ -1494,6 +1520,8 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
     auto Tget = [&](int i, int c) -> double { return stc ? Tsm[c * (c + 1) / 2 + i] : T[(size_t)c * nb + i]; };
     unsigned epoch = a.epoch;
     int k = 0, failed = 0;
+    int nsweep = 0;  // sweeps so far: sweep s uses counter a.sweep_ctr[s & 1]
+    if (C.bid == 0 && C.tid == 0) a.sweep_ctr[0] = a.sweep_ctr[1] = 0u;  // grid barriers precede the first sweep
     long long ir_steps = 0, ir_cols = 0, rescales = 0;
     int ffi = 0;  // cursor into the forced-failure list
     const bool prof = a.ptime && C.bid == 0 && C.tid == 0;
@@ -1664,8 +1692,10 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             __syncthreads();
             if (k > 0) { if (stc) C.trimv_sm<false>(Tsm, k, g_sm.svx, g_sm.sv2); else C.trimv<false>(Tget, k, g_sm.svx, g_sm.sv2); }  // z = T V^T x
             mark(6);
-            tiled_matvec(C, tga, A, lda, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypart);
-            tiled_matvec(C, tgb, a.B, a.ldb, [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.ypartB);
+            if (C.bid == 0 && C.tid == 0) a.sweep_ctr[(nsweep + 1) & 1] = 0u;  // the next sweep's counter
+            tiled_matvec2(C, tga, A, lda, a.ypart, tgb, a.B, a.ldb, a.ypartB,
+                          [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.sweep_ctr + (nsweep & 1));
+            ++nsweep;
             grid.sync();
             mark(4);
             if (k > 0) C.rowgemv(a.BV, n, k, g_sm.sv2);  // (B V) z for own rows
