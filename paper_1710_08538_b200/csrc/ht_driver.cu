@@ -601,7 +601,7 @@ struct Run {
             extra_flops += 2.0 * x.q * (double)x.q * (x.p - x.q / 3.0) + x.q * (double)x.q * x.q / 3.0;
         }
         // more than four descriptors go through device memory (<= 4 travel in the launch parameters)
-        const bool fbyval = nd <= 4 && getenv("HT_FACTOR_BYREF") == nullptr;
+        const bool fbyval = nd <= 4;  // descriptors in the launch parameters (no copy ahead of the kernel)
         if (!fbyval) HT_CUDA_TRY(cudaMemcpyAsync(w->d_fd + w->fd_cur, hf, nd * sizeof(FactorDesc), cudaMemcpyHostToDevice, s));
         tm.begin(s, s == st ? 7 : 2);
         if (wave && nd > 1 && !no_wave()) {
@@ -667,11 +667,12 @@ struct Run {
                 }
             }
         }
-        const bool byval = nw <= 4 && getenv("HT_CHAIN_BYVAL") != nullptr;
-        if (!byval) HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
+        // (chain windows stay in device memory: passing them in the launch parameters made the side
+        // streams faster at the critical stream's expense before the SM partition, and is neutral with it)
+        HT_CUDA_TRY(cudaMemcpyAsync(w->d_cw + w->cw_cur, hc, nw * sizeof(ChainWin), cudaMemcpyHostToDevice, s));
         tm.begin(s, 4);
         ++chain_launches;
-        int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid, byval ? hc : nullptr);
+        int rc = ht_chain_apply(s, mats.data(), (int)mats.size(), w->d_cw + w->cw_cur, nw, pmax, maxgrid);
         tm.end(s);
         w->cw_cur += nw;
         return rc;
