@@ -246,7 +246,11 @@ HT_API const char *ht_strerror(int code);
 /* Library version: major*10000 + minor*100 + patch. */
 HT_API int ht_version(void);
 
-/* Release the cached device workspace of the current device. Returns HT_OK. */
+/* Release the cached device workspace of the current device. Returns HT_OK.
+ * Process-level state that persists (created once per device by the first call): the
+ * library's streams (the A and Q/Z side streams live in two green-context SM partitions of
+ * 100 and 120 SMs when the driver supports them) and the device's persisting-L2 limit
+ * (cudaLimitPersistingL2CacheSize, raised to at most 3/8 of L2 for the panel workspace). */
 HT_API int ht_release_workspace(void);
 
 /*
