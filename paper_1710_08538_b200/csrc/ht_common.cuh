@@ -65,6 +65,12 @@ struct GemmBatchItem {
 int ht_gemm(cudaStream_t st, char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
             const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
             int64_t ldc);
+// split-K for small outputs with a long K (e.g. the k x k spike U^T B): the K range
+// is cut into slices whose partial products go to `work` (>= slices * M * N doubles), then added
+// in slice order (deterministic).  Falls back to ht_gemm when the output alone fills the GPU.
+int ht_gemm_splitk(cudaStream_t st, char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                   const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                   int64_t ldc, double *work, int64_t work_doubles);
 // batched: items live in device memory (d_items), all with the same transposition
 int ht_gemm_batched(cudaStream_t st, char transA, char transB, const GemmBatchItem *d_items, int nitems,
                     int maxM, int maxN);

@@ -1065,7 +1065,12 @@ struct Run {
         HT_CUDA_TRY(cudaStreamWaitEvent(st, w->ev_join, 0));  // join the L1 staircase
         ph.mark(st, 4);
         // ===== L2: spike, chain on B, A, Q, W-updates =====
-        TRY(gemm('T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb));
+        {  // the k x k spike U^T B has a long K: split-K with W2 (free until the next GEMM) as slices
+            tm.begin(st, 1);
+            TRY(ht_gemm_splitk(st, 'T', 'N', k, k, n - p0, 1.0, U + p0, n, B + p0 + p0 * ldb, ldb, 0.0, w->W1, nb, w->W2,
+                               (int64_t)n * nb));
+            tm.end(st);
+        }
         TRY(gemm('T', 'N', k, k, k, 1.0, S, nb, w->W1, nb, 0.0, w->W2, nb));
         TRY(gemm('N', 'N', k, k, k, -1.0, U + p0, n, w->W2, nb, 1.0, B + p0 + p0 * ldb, ldb));
         TRY(zero_lower(n - p0, k, B + p0 + p0 * ldb, ldb, 0));

@@ -6,6 +6,7 @@
 // Note: sm_100a has no tcgen05 kind::f64; DMMA is the FP64 tensor path.
 #include "ht_common.cuh"
 #include <stdio.h>
+#include <algorithm>
 
 thread_local double g_ht_flops = 0.0;  // per calling thread: concurrent calls on different devices
 
@@ -142,6 +143,35 @@ __global__ void __launch_bounds__(NT) gemm_batched_kernel(const GemmBatchItem *i
                       it.diag_add);
 }
 
+// slice z of the K range: work[z] = A(:, K_z) B(K_z, :)  (M x N, column-major, ld M)
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NT) gemm_splitk_kernel(const double *A, int64_t lda, const double *B, int64_t ldb,
+                                                         double *work, int M, int N, int K, int kchunk)
+{
+    const int z = blockIdx.z;
+    const int64_t k0 = (int64_t)z * kchunk;
+    const int kc = (int)((int64_t)kchunk < K - k0 ? (int64_t)kchunk : K - k0);
+    const double *Az = TA ? A + k0 : A + k0 * lda;
+    const double *Bz = TB ? B + k0 * ldb : B + k0;
+    gemm_tile<TA, TB>(Az, lda, Bz, ldb, work + (size_t)z * M * N, M, M, N, kc, 1.0, 0.0, blockIdx.x * BM, blockIdx.y * BN);
+}
+
+// C = alpha * sum_z work[z] + beta * C, slices added in order z = 0, 1, ... (deterministic)
+__global__ void splitk_reduce_kernel(const double *__restrict__ work, int nz, int M, int N, double alpha, double beta,
+                                     double *C, int64_t ldc)
+{
+    const int64_t MN = (int64_t)M * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < nz; ++z) s += work[(size_t)z * MN + e];
+        const int64_t gm = e % M, gn = e / M;
+        double *cp = C + gn * ldc + gm;
+        double v = alpha * s;
+        if (beta != 0.0) v += beta * *cp;
+        *cp = v;
+    }
+}
+
 struct GemmBatch16 {
     GemmBatchItem it[16];
 };
@@ -183,6 +213,33 @@ int ht_gemm(cudaStream_t st, char transA, char transB, int64_t M, int64_t N, int
     else if (!ta && tb) gemm_kernel<false, true><<<grid, NT, 0, st>>>(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, alpha, beta);
     else if (ta && !tb) gemm_kernel<true, false><<<grid, NT, 0, st>>>(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, alpha, beta);
     else gemm_kernel<true, true><<<grid, NT, 0, st>>>(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, alpha, beta);
+    HT_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int ht_gemm_splitk(cudaStream_t st, char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                   const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                   double *work, int64_t work_doubles)
+{
+    if (M <= 0 || N <= 0) return 0;
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    // slices of >= 256 K, enough of them to give ~1 CTA per SM, bounded by the workspace
+    int64_t nz = std::min<int64_t>((K + 255) / 256, std::max<int64_t>(1, 148 / tiles));
+    nz = std::min<int64_t>(nz, work ? work_doubles / (M * N) : 0);
+    if (nz < 2) return ht_gemm(st, transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    const int kchunk = (int)(((K + nz - 1) / nz + 3) & ~(int64_t)3);
+    nz = (K + kchunk - 1) / kchunk;
+    g_ht_flops += 2.0 * (double)M * (double)N * (double)K;
+    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)nz);
+    const bool ta = (transA == 'T' || transA == 't'), tb = (transB == 'T' || transB == 't');
+    if (!ta && !tb) gemm_splitk_kernel<false, false><<<grid, NT, 0, st>>>(A, lda, B, ldb, work, (int)M, (int)N, (int)K, kchunk);
+    else if (!ta && tb) gemm_splitk_kernel<false, true><<<grid, NT, 0, st>>>(A, lda, B, ldb, work, (int)M, (int)N, (int)K, kchunk);
+    else if (ta && !tb) gemm_splitk_kernel<true, false><<<grid, NT, 0, st>>>(A, lda, B, ldb, work, (int)M, (int)N, (int)K, kchunk);
+    else gemm_splitk_kernel<true, true><<<grid, NT, 0, st>>>(A, lda, B, ldb, work, (int)M, (int)N, (int)K, kchunk);
+    HT_CUDA_TRY(cudaGetLastError());
+    const int64_t MN = M * N;
+    splitk_reduce_kernel<<<(unsigned)std::min<int64_t>((MN + 255) / 256, 148), 256, 0, st>>>(work, (int)nz, (int)M, (int)N,
+                                                                                            alpha, beta, C, ldc);
     HT_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -1878,47 +1878,91 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
 // safety flag: finite, max|inv| <= 2^200, and max|inv| * max|D| <= 4e3 (well-conditioned, so the
 // look-ahead block solve stays backward stable to ~4e3 u) (else the
 // panel uses the overflow-safe sequential substitution for that block).
-__global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
-                                                      double *Dinv, int *dsafe)
+constexpr int IDT = 512;                    // inv_diag_kernel threads: 128 rows x 4 column groups
+constexpr int TRI = TB * (TB + 1) / 2;      // packed upper triangle, P(i, j) = j (j + 1) / 2 + i
+__global__ void __launch_bounds__(IDT) inv_diag_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
+                                                       double *Dinv, int *dsafe)
 {
-    extern __shared__ __align__(16) double X[];  // TB x TB, column j = thread j
-    __shared__ double smax[2][TB / 32];
-    const int b = blockIdx.x, j = threadIdx.x;
+    // Column j of X = D^{-1} by back substitution on e_j (for l = j .. 0: x_l /= D_ll, then
+    // x_i -= D_il x_l for i < l), all columns in lock step over l: D and X as packed upper
+    // triangles in shared memory, thread (i, jg) owns row i of the columns j = jg mod 4, and
+    // row l of X (scaled) goes through a double-buffered row so each l costs one barrier.
+    // Every x_i(j) sees the same operations in the same order as the column-by-column
+    // substitution (bitwise the same inverse).
+    extern __shared__ __align__(16) double X[];
+    double *Dp = X, *Xp = X + TRI;
+    __shared__ double rowb[2][TB];
+    __shared__ double smax[2][IDT / 32];
+    const int b = blockIdx.x, tid = threadIdx.x, i = tid % TB, jg = tid / TB;
     const int64_t r0 = p0 + (int64_t)b * TB;
     const int h = (int)(n - r0 < TB ? n - r0 : TB);
     const double *D = B + r0 + r0 * ldb;
-    for (int i = 0; i < TB; ++i) X[j * TB + i] = (i == j && j < h) ? 1.0 : 0.0;
     double dmax = 0.0;
-    if (j < h) {
-        for (int i = 0; i <= j; ++i) dmax = fmax(dmax, fabs(D[(size_t)j * ldb + i]));
-        // column j of D^{-1}: column-oriented back substitution on e_j
-        double *x = X + j * TB;
-        for (int l = j; l >= 0; --l) {
-            const double xl = x[l] / D[(size_t)l * ldb + l];
-            x[l] = xl;
-            if (xl != 0.0)
-                for (int i = 0; i < l; ++i) x[i] -= D[(size_t)l * ldb + i] * xl;
+    for (int j = jg; j < TB; j += IDT / TB) {
+        if (i > j) continue;
+        double d = 0.0;
+        if (j < h) {
+            d = D[(size_t)j * ldb + i];
+            dmax = fmax(dmax, fabs(d));
+        }
+        Dp[j * (j + 1) / 2 + i] = d;
+        Xp[j * (j + 1) / 2 + i] = (i == j && j < h) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // row l of X: x_l(j) /= D_ll for the owned columns j >= l (run by the threads with i == l)
+    auto finish_row = [&](int l) {
+        const double dl = Dp[l * (l + 1) / 2 + l];
+        for (int j = l + ((jg - l) % 4 + 4) % 4; j < h; j += 4) {
+            const double x = Xp[j * (j + 1) / 2 + l] / dl;
+            Xp[j * (j + 1) / 2 + l] = x;
+            rowb[l & 1][j] = x;
+        }
+    };
+    if (h > 0 && i == h - 1) finish_row(h - 1);
+    for (int l = h - 1; l >= 1; --l) {
+        __syncthreads();
+        if (i < l) {
+            const double dil = Dp[l * (l + 1) / 2 + i];
+            const double *rl = rowb[l & 1];
+            int j = l + ((jg - l) % 4 + 4) % 4;
+            for (; j + 12 < h; j += 16) {  // four columns per round: loads ahead of the stores
+                double xl[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xl[u] = rl[j + 4 * u];
+                    xv[u] = Xp[(j + 4 * u) * (j + 4 * u + 1) / 2 + i];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (xl[u] != 0.0) Xp[(j + 4 * u) * (j + 4 * u + 1) / 2 + i] = xv[u] - dil * xl[u];
+            }
+            for (; j < h; j += 4) {
+                const double xl = rl[j];
+                if (xl != 0.0) Xp[j * (j + 1) / 2 + i] -= dil * xl;
+            }
+            if (i == l - 1) finish_row(l - 1);
         }
     }
+    __syncthreads();
     double imax = 0.0;
     bool fin = true;
-    for (int i = 0; i < TB; ++i) {
-        double v = X[j * TB + i];
+    double *out = Dinv + (size_t)b * TB * TB;
+    for (int j = jg; j < TB; j += IDT / TB) {
+        const double v = (i <= j) ? Xp[j * (j + 1) / 2 + i] : 0.0;
         if (!isfinite(v)) fin = false;
         imax = fmax(imax, fabs(v));
+        out[(size_t)j * TB + i] = v;
     }
     if (!fin) imax = INFINITY;
     double a1 = warp_max(imax), a2 = warp_max(dmax);
-    if ((j & 31) == 0) {
-        smax[0][j >> 5] = a1;
-        smax[1][j >> 5] = a2;
+    if ((tid & 31) == 0) {
+        smax[0][tid >> 5] = a1;
+        smax[1][tid >> 5] = a2;
     }
     __syncthreads();
-    double *out = Dinv + (size_t)b * TB * TB;
-    for (int i = 0; i < TB; ++i) out[j * TB + i] = X[j * TB + i];
-    if (j == 0) {
+    if (tid == 0) {
         double im = 0.0, dm = 0.0;
-        for (int w = 0; w < TB / 32; ++w) {
+        for (int w = 0; w < IDT / 32; ++w) {
             im = fmax(im, smax[0][w]);
             dm = fmax(dm, smax[1][w]);
         }
@@ -1930,39 +1974,56 @@ __global__ void __launch_bounds__(TB) inv_diag_kernel(const double *B, int64_t l
 // Dinv_2b+1 formed by two GEMMs afterwards; this kernel writes the diagonal quadrants and zeros
 // the rest (the lower-left quadrant doubles as the GEMMs' scratch and is zeroed again by
 // inv4_safety_kernel).
-__global__ void __launch_bounds__(256) inv4_assemble_kernel(const double *Dinv, int Nb, double *Dinv4)
+constexpr int I4T = 1024, I4U = 16;  // inv4 kernels: threads, elements per thread and round
+__global__ void __launch_bounds__(I4T) inv4_assemble_kernel(const double *__restrict__ Dinv, int Nb,
+                                                            double *__restrict__ Dinv4)
 {
     const int b4 = blockIdx.x, i0 = 2 * b4;
     double *D = Dinv4 + (size_t)b4 * T4 * T4;
-    for (int idx = threadIdx.x; idx < T4 * T4; idx += 256) {
-        const int r = idx % T4, c = idx / T4;
-        double v = 0.0;
-        if (r < TB && c < TB) v = Dinv[(size_t)i0 * TB * TB + (size_t)c * TB + r];
-        else if (r >= TB && c >= TB && i0 + 1 < Nb) v = Dinv[(size_t)(i0 + 1) * TB * TB + (size_t)(c - TB) * TB + (r - TB)];
-        D[idx] = v;
+    for (int base = 0; base < T4 * T4; base += I4T * I4U) {
+        double v[I4U];
+#pragma unroll
+        for (int u = 0; u < I4U; ++u) {  // all loads of a round in flight
+            const int idx = base + u * I4T + threadIdx.x, r = idx % T4, c = idx / T4;
+            v[u] = 0.0;
+            if (r < TB && c < TB) v[u] = Dinv[(size_t)i0 * TB * TB + (size_t)c * TB + r];
+            else if (r >= TB && c >= TB && i0 + 1 < Nb) v[u] = Dinv[(size_t)(i0 + 1) * TB * TB + (size_t)(c - TB) * TB + (r - TB)];
+        }
+#pragma unroll
+        for (int u = 0; u < I4U; ++u) D[base + u * I4T + threadIdx.x] = v[u];
     }
 }
 // Safety of each 256-row block (the criterion of inv_diag_kernel on the whole block) and the
 // final zeroing of the scratch quadrant.
-__global__ void __launch_bounds__(256) inv4_safety_kernel(const double *B, int64_t ldb, int64_t p0, int64_t n,
-                                                          double *Dinv4, const int *dsafe, int Nb, int *dsafe4)
+__global__ void __launch_bounds__(I4T) inv4_safety_kernel(const double *__restrict__ B, int64_t ldb, int64_t p0,
+                                                          int64_t n, double *__restrict__ Dinv4, const int *dsafe, int Nb,
+                                                          int *dsafe4)
 {
-    __shared__ double sm[2][8];
+    __shared__ double sm[2][I4T / 32];
     const int b4 = blockIdx.x, i0 = 2 * b4, tid = threadIdx.x;
     const int64_t r0 = p0 + (int64_t)b4 * T4;
     const int h = (int)(n - r0 < T4 ? n - r0 : T4);
     double *D = Dinv4 + (size_t)b4 * T4 * T4;
     double im = 0.0, dm = 0.0;
     bool fin = true;
-    for (int idx = tid; idx < T4 * T4; idx += 256) {
-        const int r = idx % T4, c = idx / T4;
-        if (r >= TB && c < TB) D[idx] = 0.0;  // scratch quadrant
-        else {
-            const double v = D[idx];
-            if (!isfinite(v)) fin = false;
-            im = fmax(im, fabs(v));
+    for (int base = 0; base < T4 * T4; base += I4T * I4U) {
+        double v[I4U], bv[I4U];
+#pragma unroll
+        for (int u = 0; u < I4U; ++u) {  // all loads of a round in flight
+            const int idx = base + u * I4T + tid, r = idx % T4, c = idx / T4;
+            v[u] = (r >= TB && c < TB) ? 0.0 : D[idx];
+            bv[u] = (r < h && c < h && r <= c) ? B[(size_t)(r0 + c) * ldb + r0 + r] : 0.0;
         }
-        if (r < h && c < h && r <= c) dm = fmax(dm, fabs(B[(size_t)(r0 + c) * ldb + r0 + r]));
+#pragma unroll
+        for (int u = 0; u < I4U; ++u) {
+            const int idx = base + u * I4T + tid, r = idx % T4, c = idx / T4;
+            if (r >= TB && c < TB) D[idx] = 0.0;  // scratch quadrant
+            else {
+                if (!isfinite(v[u])) fin = false;
+                im = fmax(im, fabs(v[u]));
+            }
+            dm = fmax(dm, fabs(bv[u]));
+        }
     }
     if (!fin) im = INFINITY;
     im = warp_max(im);
@@ -1974,7 +2035,7 @@ __global__ void __launch_bounds__(256) inv4_safety_kernel(const double *B, int64
     __syncthreads();
     if (tid == 0) {
         double a = 0.0, d = 0.0;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < I4T / 32; ++w) {
             a = fmax(a, sm[0][w]);
             d = fmax(d, sm[1][w]);
         }
@@ -1993,7 +2054,7 @@ int ht_panel_max_blocks(int *nblocks_out)
     HT_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      DYN_DOUBLES * (int)sizeof(double)));
     HT_CUDA_TRY(cudaFuncSetAttribute(inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     TB * TB * (int)sizeof(double)));
+                                     2 * TRI * (int)sizeof(double)));
     HT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, panel_kernel, PNT,
                                                               DYN_DOUBLES * sizeof(double)));
     if (per < 1) return 4;
@@ -2035,7 +2096,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
 {
     const int64_t M = a->n - a->s0 - 1;
     const int Nb = (int)((M + TB - 1) / TB);
-    inv_diag_kernel<<<Nb, TB, TB * TB * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
+    inv_diag_kernel<<<Nb, IDT, 2 * TRI * sizeof(double), st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv, a->dsafe);
     HT_CUDA_TRY(cudaGetLastError());
     // The 256-row solve on 4-CTA clusters (trsv4) when every 256-row diagonal block is safe
     // (decided on the host: one small copy per panel), else the 128-row paired solve.
@@ -2066,7 +2127,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
         use4 = ncl4 >= 2;
     }
     if (use4) {
-        inv4_assemble_kernel<<<Nb4, 256, 0, st>>>(a->Dinv, Nb, a->Dinv4);
+        inv4_assemble_kernel<<<Nb4, I4T, 0, st>>>(a->Dinv, Nb, a->Dinv4);
         HT_CUDA_TRY(cudaGetLastError());
         std::vector<GemmBatchItem> g1, g2;
         for (int b4 = 0; b4 < Nb4; ++b4) {
@@ -2087,7 +2148,7 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
             rc = ht_gemm_multi(st, 'N', 'N', g2.data(), (int)g2.size());
             if (rc) return rc;
         }
-        inv4_safety_kernel<<<Nb4, 256, 0, st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv4, a->dsafe, Nb, a->dsafe4);
+        inv4_safety_kernel<<<Nb4, I4T, 0, st>>>(a->B, a->ldb, a->s0 + 1, a->n, a->Dinv4, a->dsafe, Nb, a->dsafe4);
         HT_CUDA_TRY(cudaGetLastError());
         HT_CUDA_TRY(cudaMemcpyAsync(a->h_dsafe4, a->dsafe4, Nb4 * sizeof(int), cudaMemcpyDeviceToHost, st));
         HT_CUDA_TRY(cudaStreamSynchronize(st));
