@@ -913,7 +913,6 @@ int launch_factor(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gs
 
 using FWide128 = FactorSmem<256, 16, true>;   // p <= 128
 using FWide256 = FactorSmem<256, 32, true>;   // p <= 256
-using FWide256x = FactorSmem<512, 16, true>;  // p <= 256, 16 warps of 16 rows (HT_FACTOR512)
 using FLeaf512 = FactorSmem<512, 8, false>;   // p <= 512
 
 }  // namespace
@@ -942,8 +941,6 @@ int ht_factor_run(cudaStream_t st, const FactorDesc *d_descs, int nd, double *gs
         grid = nd < HT_WAVE_CTAS ? nd : HT_WAVE_CTAS;
     }
     if (maxp <= FWide128::MAXP) return launch_factor<FWide128>(st, d_descs, nd, gscratch, wa, grid, inl);
-    static const bool f512 = getenv("HT_FACTOR512") != nullptr;
-    if (f512 && maxp <= FWide256x::MAXP) return launch_factor<FWide256x>(st, d_descs, nd, gscratch, wa, grid, inl);
     if (maxp <= FWide256::MAXP) return launch_factor<FWide256>(st, d_descs, nd, gscratch, wa, grid, inl);
     if (maxp <= FLeaf512::MAXP) return launch_factor<FLeaf512>(st, d_descs, nd, gscratch, wa, grid, inl);
     return 4;  // HT_ENUMERIC: window taller than 512 rows (nb <= 256 guarantees p <= 512)
