@@ -1885,51 +1885,56 @@ __global__ void __launch_bounds__(IDT) inv_diag_kernel(const double *B, int64_t 
 {
     // Column j of X = D^{-1} by back substitution on e_j (for l = j .. 0: x_l /= D_ll, then
     // x_i -= D_il x_l for i < l), all columns in lock step over l: D and X as packed upper
-    // triangles in shared memory, thread (i, jg) owns row i of the columns j = jg mod 4, and
-    // row l of X (scaled) goes through a double-buffered row so each l costs one barrier.
+    // triangles in shared memory, thread (i, jg) owns row i of the columns j = jg mod 4 in the
+    // updates, and the scaled row l of X goes through a shared row (two barriers per l).
     // Every x_i(j) sees the same operations in the same order as the column-by-column
     // substitution (bitwise the same inverse).
     extern __shared__ __align__(16) double X[];
     double *Dp = X, *Xp = X + TRI;
-    __shared__ double rowb[2][TB];
+    __shared__ double rowl[TB];
     __shared__ double smax[2][IDT / 32];
     const int b = blockIdx.x, tid = threadIdx.x, i = tid % TB, jg = tid / TB;
     const int64_t r0 = p0 + (int64_t)b * TB;
     const int h = (int)(n - r0 < TB ? n - r0 : TB);
     const double *D = B + r0 + r0 * ldb;
     double dmax = 0.0;
-    for (int j = jg; j < TB; j += IDT / TB) {
-        if (i > j) continue;
-        double d = 0.0;
-        if (j < h) {
-            d = D[(size_t)j * ldb + i];
-            dmax = fmax(dmax, fabs(d));
+    {
+        constexpr int JU = TB / (IDT / TB);  // columns per thread: all loads before any store
+        double dv[JU];
+#pragma unroll
+        for (int u = 0; u < JU; ++u) {
+            const int j = jg + (IDT / TB) * u;
+            dv[u] = (i <= j && j < h) ? D[(size_t)j * ldb + i] : 0.0;
         }
-        Dp[j * (j + 1) / 2 + i] = d;
-        Xp[j * (j + 1) / 2 + i] = (i == j && j < h) ? 1.0 : 0.0;
+#pragma unroll
+        for (int u = 0; u < JU; ++u) {
+            const int j = jg + (IDT / TB) * u;
+            if (i > j) continue;
+            dmax = fmax(dmax, fabs(dv[u]));
+            Dp[j * (j + 1) / 2 + i] = dv[u];
+            Xp[j * (j + 1) / 2 + i] = (i == j && j < h) ? 1.0 : 0.0;
+        }
     }
     __syncthreads();
-    // row l of X: x_l(j) /= D_ll for the owned columns j >= l (run by the threads with i == l)
-    auto finish_row = [&](int l) {
+    // per l: (a) row l of X is final up to its scaling: x_l(j) /= D_ll for all j in [l, h), one
+    // column per thread (the divisions run in parallel), the scaled row also to rowl; (b) rank-1
+    // update of the rows i < l with it.  Two barriers per l.
+    for (int l = h - 1; l >= 0; --l) {
         const double dl = Dp[l * (l + 1) / 2 + l];
-        for (int j = l + ((jg - l) % 4 + 4) % 4; j < h; j += 4) {
+        for (int j = l + tid; j < h; j += IDT) {
             const double x = Xp[j * (j + 1) / 2 + l] / dl;
             Xp[j * (j + 1) / 2 + l] = x;
-            rowb[l & 1][j] = x;
+            rowl[j] = x;
         }
-    };
-    if (h > 0 && i == h - 1) finish_row(h - 1);
-    for (int l = h - 1; l >= 1; --l) {
         __syncthreads();
         if (i < l) {
             const double dil = Dp[l * (l + 1) / 2 + i];
-            const double *rl = rowb[l & 1];
             int j = l + ((jg - l) % 4 + 4) % 4;
             for (; j + 12 < h; j += 16) {  // four columns per round: loads ahead of the stores
                 double xl[4], xv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    xl[u] = rl[j + 4 * u];
+                    xl[u] = rowl[j + 4 * u];
                     xv[u] = Xp[(j + 4 * u) * (j + 4 * u + 1) / 2 + i];
                 }
 #pragma unroll
@@ -1937,13 +1942,12 @@ __global__ void __launch_bounds__(IDT) inv_diag_kernel(const double *B, int64_t 
                     if (xl[u] != 0.0) Xp[(j + 4 * u) * (j + 4 * u + 1) / 2 + i] = xv[u] - dil * xl[u];
             }
             for (; j < h; j += 4) {
-                const double xl = rl[j];
+                const double xl = rowl[j];
                 if (xl != 0.0) Xp[j * (j + 1) / 2 + i] -= dil * xl;
             }
-            if (i == l - 1) finish_row(l - 1);
         }
+        __syncthreads();
     }
-    __syncthreads();
     double imax = 0.0;
     bool fin = true;
     double *out = Dinv + (size_t)b * TB * TB;
