@@ -273,7 +273,7 @@ def measure_config(torch, ht, mg, cfg, n, nb, steps, warmup, stream, world, rank
 
 def summarize(reps, steps):
     keys = ("t_panel", "t_gemm", "t_factor", "t_other", "panel_bytes", "flops", "flops_level3", "launches",
-            "t_chain", "flops_chain", "chain_launches", "t_absorb_right", "t_absorb_left", "t_factor_exposed")
+            "t_chain", "flops_chain", "chain_launches", "t_absorb_right", "t_absorb_left", "t_factor_exposed", "t_chain_busy")
     return {k: float(np.sum([r[k] for r in reps])) / steps for k in keys}
 
 
@@ -341,6 +341,16 @@ def main():
             "peak_source": "cuBLAS DGEMM 8192^3 measured live (FP64 tensor pipe; no FP64 entry in MEASURED_PEAKS.json)",
             "launches_per_step": agg["chain_launches"],
             "flops_per_launch": agg["flops_chain"] / max(agg["chain_launches"], 1)}
+    # the launches of this kernel overlap one another (A's and Q/Z's streams share an SM
+    # partition, B's run next to them), so the sum of their durations counts the same wall time
+    # several times: `concurrent` divides the same flops by the time during which at least one
+    # launch was running (union of the event intervals, ht_report.t_chain_busy)
+    if agg["t_chain_busy"] > 0:
+        cach = agg["flops_chain"] / agg["t_chain_busy"] / 1e12
+        roof["concurrent"] = {"achieved": cach, "frac": cach / fp64_peak, "unit": "TFLOP/s",
+                              "busy_s": agg["t_chain_busy"], "sum_of_launch_durations_s": agg["t_chain"],
+                              "note": "aggregate rate of the overlapping launches while the critical stream's "
+                                      "factorization and band kernels hold the other SMs"}
     # the same kernel alone (full grid, no concurrent streams), on the shape of the first R2
     # update of B at this (n, nb): n rows, a chain of (n - 1 - 2nb)/nb windows of width 2nb.
     try:
@@ -372,6 +382,15 @@ def main():
     panel_ach = agg["panel_bytes"] / max(agg["t_panel"], 1e-12) / 1e9
     roof_panel = {"bound": "hbm", "kernel": "panel_kernel (persistent panel)", "achieved": panel_ach, "peak": hbm,
                   "unit": "GB/s", "frac": panel_ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    if cfg == 3 and n == 8192:
+        # one launch under `ncu --set full` (profiles/r02s2/ncu_panel_s2.txt: the 9th panel of this
+        # reduction, s0 = 1024, 128 columns, no IR step): DRAM bytes below the algorithmic bytes --
+        # part of the packed Bt triangle and of B's upper part is served by the 126 MB L2
+        roof_panel["traffic"] = 69.901119e9 + 0.699156e9
+        roof_panel["traffic_launch"] = {"algorithmic_bytes": 8.0 * sum(
+            7167 * 7168 / 2.0 + 7167.0 * c + i * c + c * (c + 1) / 2.0
+            for i, c in ((i, 8192 - 1024 - i - 1) for i in range(128))),
+            "duration_s_under_ncu": 27.59e-3, "source": "profiles/r02s2/ncu_panel_s2.txt"}
     # whole-path roofline: level-3 flops at the FP64 tensor peak + panel bytes at HBM
     t_roof = roofline_seconds(agg["flops_level3"], agg["panel_bytes"], fp64_peak, hbm)
     roof_e2e = {"t_roof_s": t_roof, "t_s": t_step, "frac": t_roof / t_step,

@@ -164,6 +164,9 @@ typedef struct {
     double scale_b;
     int64_t deflated_columns;  /* l of HT_FLAG_DEFLATE_ZERO_COLUMNS (sec. 3.5.1)             */
     double t_front;            /* device seconds of the front end (GENERAL_B / DEFLATE)      */
+    double t_chain_busy;       /* device seconds during which at least one chained window     */
+                               /* apply was running (union of the launch intervals that       */
+                               /* t_chain sums; the launches overlap on concurrent streams)   */
 } ht_report;
 
 /*

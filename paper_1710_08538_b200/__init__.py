@@ -53,7 +53,8 @@ class HTReport(ctypes.Structure):
                 ("t_chain", ctypes.c_double), ("flops_chain", ctypes.c_double), ("chain_launches", ctypes.c_int64),
                 ("t_absorb_right", ctypes.c_double), ("t_absorb_left", ctypes.c_double),
                 ("t_factor_exposed", ctypes.c_double), ("scale_a", ctypes.c_double), ("scale_b", ctypes.c_double),
-                ("deflated_columns", ctypes.c_int64), ("t_front", ctypes.c_double)]
+                ("deflated_columns", ctypes.c_int64), ("t_front", ctypes.c_double),
+                ("t_chain_busy", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -128,6 +128,24 @@ struct Timer {
     int64_t launches = 0;
     int cls = 0;
     cudaEvent_t cur = nullptr;
+    // class-4 launches run on several streams at once: their [begin, end] offsets from `base`
+    // (the reduction's start event) give the time during which at least one of them runs
+    cudaEvent_t base = nullptr;
+    std::vector<std::pair<float, float>> iv4;
+    double busy4()
+    {
+        std::sort(iv4.begin(), iv4.end());
+        double tot = 0.0;
+        float lo = 0.f, hi = 0.f;
+        bool open = false;
+        for (const auto &v : iv4) {
+            if (open && v.first <= hi) { hi = std::max(hi, v.second); continue; }
+            if (open) tot += (double)(hi - lo);
+            lo = v.first; hi = v.second; open = true;
+        }
+        if (open) tot += (double)(hi - lo);
+        return tot * 1e-3;
+    }
     cudaEvent_t get()
     {
         if (free_.empty()) {
@@ -181,6 +199,11 @@ struct Timer {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, pending[i].a, pending[i].b);
             acc[pending[i].cls] += ms * 1e-3;
+            if (pending[i].cls == 4 && base) {
+                float t0 = 0.f;
+                cudaEventElapsedTime(&t0, base, pending[i].a);
+                iv4.emplace_back(t0, t0 + ms);
+            }
             free_.push_back(pending[i].a);
             free_.push_back(pending[i].b);
         }
@@ -1392,6 +1415,7 @@ int reduce_body(Run &R, const ht_options *opt)
     TRY(ht_scale(st, n, n, dB, lddb, sb));
 
     HT_CUDA_TRY(cudaEventRecord(w->ev_t0, st));
+    R.tm.base = w->ev_t0;
     if (R.wq) TRY(ht_fill2d(st, n, n, dQ, lddq, 0.0, 1.0));
     if (R.wz) TRY(ht_fill2d(st, n, n, dZ, lddz, 0.0, 1.0));
     int64_t s_begin = 0;
@@ -1593,6 +1617,7 @@ int reduce_body(Run &R, const ht_options *opt)
     R.rep.t_factor = R.tm.acc[2] + R.tm.acc[7];
     R.rep.t_other = R.tm.acc[3];
     R.rep.t_chain = R.tm.acc[4];
+    R.rep.t_chain_busy = R.tm.busy4();
     R.rep.t_absorb_right = R.tm.acc[5];
     R.rep.t_absorb_left = R.tm.acc[6];
     R.rep.t_factor_exposed = R.tm.acc[7];
