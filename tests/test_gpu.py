@@ -180,6 +180,20 @@ def test_flop_accounting_within_15pct_of_model():
         assert 0.85 <= ratio <= 1.15, (cfg, n, nb, ratio)
 
 
+def test_report_times_are_consistent():
+    """ht_report timing fields (include/ht.h): the union of the chain-apply launch intervals
+    (t_chain_busy) is positive, no longer than their sum (t_chain; they overlap on concurrent
+    streams) and no longer than the reduction; the critical-stream spans fit in the reduction."""
+    A, B, _ = ht_inputs.config_pencil(3, n=1300)
+    *_, rep = gpu_reduce(A, B, nb=128)
+    eps = 1e-4
+    assert rep["chain_launches"] > 0 and rep["flops_chain"] > 0
+    assert 0.0 < rep["t_chain_busy"] <= rep["t_chain"] + eps
+    assert rep["t_chain_busy"] <= rep["seconds"] + eps
+    assert rep["t_panel"] + rep["t_absorb_right"] + rep["t_absorb_left"] <= rep["seconds"] + eps
+    assert rep["t_factor_exposed"] <= rep["t_factor"] + eps
+
+
 @pytest.mark.parametrize("sa,sb", [(1e200, 1.0), (1.0, 1e-200), (1e-200, 1e200), (1e300, 1e300)])
 def test_extreme_scaling_is_invariant(sa, sb):
     """Any finite pencil is accepted (include/ht.h "Range"): entries near 1e+-200 would
