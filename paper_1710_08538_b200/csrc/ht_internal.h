@@ -92,6 +92,7 @@ struct PanelArgs {
     double *Dinv4;
     int *dsafe4, *h_dsafe4;  // device / pinned host
     int solve4;
+    int sweep_res;      // fused sweep: items kept L2-resident (the rest is read evict-first); < 0: no hints
     int *bexp;          // trsv block exponents
     unsigned epoch;     // trsv flag epoch base
     double tol;         // 2 u ||B||_F

@@ -1325,7 +1325,7 @@ struct TileGeom {
 // One 256 x 256 item of a fused-sweep mat-vec (see tiled_matvec2).
 template <class VF>
 __device__ __forceinline__ void sweep_item(Ctx &C, const TileGeom &tg, const double *X, int64_t ldx, VF vf, double *yp,
-                                           int it)
+                                           int it, bool cs)
 {
     double *red = g_dyn;               // [NWP][TRT]
     double *vs = g_dyn + NWP * TRT;    // [TCW]
@@ -1355,7 +1355,7 @@ __device__ __forceinline__ void sweep_item(Ctx &C, const TileGeom &tg, const dou
                     const int64_t c = c0 + cw0 + u0 + u;
                     const double2 *col = reinterpret_cast<const double2 *>(X + (size_t)(c < tg.c_end ? c : c0) * ldx + r0);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[u][i] = col[C.lane + 32 * i];
+                    for (int i = 0; i < 4; ++i) xv[u][i] = cs ? __ldcs(col + C.lane + 32 * i) : col[C.lane + 32 * i];
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -1377,7 +1377,7 @@ __device__ __forceinline__ void sweep_item(Ctx &C, const TileGeom &tg, const dou
                     const int64_t c = c0 + cw0 + u0 + u;
                     const double2 *col = reinterpret_cast<const double2 *>(X + (size_t)(c < tg.c_end ? c : c0) * ldx + r0);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[u][i] = col[C.lane + 32 * i];
+                    for (int i = 0; i < 4; ++i) xv[u][i] = cs ? __ldcs(col + C.lane + 32 * i) : col[C.lane + 32 * i];
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -1436,7 +1436,7 @@ __device__ __forceinline__ void sweep_item(Ctx &C, const TileGeom &tg, const dou
 // ctr: this sweep's counter (zeroed before the sweep, see the panel loop).
 template <class VF>
 __device__ void tiled_matvec2(Ctx &C, const TileGeom &ta, const double *XA, int64_t lda_, double *ypA, const TileGeom &tb,
-                              const double *XB, int64_t ldb_, double *ypB, VF vf, unsigned *ctr)
+                              const double *XB, int64_t ldb_, double *ypB, VF vf, unsigned *ctr, int res)
 {
     const int na = ta.items(), nt = na + tb.items();
     if (C.tid == 0) g_sm.ival[2] = (int)atomicAdd(ctr, 1u);
@@ -1445,8 +1445,12 @@ __device__ void tiled_matvec2(Ctx &C, const TileGeom &ta, const double *XA, int6
     while (it < nt) {
         unsigned nxt = 0;
         if (C.tid == 0) nxt = atomicAdd(ctr, 1u);  // in flight while this item streams
-        if (it < na) sweep_item(C, ta, XA, lda_, vf, ypA, it);
-        else sweep_item(C, tb, XB, ldb_, vf, ypB, it - na);
+        // L2 residency (res >= 0): the first `res` items of the pool B-then-A keep the default
+        // policy and stay in the L2 from one column's sweep to the next (their rows are fixed
+        // for the panel, their columns move by one per step); all other items are read with the
+        // evict-first hint, so the stream does not push the resident ones out.
+        if (it < na) sweep_item(C, ta, XA, lda_, vf, ypA, it, res >= 0 && it >= res - (nt - na));
+        else sweep_item(C, tb, XB, ldb_, vf, ypB, it - na, res >= 0 && it - na >= res);
         __syncthreads();  // every thread has read g_sm.ival[2]
         if (C.tid == 0) g_sm.ival[2] = (int)nxt;
         __syncthreads();
@@ -1694,7 +1698,7 @@ __global__ void __launch_bounds__(PNT, 1) panel_kernel(const __grid_constant__ P
             mark(6);
             if (C.bid == 0 && C.tid == 0) a.sweep_ctr[(nsweep + 1) & 1] = 0u;  // the next sweep's counter
             tiled_matvec2(C, tga, A, lda, a.ypart, tgb, a.B, a.ldb, a.ypartB,
-                          [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.sweep_ctr + (nsweep & 1));
+                          [&](int64_t c) { return __ldcg(&a.vx[c]); }, a.sweep_ctr + (nsweep & 1), a.sweep_res);
             ++nsweep;
             grid.sync();
             mark(4);
@@ -2108,6 +2112,14 @@ int ht_panel_run(cudaStream_t st, PanelArgs *a, int nblocks)
     static const bool nocl = getenv("HT_PANEL_NOCLUSTER") != nullptr;
     const int Nb4 = (int)((M + T4 - 1) / T4);
     a->solve4 = 0;
+    {
+        // Fused sweep: a panel whose per-column stream (A block + B's upper part, ~1.5 M^2
+        // doubles) exceeds the L2 keeps only a fixed part of it resident (ht_panel.cu
+        // tiled_matvec2); HT_SWEEP_RES_MB sets that part (default 0: every item evict-first; < 0: no hints).
+        const char *e = getenv("HT_SWEEP_RES_MB");
+        const double mb = e ? atof(e) : 0.0;
+        a->sweep_res = mb < 0 ? -1 : (int)(mb * 1e6 / (8.0 * 256 * 256));
+    }
     int ncl4 = 0;
     const bool cl4 = getenv("HT_TRSV4_CLUSTER") != nullptr;  // read per panel (tests toggle it)
     bool use4 = false;  // the 256-row solve is possible (trsv4r needs no clusters; trsv4 needs 4-CTA ones)
