@@ -49,7 +49,7 @@ WORKLOAD = {
 
 from paper_1710_08538_b200.model import model_flops, roofline_seconds  # noqa: E402  (measurement logic)
 
-ENV_KNOBS = ("HT_NO_TRSV4", "HT_NO_GREEN", "HT_GREEN_SMS", "HT_TRSV4_CLUSTER", "HT_NO_L2PERSIST", "HT_NO_WAVE", "HT_WAVE_GROUP", "HT_SIDE_GRID_QZ", "HT_SERIAL", "HT_BATCH", "HT_SIDE_GRID", "HT_SB_GRID", "HT_PANEL_NOCLUSTER", "HT_PHASES",
+ENV_KNOBS = ("HT_NO_TRSV4", "HT_NO_GREEN", "HT_GREEN_SMS", "HT_TRSV4_CLUSTER", "HT_L2PERSIST", "HT_SWEEP_RES_MB", "HT_NO_WAVE", "HT_WAVE_GROUP", "HT_SIDE_GRID_QZ", "HT_SERIAL", "HT_BATCH", "HT_SIDE_GRID", "HT_SB_GRID", "HT_PANEL_NOCLUSTER", "HT_PHASES",
              "HT_PROFILE", "HT_DEBUG_IR", "HT_TRACE_COL", "HT_FPROF", "HT_SYNC_CHECK")
 
 

@@ -252,8 +252,9 @@ HT_API int ht_version(void);
 /* Release the cached device workspace of the current device. Returns HT_OK.
  * Process-level state that persists (created once per device by the first call): the
  * library's streams (the A and Q/Z side streams live in two green-context SM partitions of
- * 100 and 120 SMs when the driver supports them) and the device's persisting-L2 limit
- * (cudaLimitPersistingL2CacheSize, raised to at most 3/8 of L2 for the panel workspace). */
+ * 100 and 120 SMs when the driver supports them).  The device's persisting-L2 limit
+ * (cudaLimitPersistingL2CacheSize) is left alone unless the development switch HT_L2PERSIST=1
+ * is set (then raised to at most 3/8 of L2 for the panel workspace). */
 HT_API int ht_release_workspace(void);
 
 /*

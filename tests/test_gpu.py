@@ -273,17 +273,18 @@ def test_streams_and_pipelining_match_one_stream_bitwise(monkeypatch):
         assert np.array_equal(M1, M2)
 
 
-@pytest.mark.parametrize("knob", ["HT_NO_WAVE", "HT_NO_L2PERSIST"])
+@pytest.mark.parametrize("knob", ["HT_NO_WAVE", "HT_L2PERSIST", "HT_SWEEP_RES_MB"])
 def test_scheduling_switches_are_bitwise_neutral(monkeypatch, knob):
     """The wavefront factorization of the R1/L1 staircase chains (window i's panel b starts once
-    (i-1, b) and (i, b-1) are stored) and the L2-persisting panel workspace change only WHEN and
-    WHERE work runs, not its arithmetic: the outputs equal the window-by-window / plain-cache run
-    bit for bit (premature absorptions included)."""
+    (i-1, b) and (i, b-1) are stored), the (opt-in) L2-persisting panel workspace and the fused
+    sweep's evict-first cache hints (HT_SWEEP_RES_MB=-1: none) change only WHEN and WHERE work
+    runs, not its arithmetic: the outputs equal the window-by-window / plain-cache run bit for
+    bit (premature absorptions included)."""
     A, B, _ = ht_inputs.config_pencil(3, n=1100)
     out = []
     for off in (False, True):
         if off:
-            monkeypatch.setenv(knob, "1")
+            monkeypatch.setenv(knob, "-1" if knob == "HT_SWEEP_RES_MB" else "1")
         out.append(gpu_reduce(A, B, nb=128, force_ir_fail=(300, 301))[:4])
     for M1, M2 in zip(*out):
         assert np.array_equal(M1, M2)
