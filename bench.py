@@ -383,14 +383,15 @@ def main():
     roof_panel = {"bound": "hbm", "kernel": "panel_kernel (persistent panel)", "achieved": panel_ach, "peak": hbm,
                   "unit": "GB/s", "frac": panel_ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     if cfg == 3 and n == 8192:
-        # one launch under `ncu --set full` (profiles/r02s2/ncu_panel_s2.txt: the 9th panel of this
-        # reduction, s0 = 1024, 128 columns, no IR step): DRAM bytes below the algorithmic bytes --
-        # part of the packed Bt triangle and of B's upper part is served by the 126 MB L2
-        roof_panel["traffic"] = 69.901119e9 + 0.699156e9
+        # one launch under `ncu --set full` (profiles/r02s4/ncu_panel_s4.txt, scripts/gpu_s4_ncu_panel.sh:
+        # the 21st panel of this reduction, s0 = 2560, 128 columns, no IR step); before the sweep's
+        # evict-first reads the same launch moved 70.6 GB in 27.6 ms (profiles/r02s2/ncu_panel_s2.txt)
+        M21 = 8192 - 2560 - 1
+        roof_panel["traffic"] = 67.108145e9 + 0.092566e9
         roof_panel["traffic_launch"] = {"algorithmic_bytes": 8.0 * sum(
-            7167 * 7168 / 2.0 + 7167.0 * c + i * c + c * (c + 1) / 2.0
-            for i, c in ((i, 8192 - 1024 - i - 1) for i in range(128))),
-            "duration_s_under_ncu": 27.59e-3, "source": "profiles/r02s2/ncu_panel_s2.txt"}
+            M21 * (M21 + 1) / 2.0 + float(M21) * c + i * c + c * (c + 1) / 2.0
+            for i, c in ((i, 8192 - 2560 - i - 1) for i in range(128))),
+            "duration_s_under_ncu": 24.25e-3, "source": "profiles/r02s4/ncu_panel_s4.txt"}
     # whole-path roofline: level-3 flops at the FP64 tensor peak + panel bytes at HBM
     t_roof = roofline_seconds(agg["flops_level3"], agg["panel_bytes"], fp64_peak, hbm)
     roof_e2e = {"t_roof_s": t_roof, "t_s": t_step, "frac": t_roof / t_step,
