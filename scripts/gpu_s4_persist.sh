@@ -1,5 +1,6 @@
 #!/bin/bash
 # with the sweep's evict-first hints: is the persisting-L2 window of the panel workspace still worth it?
+# (run when the window was still the default and HT_NO_L2PERSIST switched it off; it is now opt-in: HT_L2PERSIST=1)
 mkdir -p gpurun_out
 out=gpurun_out/persist_ab.txt; : > $out
 for v in default nopersist default nopersist; do
